@@ -1,0 +1,156 @@
+/*
+ * relax_q4.h -- C-ABI of the B200-native fused q4f16 dequantize+matmul.
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, arXiv 2311.02103):
+ *
+ *     y[n, N] = x[n, K] . dequant(Wq[K, N])
+ *
+ * with "4-bit integer (int4) weight quantization and float16 activations"
+ * (P:640), the dequantize step fused into the matmul as one tensor program
+ * (FuseOps / FuseTensorIR), n a symbolic token count passed at run
+ * time while K and N are static per call site (call_tir "specializes to most
+ * static dimensions and only uses dynamic dimensions when necessary (like
+ * dimension n)"), called in destination-passing style -- the
+ * caller passes input and output memory explicitly (P:394-396,
+ * call_dps_library P:415-416) -- with any temporary workspace lifted out of
+ * the kernel into caller-planned memory sized from the upper
+ * bound of n.
+ *
+ * Storage format (the paper names int4 only; DESIGN.md §3 readings 1-4):
+ *   packed_w  uint32 [N][K/8]   8 unsigned 4-bit codes per word, element k at
+ *                               bits 4*(k mod 8) of word k/8 (low nibble first)
+ *   scales    fp16   [N][K/32]  one scale per 32 consecutive k
+ *   W(k, j) = fp16_RNE((q(k,j) - 7) * scales[j][k/32])      (zero point 7)
+ *   x         fp16   [n][K]     row-major
+ *   y         fp16   [n][N]     row-major; fp32 accumulation, one RNE rounding
+ * Every array is dense, IEEE binary16 where fp16, little-endian.
+ *
+ * Conventions shared by every entry point:
+ *   - Returns an int status (RELAX_OK == 0, codes below); never throws,
+ *     never aborts, never prints.
+ *   - All pointers except those named "host" are DEVICE pointers owned by
+ *     the caller; the library keeps none of them after return.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Work is enqueued asynchronously; the library never
+ *     synchronises the host, never allocates or frees device memory, so
+ *     every call can be captured into a CUDA graph.
+ *   - Inputs are never modified (DPS "inputs unmodified").
+ *   - Argument validation is O(1) and happens before any CUDA call; on any
+ *     error nothing is launched and y is untouched ("never a wrong answer",
+ *     S:629).
+ *   - Kernels are compiled for sm_100a (B200) only.
+ *   - Reentrant; the only global state is lazily initialised per-process
+ *     kernel attributes and the cuTensorMapEncodeTiled entry point.
+ */
+#ifndef RELAX_Q4_H
+#define RELAX_Q4_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RELAX_API __attribute__((visibility("default")))
+#else
+#define RELAX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum relax_status {
+    RELAX_OK = 0,
+    RELAX_ERR_INVALID_ARG = 1,       /* NULL pointer with work to do, n < 0, K <= 0, N <= 0 */
+    RELAX_ERR_UNSUPPORTED_SHAPE = 2, /* K not a multiple of 32, or a forced variant that cannot run it */
+    RELAX_ERR_MISALIGNED = 3,        /* a pointer is not 16-byte aligned */
+    RELAX_ERR_ALIAS = 4,             /* y (or w_out) overlaps an input or the workspace */
+    RELAX_ERR_WORKSPACE = 5,         /* ws_bytes smaller than the chosen schedule needs */
+    RELAX_ERR_DEVICE = 6,            /* no CUDA device, or current device is not sm_100 */
+    RELAX_ERR_CUDA = 7               /* a CUDA runtime call or launch failed */
+};
+
+/* Variants (the dispatch decision on n, "partial lowering" made at
+ * run time).  RELAX_VARIANT_AUTO lets the library choose. */
+enum relax_variant {
+    RELAX_VARIANT_AUTO = 0,
+    RELAX_VARIANT_GEMV = 1,   /* CUDA-core split-free GEMV, 128-bit loads, warp-shuffle reduce */
+    RELAX_VARIANT_TC = 2      /* TMA + tcgen05/TMEM GEMM with in-kernel dequant (K % 256 == 0) */
+};
+
+/* Flags for relax_q4_matmul_ex. */
+#define RELAX_FLAG_NO_PDL 1u  /* launch without programmatic dependent launch */
+
+/* Upper-bound workspace plan (lifted workspace P:438-441).
+ * Host only, pure: no CUDA call, no allocation.
+ *   n_max     largest token count the caller will pass (>= 0)
+ *   K, N      static shape of the weight
+ *   ws_bytes  out: max over n in [1, n_max] of the bytes the automatic
+ *             schedule of relax_q4_matmul_ws needs (0 when no n needs one)
+ * Guarantee: every relax_q4_matmul_ws call with n <= n_max and a workspace of
+ * at least *ws_bytes bytes succeeds (never RELAX_ERR_WORKSPACE).
+ * The workspace must be zero-filled before its first use; every call leaves
+ * it zero-filled again (its split-K tickets reset themselves), so one buffer
+ * serves any number of sequential calls.  Calls that may run concurrently
+ * need separate workspaces.
+ * Errors: RELAX_ERR_INVALID_ARG (ws_bytes NULL, n_max < 0, K <= 0, N <= 0),
+ *         RELAX_ERR_UNSUPPORTED_SHAPE (K % 32 != 0). */
+RELAX_API int relax_plan_workspace(int64_t n_max, int64_t K, int64_t N, size_t* ws_bytes);
+
+/* y = x . dequant(packed_w, scales), no workspace (schedules that need one
+ * are replaced by workspace-free ones).  n == 0 is a no-op (RELAX_OK).
+ *   x         device fp16 [n][K]
+ *   n         runtime token count (>= 0)
+ *   K, N      K % 32 == 0
+ *   packed_w  device uint32 [N][K/8];  scales device fp16 [N][K/32]
+ *   y         device fp16 [n][N] (output; must not overlap any input)
+ *   stream    cudaStream_t or NULL */
+RELAX_API int relax_q4_matmul(const void* x, int64_t n, int64_t K, int64_t N,
+                    const uint32_t* packed_w, const void* scales, void* y, void* stream);
+
+/* As relax_q4_matmul, plus a caller-provided device workspace (DPS: the
+ * lifted workspace is an extra output-position argument).
+ *   workspace  device memory of ws_bytes bytes, 16-byte aligned, zero-filled
+ *              before first use (see relax_plan_workspace); may be NULL when
+ *              ws_bytes == 0. */
+RELAX_API int relax_q4_matmul_ws(const void* x, int64_t n, int64_t K, int64_t N,
+                       const uint32_t* packed_w, const void* scales, void* y,
+                       void* workspace, size_t ws_bytes, void* stream);
+
+/* Explicit-schedule form, for parity tests of every variant and for benches.
+ *   variant   enum relax_variant (AUTO = same as relax_q4_matmul_ws)
+ *   split_k   TC only: split-K factor, 0 = choose; > 1 needs a workspace
+ *   bn        TC only: token tile in {16,32,64,128,256}, 0 = choose
+ *   flags     RELAX_FLAG_* bits
+ * Errors as relax_q4_matmul_ws, plus RELAX_ERR_UNSUPPORTED_SHAPE when the
+ * forced variant cannot run this shape (TC needs K % 256 == 0). */
+RELAX_API int relax_q4_matmul_ex(const void* x, int64_t n, int64_t K, int64_t N,
+                       const uint32_t* packed_w, const void* scales, void* y,
+                       void* workspace, size_t ws_bytes, int variant, int split_k,
+                       int bn, unsigned flags, void* stream);
+
+/* Host-only report of the schedule relax_q4_matmul_ws would use for (n,K,N):
+ * out pointers may be NULL.  variant: enum relax_variant; tile: GEMV tokens
+ * per launch or TC token tile; split_k: TC split factor; ws_bytes: bytes
+ * needed.  Errors: RELAX_ERR_INVALID_ARG, RELAX_ERR_UNSUPPORTED_SHAPE. */
+RELAX_API int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile,
+                         int* split_k, size_t* ws_bytes);
+
+/* Bit-exact dequant export: w_out[j][k] = fp16_RNE((q(k,j) - 7) * s), the
+ * producer half of the fused op on its own (used to pin the in-kernel
+ * dequant).
+ *   w_out   device fp16 [N][K] (output; must not overlap the inputs)
+ * Errors: as relax_q4_matmul (N == 0 is a no-op). */
+RELAX_API int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int64_t K, int64_t N,
+                     void* w_out, void* stream);
+
+/* Static description of a status code; never NULL. */
+RELAX_API const char* relax_status_str(int status);
+
+/* Library version string, e.g. "relax_q4 0.1 sm_100a". */
+RELAX_API const char* relax_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RELAX_Q4_H */

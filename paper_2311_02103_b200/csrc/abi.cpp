@@ -1,0 +1,272 @@
+// abi.cpp -- the C-ABI boundary (include/relax_q4.h): O(1) validation,
+// shape-specialised dispatch on the runtime token count n (P:409-413,
+// P:432-433), the upper-bound workspace plan, and the
+// launches.  No exceptions cross this boundary; nothing here allocates.
+#include "relax_q4.h"
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace rq4 {
+
+int gemv_max_n() {
+    static int v = [] {
+        const char* e = std::getenv("RELAX_Q4_GEMV_MAX_N");
+        if (e && *e) {
+            const int x = std::atoi(e);
+            if (x >= 0) return x;
+        }
+        return 4;   // measured crossover: DESIGN.md §6
+    }();
+    return v;
+}
+
+static int ctas_per_sm_tc(int bn) { return bn <= 64 ? 2 : 1; }
+
+static int choose_bn(int64_t n, int64_t N) {
+    if (n <= 16) return 16;
+    if (n <= 32) return 32;
+    if (n <= 64) return 64;
+    if (n <= 128) return 128;
+    const int64_t tm = (N + kTcBM - 1) / kTcBM;
+    if (n <= 256) return tm >= kNumSMs ? 256 : 128;
+    const int64_t t256 = tm * ((n + 255) / 256);
+    return t256 >= kNumSMs ? 256 : 128;
+}
+
+// Split-K factor that best fills whole waves of the machine (HBM-bound small
+// n); each split keeps >= 2 weight stages.
+static int choose_split(int64_t tiles, int kt, int bn) {
+    const int64_t slots = static_cast<int64_t>(kNumSMs) * ctas_per_sm_tc(bn);
+    if (tiles >= slots) return 1;
+    int best = 1;
+    double best_eff = 0.0;
+    const int smax = kt / 2 < 16 ? (kt / 2 < 1 ? 1 : kt / 2) : 16;
+    for (int s = 1; s <= smax; ++s) {
+        const int64_t ctas = tiles * s;
+        const int64_t waves = (ctas + slots - 1) / slots;
+        const double eff = static_cast<double>(ctas) / static_cast<double>(waves * slots);
+        if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+    }
+    return best;
+}
+
+int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split, int force_bn,
+              Plan* out) {
+    if (n < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
+    if (K % kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    Plan p;
+    const bool tc_ok = (K % kTcWStageK == 0);
+    int v = force_variant;
+    if (v == kVariantAuto) {
+        const int nt = static_cast<int>(n < kGemvMaxNT ? n : kGemvMaxNT);
+        if (n <= gemv_max_n() && gemv_fits(nt < 1 ? 1 : nt, K)) v = kVariantGemv;
+        else if (tc_ok) v = kVariantTc;
+        else v = kVariantGemv;
+    }
+    if (v == kVariantGemv) {
+        int nt = static_cast<int>(n < kGemvMaxNT ? n : kGemvMaxNT);
+        if (nt < 1) nt = 1;
+        while (nt > 1 && !gemv_fits(nt, K)) --nt;
+        if (!gemv_fits(nt, K)) return RELAX_ERR_UNSUPPORTED_SHAPE;
+        p.variant = kVariantGemv;
+        p.nt = nt;
+        p.ws_bytes = 0;
+    } else if (v == kVariantTc) {
+        if (!tc_ok) return RELAX_ERR_UNSUPPORTED_SHAPE;
+        p.variant = kVariantTc;
+        if (force_bn) {
+            if (force_bn != 16 && force_bn != 32 && force_bn != 64 && force_bn != 128 && force_bn != 256)
+                return RELAX_ERR_INVALID_ARG;
+            p.bn = force_bn;
+        } else {
+            p.bn = choose_bn(n, N);
+        }
+        const int kt = static_cast<int>(K / kTcWStageK);
+        const int64_t tiles = ((N + kTcBM - 1) / kTcBM) * ((n + p.bn - 1) / p.bn);
+        int s = force_split > 0 ? force_split : choose_split(tiles, kt, p.bn);
+        if (s > kt) s = kt;
+        if (s < 1) s = 1;
+        p.split = s;
+        p.ws_bytes = tc_workspace_bytes(n, N, p.bn, s);
+    } else {
+        return RELAX_ERR_INVALID_ARG;
+    }
+    *out = p;
+    return RELAX_OK;
+}
+
+// ---------------------------------------------------------------------------
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+    if (!a || !b || na == 0 || nb == 0) return false;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), b0 = reinterpret_cast<uintptr_t>(b);
+    return a0 < b0 + nb && b0 < a0 + na;
+}
+
+static int check_device() {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) {
+        cudaGetLastError();
+        return RELAX_ERR_DEVICE;
+    }
+    static std::mutex mu;
+    static int cc[64];           // 0 = unknown, else major*10+minor
+    if (dev >= 64) return RELAX_ERR_DEVICE;
+    int c;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        c = cc[dev];
+    }
+    if (c == 0) {
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return RELAX_ERR_DEVICE;
+        }
+        c = major * 10 + minor;
+        std::lock_guard<std::mutex> lk(mu);
+        cc[dev] = c;
+    }
+    return c == 100 ? RELAX_OK : RELAX_ERR_DEVICE;
+}
+
+static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
+                       const void* scales, void* y, void* ws, size_t ws_bytes, int variant,
+                       int split_k, int bn, unsigned flags, void* stream) {
+    if (n < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
+    if (K % kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if (variant < 0 || variant > 2 || split_k < 0) return RELAX_ERR_INVALID_ARG;
+    if (n == 0) return RELAX_OK;
+    if (!x || !packed_w || !scales || !y) return RELAX_ERR_INVALID_ARG;
+    if (ws_bytes > 0 && !ws) return RELAX_ERR_INVALID_ARG;
+    if (!aligned16(x) || !aligned16(packed_w) || !aligned16(scales) || !aligned16(y) ||
+        (ws && !aligned16(ws)))
+        return RELAX_ERR_MISALIGNED;
+    const size_t xb = static_cast<size_t>(n) * K * 2, yb = static_cast<size_t>(n) * N * 2;
+    const size_t wb = static_cast<size_t>(N) * K / 2, sb = static_cast<size_t>(N) * (K / kGroup) * 2;
+    if (overlap(y, yb, x, xb) || overlap(y, yb, packed_w, wb) || overlap(y, yb, scales, sb) ||
+        overlap(y, yb, ws, ws_bytes) || overlap(ws, ws_bytes, x, xb) ||
+        overlap(ws, ws_bytes, packed_w, wb) || overlap(ws, ws_bytes, scales, sb))
+        return RELAX_ERR_ALIAS;
+    Plan plan;
+    // Without a workspace the schedule is workspace-free (split-K = 1).
+    const int fs = (ws_bytes == 0 && split_k == 0) ? 1 : split_k;
+    int rc = make_plan(n, K, N, variant, fs, bn, &plan);
+    if (rc != RELAX_OK) return rc;
+    if (plan.ws_bytes > ws_bytes) return RELAX_ERR_WORKSPACE;
+    rc = check_device();
+    if (rc != RELAX_OK) return rc;
+    const bool pdl = (flags & RELAX_FLAG_NO_PDL) == 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int e;
+    if (plan.variant == kVariantGemv)
+        e = launch_gemv(static_cast<const uint16_t*>(x), n, K, N, packed_w,
+                        static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), plan.nt, pdl, st);
+    else
+        e = launch_tc(static_cast<const uint16_t*>(x), n, K, N, packed_w,
+                      static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), plan, ws, pdl, st);
+    if (e != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
+}  // namespace rq4
+
+extern "C" {
+
+int relax_plan_workspace(int64_t n_max, int64_t K, int64_t N, size_t* ws_bytes) {
+    if (!ws_bytes || n_max < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
+    if (K % rq4::kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    // Beyond this n every schedule has >= one full wave of tiles, so split-K
+    // (the only workspace user) is 1: the maximum is reached below it.
+    const int64_t n_cap = static_cast<int64_t>(rq4::kNumSMs) * 256;
+    const int64_t hi = n_max < n_cap ? n_max : n_cap;
+    size_t best = 0;
+    for (int64_t n = 1; n <= hi; ++n) {
+        rq4::Plan p;
+        const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p);
+        if (rc != RELAX_OK) return rc;
+        if (p.ws_bytes > best) best = p.ws_bytes;
+    }
+    *ws_bytes = best;
+    return RELAX_OK;
+}
+
+int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile, int* split_k,
+                         size_t* ws_bytes) {
+    rq4::Plan p;
+    const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p);
+    if (rc != RELAX_OK) return rc;
+    if (variant) *variant = p.variant;
+    if (tile) *tile = p.variant == rq4::kVariantGemv ? p.nt : p.bn;
+    if (split_k) *split_k = p.split;
+    if (ws_bytes) *ws_bytes = p.ws_bytes;
+    return RELAX_OK;
+}
+
+int relax_q4_matmul(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
+                    const void* scales, void* y, void* stream) {
+    return rq4::matmul_impl(x, n, K, N, packed_w, scales, y, nullptr, 0, 0, 0, 0, 0u, stream);
+}
+
+int relax_q4_matmul_ws(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
+                       const void* scales, void* y, void* workspace, size_t ws_bytes, void* stream) {
+    return rq4::matmul_impl(x, n, K, N, packed_w, scales, y, workspace, ws_bytes, 0, 0, 0, 0u, stream);
+}
+
+int relax_q4_matmul_ex(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
+                       const void* scales, void* y, void* workspace, size_t ws_bytes, int variant,
+                       int split_k, int bn, unsigned flags, void* stream) {
+    return rq4::matmul_impl(x, n, K, N, packed_w, scales, y, workspace, ws_bytes, variant, split_k,
+                            bn, flags, stream);
+}
+
+int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int64_t K, int64_t N,
+                     void* w_out, void* stream) {
+    if (K <= 0 || N < 0) return RELAX_ERR_INVALID_ARG;
+    if (K % rq4::kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if (N == 0) return RELAX_OK;
+    if (!packed_w || !scales || !w_out) return RELAX_ERR_INVALID_ARG;
+    if (!rq4::aligned16(packed_w) || !rq4::aligned16(scales) || !rq4::aligned16(w_out))
+        return RELAX_ERR_MISALIGNED;
+    const size_t ob = static_cast<size_t>(N) * K * 2;
+    if (rq4::overlap(w_out, ob, packed_w, static_cast<size_t>(N) * K / 2) ||
+        rq4::overlap(w_out, ob, scales, static_cast<size_t>(N) * (K / rq4::kGroup) * 2))
+        return RELAX_ERR_ALIAS;
+    const int rc = rq4::check_device();
+    if (rc != RELAX_OK) return rc;
+    const int e = rq4::launch_dequant(packed_w, static_cast<const uint16_t*>(scales), K, N,
+                                      static_cast<uint16_t*>(w_out), static_cast<cudaStream_t>(stream));
+    if (e != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
+const char* relax_status_str(int status) {
+    switch (status) {
+        case RELAX_OK: return "RELAX_OK";
+        case RELAX_ERR_INVALID_ARG: return "RELAX_ERR_INVALID_ARG: null pointer, negative n, or non-positive K/N";
+        case RELAX_ERR_UNSUPPORTED_SHAPE: return "RELAX_ERR_UNSUPPORTED_SHAPE: K % 32 != 0 or variant cannot run shape";
+        case RELAX_ERR_MISALIGNED: return "RELAX_ERR_MISALIGNED: pointer not 16-byte aligned";
+        case RELAX_ERR_ALIAS: return "RELAX_ERR_ALIAS: output overlaps an input or the workspace";
+        case RELAX_ERR_WORKSPACE: return "RELAX_ERR_WORKSPACE: workspace smaller than the schedule needs";
+        case RELAX_ERR_DEVICE: return "RELAX_ERR_DEVICE: no CUDA device or device is not sm_100";
+        case RELAX_ERR_CUDA: return "RELAX_ERR_CUDA: CUDA launch or runtime call failed";
+        default: return "RELAX_ERR_UNKNOWN";
+    }
+}
+
+const char* relax_version(void) { return "relax_q4 0.1 sm_100a"; }
+
+}  // extern "C"

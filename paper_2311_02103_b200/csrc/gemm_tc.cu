@@ -1,0 +1,367 @@
+// gemm_tc.cu -- the tensor-core path: fused q4f16 dequant + tcgen05 GEMM.
+//
+// y[t][j] = sum_k x[t][k] * W(k, j) with W = fp16_RNE((q-7) s), the
+// dequant producer fused into the matmul, specialised on the
+// static (K, N) with n a runtime argument, and split-K partials in
+// a caller-planned workspace (workspace lifting; upper-bound
+// planning).
+//
+// "Swap AB" mapping: MMA M = 128 weight rows (output
+// features), MMA N = BN tokens, K = 16 per instruction.
+//   warp 0   W producer : TMA of packed codes (128 rows x 128 B, SW128) and
+//                         scales (128 rows x 16 B) per 256-k stage
+//   warp 2   x producer : TMA of x (BN rows x 64 k, SW128) per 64-k sub-block;
+//                         out-of-range tokens / k are zero-filled by TMA
+//   warps 4-7 transform : thread m owns weight row m (= TMEM lane m); reads its
+//                         row's codes from SMEM, dequantises bit-exactly to
+//                         fp16 in registers and writes the A operand straight
+//                         into TMEM (tcgen05.st 32x32b) -- A never touches HBM
+//                         or SMEM in fp16
+//   warp 1   MMA issuer : one thread issues tcgen05.mma.kind::f16 with A from
+//                         TMEM, B (x) from SMEM, fp32 D in TMEM
+//   warps 4-7 epilogue  : tcgen05.ld of D, fp32 -> fp16 RNE, store y; with
+//                         split-K, fp32 partials go to the workspace and the
+//                         last CTA of a tile (atomic ticket) sums them in fixed
+//                         split order -> deterministic.
+#include <cuda.h>
+#include <cstdio>
+#include "internal.h"
+#include "ptx.cuh"
+#include "q4_unpack.cuh"
+
+namespace rq4 {
+
+constexpr int kTcThreads = 256;
+constexpr int kWStages = 4;            // 256-k codes+scales stages in flight
+constexpr int kAStages = 4;            // 64-k x / A sub-blocks in flight
+constexpr uint32_t kCodesStageBytes = kTcBM * (kTcWStageK / 2);     // 16 KB
+constexpr uint32_t kScalesStageBytes = kTcBM * (kTcWStageK / kGroup) * 2;  // 2 KB
+
+struct TcArgs {
+    int64_t n, K, N;
+    uint16_t* y;
+    float* part;          // [split][n][N] fp32 partials (split > 1)
+    uint32_t* cnt;        // [tiles_m * tiles_n] tickets, zero between calls
+    int split;
+    int kt;               // number of 256-k W stages covering K
+};
+
+template <int BN>
+struct TcCfg {
+    static constexpr uint32_t kXStageBytes = BN * 128;
+    static constexpr uint32_t kA0 = (BN < 32 ? 32 : BN);                   // TMEM col of A ring
+    static constexpr uint32_t kColsNeeded = kA0 + kAStages * 32;
+    static constexpr uint32_t kTmemCols = kColsNeeded <= 32 ? 32 : kColsNeeded <= 64 ? 64
+                                        : kColsNeeded <= 128 ? 128 : kColsNeeded <= 256 ? 256 : 512;
+    static constexpr uint32_t kOffCodes = 0;
+    static constexpr uint32_t kOffScales = kOffCodes + kWStages * kCodesStageBytes;
+    static constexpr uint32_t kOffX = kOffScales + kWStages * kScalesStageBytes;
+    static constexpr uint32_t kOffBar = kOffX + kAStages * kXStageBytes;
+    static constexpr uint32_t kNumBars = 2 * kWStages + 2 * kAStages + 1;
+    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kTcThreads, 1)
+tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
+             const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TcArgs a) {
+    using Cfg = TcCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-B alignment for the 128B-swizzle atoms.
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* codes_sm = smem + Cfg::kOffCodes;
+    uint8_t* scales_sm = smem + Cfg::kOffScales;
+    uint8_t* x_sm = smem + Cfg::kOffX;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
+    uint64_t* w_full = bars;
+    uint64_t* w_empty = bars + kWStages;
+    uint64_t* ax_full = bars + 2 * kWStages;
+    uint64_t* ax_empty = bars + 2 * kWStages + kAStages;
+    uint64_t* acc_full = bars + 2 * kWStages + 2 * kAStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
+    uint32_t* flag_slot = tmem_slot + 1;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kTcBM;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BN;
+    const int z = blockIdx.z;
+    const int ks0 = static_cast<int>(static_cast<int64_t>(z) * a.kt / a.split);
+    const int ks1 = static_cast<int>(static_cast<int64_t>(z + 1) * a.kt / a.split);
+    const int nst = ks1 - ks0;              // >= 1 (split <= kt)
+    const int nsub = nst * (kTcWStageK / kTcXStageK);
+
+    pdl_launch_dependents();
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 4); }
+        for (int i = 0; i < kAStages; ++i) { mbar_init(&ax_full[i], 1 + 4); mbar_init(&ax_empty[i], 1); }
+        mbar_init(acc_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_w);
+        tma_prefetch_desc(&tm_s);
+        tma_prefetch_desc(&tm_x);
+    }
+    if (warp == 3) {
+        tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- W producer (weights never depend on the previous kernel)
+        if (elect_one()) {
+            const uint64_t pol = policy_evict_first();
+            for (int i = 0; i < nst; ++i) {
+                const int slot = i % kWStages;
+                const uint32_t ph = (i / kWStages) & 1;
+                mbar_wait(&w_empty[slot], ph ^ 1);
+                mbar_arrive_expect_tx(&w_full[slot], kCodesStageBytes + kScalesStageBytes);
+                const int kb = ks0 + i;
+                tma_load_2d(codes_sm + slot * kCodesStageBytes, &tm_w, &w_full[slot],
+                            kb * (kTcWStageK / 2), static_cast<int32_t>(m0), pol);
+                tma_load_2d(scales_sm + slot * kScalesStageBytes, &tm_s, &w_full[slot],
+                            kb * (kTcWStageK / kGroup), static_cast<int32_t>(m0), pol);
+            }
+        }
+    } else if (warp == 2) {
+        // ---------------- x producer
+        if (elect_one()) {
+            pdl_wait();
+            const uint64_t pol = policy_evict_last();
+            for (int j = 0; j < nsub; ++j) {
+                const int slot = j % kAStages;
+                const uint32_t ph = (j / kAStages) & 1;
+                mbar_wait(&ax_empty[slot], ph ^ 1);
+                mbar_arrive_expect_tx(&ax_full[slot], Cfg::kXStageBytes);
+                const int32_t k = (ks0 * (kTcWStageK / kTcXStageK) + j) * kTcXStageK;
+                tma_load_2d(x_sm + slot * Cfg::kXStageBytes, &tm_x, &ax_full[slot], k,
+                            static_cast<int32_t>(n0), pol);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (elect_one()) {
+            constexpr uint32_t idesc = idesc_f16_f32(kTcBM, BN);
+            for (int j = 0; j < nsub; ++j) {
+                const int slot = j % kAStages;
+                const uint32_t ph = (j / kAStages) & 1;
+                mbar_wait(&ax_full[slot], ph);
+                tc_fence_after();
+                const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + slot * Cfg::kXStageBytes));
+#pragma unroll
+                for (int kk = 0; kk < kTcXStageK / 16; ++kk) {
+                    tc_mma_ts(tmem_base, tmem_base + Cfg::kA0 + slot * 32 + kk * 8,
+                              bdesc + static_cast<uint64_t>(kk * 2),  // +32 B along K in the atom
+                              idesc, (j | kk) != 0 ? 1u : 0u);
+                }
+                tc_commit(&ax_empty[slot]);
+            }
+            tc_commit(acc_full);
+        }
+    } else if (warp >= 4) {
+        // ---------------- transform: dequantise row m into the TMEM A ring
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        for (int i = 0; i < nst; ++i) {
+            const int ws = i % kWStages;
+            mbar_wait(&w_full[ws], (i / kWStages) & 1);
+            const uint8_t* crow = codes_sm + ws * kCodesStageBytes + m * 128;
+            const uint4 sv = *reinterpret_cast<const uint4*>(scales_sm + ws * kScalesStageBytes + m * 16);
+            const uint32_t sw[4] = {sv.x, sv.y, sv.z, sv.w};     // 8 scales, 2 per word
+#pragma unroll
+            for (int sub = 0; sub < kTcWStageK / kTcXStageK; ++sub) {
+                const int j = i * (kTcWStageK / kTcXStageK) + sub;
+                const int as = j % kAStages;
+                const uint4 c0 = *reinterpret_cast<const uint4*>(crow + (((2 * sub) ^ (m & 7)) << 4));
+                const uint4 c1 = *reinterpret_cast<const uint4*>(crow + (((2 * sub + 1) ^ (m & 7)) << 4));
+                const __half s_lo = __ushort_as_half(lo16(sw[sub]));   // group 2*sub
+                const __half s_hi = __ushort_as_half(hi16(sw[sub]));   // group 2*sub+1
+                const __half2 s2a = __halves2half2(s_lo, s_lo);
+                const __half2 s2b = __halves2half2(s_hi, s_hi);
+                uint32_t v[32];
+                {
+                    uint32_t o[4];
+                    dequant_word_natural(c0.x, s2a, o); v[0] = o[0]; v[1] = o[1]; v[2] = o[2]; v[3] = o[3];
+                    dequant_word_natural(c0.y, s2a, o); v[4] = o[0]; v[5] = o[1]; v[6] = o[2]; v[7] = o[3];
+                    dequant_word_natural(c0.z, s2a, o); v[8] = o[0]; v[9] = o[1]; v[10] = o[2]; v[11] = o[3];
+                    dequant_word_natural(c0.w, s2a, o); v[12] = o[0]; v[13] = o[1]; v[14] = o[2]; v[15] = o[3];
+                    dequant_word_natural(c1.x, s2b, o); v[16] = o[0]; v[17] = o[1]; v[18] = o[2]; v[19] = o[3];
+                    dequant_word_natural(c1.y, s2b, o); v[20] = o[0]; v[21] = o[1]; v[22] = o[2]; v[23] = o[3];
+                    dequant_word_natural(c1.z, s2b, o); v[24] = o[0]; v[25] = o[1]; v[26] = o[2]; v[27] = o[3];
+                    dequant_word_natural(c1.w, s2b, o); v[28] = o[0]; v[29] = o[1]; v[30] = o[2]; v[31] = o[3];
+                }
+                mbar_wait(&ax_empty[as], ((j / kAStages) & 1) ^ 1);
+                tc_fence_after();
+                tmem_st_32x32b_x32(tmem_base + lane_base + Cfg::kA0 + as * 32, v);
+                tc_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ax_full[as]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&w_empty[ws]);
+        }
+
+        // ---------------- epilogue
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+        pdl_wait();
+        const int64_t row = m0 + m;
+        const bool row_ok = row < a.N;
+        const bool split = a.split > 1;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld_32x32b_x16(tmem_base + lane_base + c0, v);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int64_t tok = n0 + c0 + i;
+                if (row_ok && tok < a.n) {
+                    const float f = __uint_as_float(v[i]);
+                    if (split) a.part[(static_cast<int64_t>(z) * a.n + tok) * a.N + row] = f;
+                    else a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(f));
+                }
+            }
+        }
+        if (split) {
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (warp == 4 && lane == 0) {
+                const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;
+                const uint32_t old = atomicInc(a.cnt + tile, static_cast<uint32_t>(a.split - 1));
+                *flag_slot = (old == static_cast<uint32_t>(a.split - 1)) ? 1u : 0u;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (*flag_slot) {
+                __threadfence();
+                if (row_ok) {
+                    for (int c = 0; c < BN; ++c) {
+                        const int64_t tok = n0 + c;
+                        if (tok >= a.n) break;
+                        float sum = 0.f;
+                        for (int s = 0; s < a.split; ++s)
+                            sum += __ldcg(a.part + (static_cast<int64_t>(s) * a.n + tok) * a.N + row);
+                        a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(sum));
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 3) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------------------
+// Host side: tensor maps (driver entry point through the runtime, so the
+// library needs no link-time libcuda) and the launch.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                       uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                       CUtensorMapSwizzle sw) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return static_cast<int>(cudaErrorInitializationError);
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
+}
+
+template <int BN>
+static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint16_t* x,
+                        const TcArgs& a, bool pdl, cudaStream_t stream) {
+    using Cfg = TcCfg<BN>;
+    CUtensorMap mx;
+    int rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, a.K, a.n, a.K * 2, kTcXStageK, BN,
+                         CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(tc_q4_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(Cfg::kSmemBytes));
+        if (e != cudaSuccess) return static_cast<int>(e);
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((a.N + kTcBM - 1) / kTcBM),
+                       static_cast<unsigned>((a.n + BN - 1) / BN), static_cast<unsigned>(a.split));
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN>, mw, ms, mx, a));
+}
+
+size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split) {
+    if (split <= 1) return 0;
+    const size_t part = static_cast<size_t>(split) * n * N * 4;
+    const size_t part_al = (part + 255) & ~static_cast<size_t>(255);
+    const size_t tiles = static_cast<size_t>((N + kTcBM - 1) / kTcBM) * ((n + bn - 1) / bn);
+    return part_al + tiles * 4;
+}
+
+int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+              const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
+              cudaStream_t stream) {
+    CUtensorMap mw, ms;
+    int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
+                         CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    rc = make_map_2d(&ms, CU_TENSOR_MAP_DATA_TYPE_UINT16, s, K / kGroup, N, (K / kGroup) * 2,
+                     kTcWStageK / kGroup, kTcBM, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+    TcArgs a;
+    a.n = n; a.K = K; a.N = N; a.y = y;
+    a.split = plan.split;
+    a.kt = static_cast<int>((K + kTcWStageK - 1) / kTcWStageK);
+    a.part = nullptr; a.cnt = nullptr;
+    if (plan.split > 1) {
+        const size_t part = static_cast<size_t>(plan.split) * n * N * 4;
+        a.part = static_cast<float*>(ws);
+        a.cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + ((part + 255) & ~static_cast<size_t>(255)));
+    }
+    switch (plan.bn) {
+        case 16: return launch_tc_bn<16>(mw, ms, x, a, pdl, stream);
+        case 32: return launch_tc_bn<32>(mw, ms, x, a, pdl, stream);
+        case 64: return launch_tc_bn<64>(mw, ms, x, a, pdl, stream);
+        case 128: return launch_tc_bn<128>(mw, ms, x, a, pdl, stream);
+        case 256: return launch_tc_bn<256>(mw, ms, x, a, pdl, stream);
+        default: return static_cast<int>(cudaErrorInvalidValue);
+    }
+}
+
+}  // namespace rq4

@@ -1,0 +1,45 @@
+// internal.h -- host-side declarations shared by the C-ABI (abi.cpp) and the
+// kernel translation units.  Not part of the public boundary (include/).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rq4 {
+
+constexpr int kGroup = 32;          // codes per fp16 scale (reading 2)
+constexpr int kNumSMs = 148;        // B200; dispatch is planned for this count
+constexpr int kGemvMaxNT = 8;       // tokens per GEMV launch
+constexpr int kTcBM = 128;          // tcgen05 tile: weight rows (MMA M)
+constexpr int kTcWStageK = 256;     // k per weight (codes+scales) TMA stage
+constexpr int kTcXStageK = 64;      // k per x TMA stage / A sub-block (4 MMAs)
+
+enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2 };
+
+struct Plan {
+    int variant = 0;
+    int nt = 0;          // GEMV: tokens per launch
+    int bn = 0;          // TC: token tile (MMA N)
+    int split = 1;       // TC: split-K factor
+    int grid = 0;
+    size_t ws_bytes = 0; // workspace bytes this plan needs
+};
+
+// Host-pure dispatch (a1): variant, tiles, split-K and workspace for (n,K,N).
+// `force_variant` / `force_split` / `force_bn` override (0 = choose).
+int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split,
+              int force_bn, Plan* out);
+size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split);
+int gemv_max_n();                   // GEMV/TC threshold (env RELAX_Q4_GEMV_MAX_N)
+bool gemv_fits(int nt, int64_t K);
+
+// Launchers (return cudaError_t as int).  All asynchronous on `stream`.
+int launch_dequant(const uint32_t* w, const uint16_t* s, int64_t K, int64_t N,
+                   uint16_t* out, cudaStream_t stream);
+int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+                const uint16_t* s, uint16_t* y, int nt, bool pdl, cudaStream_t stream);
+int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+              const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
+              cudaStream_t stream);
+
+}  // namespace rq4

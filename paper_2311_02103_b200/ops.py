@@ -1,0 +1,177 @@
+"""Python binding of the C-ABI in include/relax_q4.h (argument marshalling only).
+
+Every function here forwards torch tensors' device pointers, sizes and the
+current CUDA stream to librelax_q4.so; every step of the computation runs in
+the library's sm_100a kernels.  There is no fallback: if the shared library
+is missing or a call fails, a RelaxError is raised.
+
+Names follow the ABI: relax_q4_matmul -> q4_matmul, relax_plan_workspace ->
+plan_workspace, relax_q4_dequant -> q4_dequant, relax_query_schedule ->
+query_schedule, relax_q4_matmul_ex -> q4_matmul_ex.
+
+Tensor conventions:
+    x         torch.float16 [n, K]          (contiguous, CUDA)
+    packed_w  torch.int32   [N, K // 8]     (uint32 bit patterns stored as int32)
+    scales    torch.float16 [N, K // 32]
+    y         torch.float16 [n, N]
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "librelax_q4.so")
+
+RELAX_OK = 0
+STATUS = {
+    0: "RELAX_OK", 1: "RELAX_ERR_INVALID_ARG", 2: "RELAX_ERR_UNSUPPORTED_SHAPE",
+    3: "RELAX_ERR_MISALIGNED", 4: "RELAX_ERR_ALIAS", 5: "RELAX_ERR_WORKSPACE",
+    6: "RELAX_ERR_DEVICE", 7: "RELAX_ERR_CUDA",
+}
+VARIANT_AUTO, VARIANT_GEMV, VARIANT_TC = 0, 1, 2
+FLAG_NO_PDL = 1
+
+# every symbol include/relax_q4.h declares
+EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",
+           "relax_query_schedule", "relax_q4_dequant", "relax_status_str", "relax_version")
+
+
+class RelaxError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = lib().relax_status_str(status).decode()
+        super().__init__(f"{where}: {msg}")
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load librelax_q4.so (built by paper_2311_02103_b200.build).  Raises if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} not built: run `python -m paper_2311_02103_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, SZ, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.c_int
+        L.relax_plan_workspace.argtypes = [I64, I64, I64, ctypes.POINTER(SZ)]
+        L.relax_plan_workspace.restype = I
+        L.relax_q4_matmul.argtypes = [P, I64, I64, I64, P, P, P, P]
+        L.relax_q4_matmul.restype = I
+        L.relax_q4_matmul_ws.argtypes = [P, I64, I64, I64, P, P, P, P, SZ, P]
+        L.relax_q4_matmul_ws.restype = I
+        L.relax_q4_matmul_ex.argtypes = [P, I64, I64, I64, P, P, P, P, SZ, I, I, I, ctypes.c_uint, P]
+        L.relax_q4_matmul_ex.restype = I
+        L.relax_query_schedule.argtypes = [I64, I64, I64, ctypes.POINTER(I), ctypes.POINTER(I),
+                                           ctypes.POINTER(I), ctypes.POINTER(SZ)]
+        L.relax_query_schedule.restype = I
+        L.relax_q4_dequant.argtypes = [P, P, I64, I64, P, P]
+        L.relax_q4_dequant.restype = I
+        L.relax_status_str.argtypes = [I]
+        L.relax_status_str.restype = ctypes.c_char_p
+        L.relax_version.argtypes = []
+        L.relax_version.restype = ctypes.c_char_p
+        _lib = L
+        return L
+
+
+def _check(rc: int, where: str):
+    if rc != RELAX_OK:
+        raise RelaxError(rc, where)
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def plan_workspace(n_max: int, K: int, N: int) -> int:
+    """Bytes of workspace that make every relax_q4_matmul_ws call with n <= n_max succeed."""
+    out = ctypes.c_size_t(0)
+    _check(lib().relax_plan_workspace(n_max, K, N, ctypes.byref(out)), "relax_plan_workspace")
+    return int(out.value)
+
+
+def query_schedule(n: int, K: int, N: int) -> dict:
+    v, t, s = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    ws = ctypes.c_size_t(0)
+    _check(lib().relax_query_schedule(n, K, N, ctypes.byref(v), ctypes.byref(t), ctypes.byref(s),
+                                      ctypes.byref(ws)), "relax_query_schedule")
+    name = {VARIANT_GEMV: "gemv", VARIANT_TC: "tc"}[v.value]
+    return {"variant": name, "tile": t.value, "split_k": s.value, "ws_bytes": int(ws.value)}
+
+
+def _shapes(x, packed_w, scales):
+    n, K = x.shape
+    N = packed_w.shape[0]
+    if packed_w.shape[1] * 8 != K or scales.shape != (N, K // 32):
+        raise ValueError(f"shape mismatch: x {tuple(x.shape)} packed_w {tuple(packed_w.shape)} "
+                         f"scales {tuple(scales.shape)}")
+    return n, K, N
+
+
+def workspace(n_max: int, K: int, N: int, device=None):
+    """Allocate a zero-filled workspace sized by plan_workspace (None if 0 bytes)."""
+    import torch
+    nb = plan_workspace(n_max, K, N)
+    if nb == 0:
+        return None
+    return torch.zeros(nb, dtype=torch.uint8, device=device or "cuda")
+
+
+def q4_matmul(x, packed_w, scales, y=None, ws=None, stream=None):
+    """y[n, N] = x[n, K] . dequant(packed_w, scales) via relax_q4_matmul(_ws)."""
+    import torch
+    n, K, N = _shapes(x, packed_w, scales)
+    if y is None:
+        y = torch.empty((n, N), dtype=torch.float16, device=x.device)
+    st = _stream_ptr(stream)
+    if ws is None:
+        rc = lib().relax_q4_matmul(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y), st)
+        _check(rc, "relax_q4_matmul")
+    else:
+        rc = lib().relax_q4_matmul_ws(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y),
+                                      _ptr(ws), ws.numel() * ws.element_size(), st)
+        _check(rc, "relax_q4_matmul_ws")
+    return y
+
+
+def q4_matmul_ex(x, packed_w, scales, y=None, ws=None, variant=VARIANT_AUTO, split_k=0, bn=0,
+                 flags=0, stream=None):
+    import torch
+    n, K, N = _shapes(x, packed_w, scales)
+    if y is None:
+        y = torch.empty((n, N), dtype=torch.float16, device=x.device)
+    nb = 0 if ws is None else ws.numel() * ws.element_size()
+    rc = lib().relax_q4_matmul_ex(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y),
+                                  _ptr(ws), nb, variant, split_k, bn, flags, _stream_ptr(stream))
+    _check(rc, "relax_q4_matmul_ex")
+    return y
+
+
+def q4_dequant(packed_w, scales, K: int, w_out=None, stream=None):
+    """w_out[N, K] fp16 = fp16_RNE((q - 7) * s), bit-exact."""
+    import torch
+    N = packed_w.shape[0]
+    if w_out is None:
+        w_out = torch.empty((N, K), dtype=torch.float16, device=packed_w.device)
+    rc = lib().relax_q4_dequant(_ptr(packed_w), _ptr(scales), K, N, _ptr(w_out), _stream_ptr(stream))
+    _check(rc, "relax_q4_dequant")
+    return w_out
+
+
+def version() -> str:
+    return lib().relax_version().decode()

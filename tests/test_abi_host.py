@@ -1,0 +1,135 @@
+"""Host-side tests of the C-ABI (no GPU needed): the library loads, exports
+every symbol include/relax_q4.h declares, validates arguments before any CUDA
+call ("never a wrong answer"), and its upper-bound workspace plan
+is sound."""
+import ctypes
+import os
+import random
+import re
+
+import pytest
+
+from paper_2311_02103_b200 import build, ops
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    build.build()
+    return ops.lib()
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "relax_q4.h")).read()
+    return sorted(set(re.findall(r"RELAX_API\s+[\w\s\*]+?\b(relax_\w+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(L):
+    syms = header_symbols()
+    assert len(syms) == 8
+    assert sorted(ops.EXPORTS) == syms
+    for s in syms:
+        assert hasattr(L, s), s
+    assert ops.version().startswith("relax_q4")
+
+
+def test_status_strings(L):
+    for code, name in ops.STATUS.items():
+        assert L.relax_status_str(code).decode().startswith(name)
+    assert L.relax_status_str(99).decode() == "RELAX_ERR_UNKNOWN"
+
+
+A = 0x10000          # fake, 16-byte aligned, never dereferenced: validation
+MB = 1 << 20         # precedes every CUDA call
+
+
+def call(L, x=A, n=1, K=256, N=256, w=A + 8 * MB, s=A + 16 * MB, y=A + 24 * MB, ws=0, wsb=0):
+    return L.relax_q4_matmul_ws(x, n, K, N, w, s, y, ws, wsb, None)
+
+
+def test_validation_codes(L):
+    assert call(L, n=-1) == 1
+    assert call(L, K=0) == 1
+    assert call(L, N=0) == 1
+    assert call(L, x=0) == 1
+    assert call(L, y=0) == 1
+    assert call(L, w=0) == 1
+    assert call(L, ws=0, wsb=64) == 1
+    assert call(L, K=100) == 2                       # K % 32 != 0
+    assert call(L, n=0, x=0, y=0) == 0               # n == 0: no-op
+    assert call(L, x=A + 2) == 3                     # misaligned
+    assert call(L, y=A + 8 * MB + 8) == 3
+    assert call(L, y=A + 8 * MB) == 4                # y overlaps packed_w
+    assert call(L, y=A + 100) in (3, 4)
+    assert call(L, y=A + 112) == 4                   # y overlaps x (aligned)
+    assert call(L, ws=A + 24 * MB, wsb=1024) == 4    # workspace overlaps y
+    # valid arguments reach the device check: there is no GPU here
+    assert call(L) == 6
+    assert L.relax_q4_matmul(A, 4, 256, 256, A + 8 * MB, A + 16 * MB, A + 24 * MB, None) == 6
+    assert L.relax_q4_dequant(A, A + MB, 256, 256, A + 8 * MB, None) == 6
+    assert L.relax_q4_dequant(A, A + MB, 256, 256, A, None) == 4
+    assert L.relax_q4_dequant(A, A + MB, 250, 256, A + 8 * MB, None) == 2
+    assert L.relax_q4_dequant(A, A + MB, 256, 0, 0, None) == 0
+
+
+def test_workspace_too_small_is_reported(L):
+    # n=16 on a 4096x4096 weight uses split-K: a 16-byte workspace is too small
+    sched = ops.query_schedule(16, 4096, 4096)
+    assert sched["variant"] == "tc" and sched["split_k"] > 1 and sched["ws_bytes"] > 16
+    assert call(L, n=16, K=4096, N=4096, y=A + 64 * MB, ws=A + 128 * MB, wsb=16) == 5
+    # without a workspace the schedule is workspace-free, so it proceeds
+    assert call(L, n=16, K=4096, N=4096, y=A + 64 * MB) == 6
+    # forced TC on a K that is not a multiple of 256
+    assert L.relax_q4_matmul_ex(A, 16, 4128, 256, A + 8 * MB, A + 16 * MB, A + 64 * MB, 0, 0,
+                                2, 0, 0, 0, None) == 2
+
+
+def test_plan_invalid(L):
+    out = ctypes.c_size_t()
+    assert L.relax_plan_workspace(-1, 256, 256, ctypes.byref(out)) == 1
+    assert L.relax_plan_workspace(8, 0, 256, ctypes.byref(out)) == 1
+    assert L.relax_plan_workspace(8, 256, 256, None) == 1
+    assert L.relax_plan_workspace(8, 100, 256, ctypes.byref(out)) == 2
+
+
+SHAPES = [(256, 256), (4096, 4096), (4096, 11008), (11008, 4096), (4096, 32000),
+          (5120, 13824), (8192, 1024), (28672, 8192), (8192, 28672), (1024, 128), (96, 64)]
+
+
+@pytest.mark.parametrize("K,N", SHAPES)
+def test_plan_soundness_random_bindings(K, N):
+    """S:467 plan soundness: every n <= n_max needs <= plan(n_max) bytes."""
+    rng = random.Random(K * 31 + N)
+    for n_max in (1, 16, 100, 4096):
+        bound = ops.plan_workspace(n_max, K, N)
+        for _ in range(250):
+            n = rng.randint(1, n_max)
+            assert ops.query_schedule(n, K, N)["ws_bytes"] <= bound
+
+
+@pytest.mark.parametrize("K,N", SHAPES[:6])
+def test_plan_monotone_in_n_max(K, N):
+    prev = 0
+    for n_max in (0, 1, 2, 8, 16, 17, 64, 100, 256, 1000, 4096, 100000):
+        b = ops.plan_workspace(n_max, K, N)
+        assert b >= prev
+        prev = b
+
+
+def test_plan_is_exact_max():
+    K, N, n_max = 4096, 4096, 300
+    m = max(ops.query_schedule(n, K, N)["ws_bytes"] for n in range(1, n_max + 1))
+    assert ops.plan_workspace(n_max, K, N) == m
+
+
+def test_dispatch_shape_specialisation():
+    """n decides the variant: GEMV at decode, tensor cores for
+    prefill; K % 256 != 0 keeps GEMV at any n."""
+    assert ops.query_schedule(1, 4096, 4096)["variant"] == "gemv"
+    s = ops.query_schedule(4096, 4096, 4096)
+    assert s["variant"] == "tc" and s["tile"] in (128, 256) and s["split_k"] == 1
+    assert ops.query_schedule(512, 4128, 4096)["variant"] == "gemv"
+    for n in (17, 100, 1000):
+        s = ops.query_schedule(n, 4096, 11008)
+        assert s["variant"] == "tc" and s["tile"] >= min(n, 16)

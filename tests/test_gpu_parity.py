@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): dequantised weights bit-exact; outputs
+within rel_F <= 2e-3 and max_rel <= 1e-2 of the oracle's fp64 sum.  Pinned
+invariants (one-hot extraction, identity scale, zeros) are bitwise.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2311_02103_b200 import inputs, ops
+from tests._util import assert_within_tol, dev_weights, dev_x, host_bits
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2311_02103_b200 import build
+    build.build()
+    ops.lib()
+
+
+def run(x_bits, packed, scales, variant=0, split_k=0, bn=0, ws_n_max=None):
+    x = dev_x(x_bits)
+    pw, sc = dev_weights(packed, scales)
+    n, K = x.shape
+    N = pw.shape[0]
+    ws = None
+    if split_k > 1 or ws_n_max:
+        nb = max(ops.plan_workspace(ws_n_max or n, K, N), split_k * n * N * 4 + 4096)
+        ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    y = torch.full((n, N), float("nan"), dtype=torch.float16, device="cuda")
+    ops.q4_matmul_ex(x, pw, sc, y=y, ws=ws, variant=variant, split_k=split_k, bn=bn)
+    torch.cuda.synchronize()
+    return host_bits(y)
+
+
+# ------------------------------------------------------------------ dequant
+def test_dequant_exhaustive_bit_exact():
+    """16 codes x 65536 scale bit patterns, GPU export == oracle, bitwise."""
+    N, K = 65536, 32
+    codes = np.tile(np.concatenate([np.arange(16), np.arange(16)]), (N, 1)).astype(np.uint8)
+    packed = inputs.pack_codes(codes)
+    scales = np.arange(N, dtype=np.uint32).astype(np.uint16).reshape(N, 1)
+    want = oracle.dequant(packed, scales, K, N)
+    pw, sc = dev_weights(packed, scales)
+    got = host_bits(ops.q4_dequant(pw, sc, K))
+    nan_w = np.isnan(want.view(np.float16))
+    nan_g = np.isnan(got.view(np.float16))
+    assert np.array_equal(nan_w, nan_g)
+    assert np.array_equal(got[~nan_g], want[~nan_w])
+
+
+@pytest.mark.parametrize("kind", ["realistic", "stress"])
+def test_dequant_llama_shape_bit_exact(kind):
+    K, N = 4096, 1024
+    packed, scales = inputs.weights(kind, 1002, K, N)
+    want = oracle.dequant(packed, scales, K, N)
+    pw, sc = dev_weights(packed, scales)
+    got = host_bits(ops.q4_dequant(pw, sc, K))
+    assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------ config 1
+@pytest.mark.parametrize("kind", ["realistic", "stress"])
+@pytest.mark.parametrize("n", [1, 4])
+def test_config1_auto(kind, n):
+    K = N = 256
+    packed, scales = inputs.weights(kind, 1000, K, N)
+    x = inputs.activations(7 + n, n, K, "normal" if kind == "realistic" else "uniform")
+    r = oracle.matmul_f64(x, packed, scales, K, N)
+    y = run(x, packed, scales)
+    assert_within_tol(y, r, f"c1 {kind} n={n}")
+
+
+VARIANTS = [("gemv", 1, 0, 0), ("tc16", 2, 1, 16), ("tc32", 2, 1, 32), ("tc64", 2, 1, 64),
+            ("tc128", 2, 1, 128), ("tc256", 2, 1, 256), ("tc16s3", 2, 3, 16), ("tc64s2", 2, 2, 64),
+            ("tc128s2", 2, 2, 128)]
+
+
+@pytest.mark.parametrize("name,variant,split,bn", VARIANTS)
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 16, 17, 33, 64, 100, 129, 257, 300])
+def test_every_variant_ragged(name, variant, split, bn, n):
+    """Several M tiles and a ragged tail (N = 328 = 2*128 + 72), 3 weight
+    stages of 256 k (K = 768), ragged token tiles."""
+    if name == "gemv" and n > 17:
+        pytest.skip("GEMV exercised at small n")
+    K, N = 768, 328
+    packed, scales = inputs.realistic_weights(2000, K, N)
+    x = inputs.activations(7 + n, n, K)
+    r = oracle.matmul_f64(x, packed, scales, K, N)
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    assert_within_tol(y, r, f"{name} n={n}")
+
+
+@pytest.mark.parametrize("name,variant,split,bn", VARIANTS)
+def test_one_hot_extraction_bitwise(name, variant, split, bn):
+    """x row i = e_{k_i} -> y[i,:] == W[k_i,:] bitwise (exact product, exact
+    zero sums, one rounding of an fp16 value)."""
+    K, N = 512, 256
+    packed, scales = inputs.stress_weights(2100, K, N)
+    ks = [0, 1, 7, 8, 31, 32, 255, 256, 300, 511, 63, 64, 127, 128, 200, 400, 5]
+    x = np.zeros((len(ks), K), dtype=np.uint16)
+    for i, k in enumerate(ks):
+        x[i, k] = 0x3C00
+    W = oracle.dequant(packed, scales, K, N)          # [N][K]
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    for i, k in enumerate(ks):
+        assert np.array_equal(y[i], W[:, k]), f"{name}: row for k={k}"
+
+
+@pytest.mark.parametrize("name,variant,split,bn", VARIANTS)
+def test_identity_scale_integer_exact(name, variant, split, bn):
+    """scales = 1, x in {-1,0,1}: every partial sum is an integer < 2^24, so y
+    is exact in any summation order."""
+    K, N, n = 1024, 200, 12
+    g = np.random.default_rng(77)
+    packed = g.integers(0, 2**32, size=(N, K // 8), dtype=np.uint64).astype(np.uint32)
+    scales = np.full((N, K // 32), 0x3C00, dtype=np.uint16)
+    xi = g.integers(-1, 2, size=(n, K))
+    x = xi.astype(np.float16).view(np.uint16)
+    r = oracle.matmul_f64(x, packed, scales, K, N)
+    assert np.all(np.abs(r) <= 2048)
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    assert np.array_equal(y.view(np.float16).astype(np.float64), r)
+
+
+@pytest.mark.parametrize("case", ["codes7", "scales0", "x0"])
+@pytest.mark.parametrize("name,variant,split,bn", VARIANTS[:3])
+def test_zero_invariants(case, name, variant, split, bn):
+    K, N, n = 512, 256, 5
+    packed, scales = inputs.stress_weights(2200, K, N)
+    x = inputs.activations(2201, n, K)
+    if case == "codes7":
+        packed = np.full_like(packed, 0x77777777)
+    elif case == "scales0":
+        scales = np.zeros_like(scales)
+    else:
+        x = np.zeros_like(x)
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    assert np.all((y & 0x7FFF) == 0)
+
+
+def test_n_zero_is_noop():
+    K, N = 256, 256
+    packed, scales = inputs.stress_weights(1, K, N)
+    pw, sc = dev_weights(packed, scales)
+    x = torch.empty((0, K), dtype=torch.float16, device="cuda")
+    y = torch.empty((0, N), dtype=torch.float16, device="cuda")
+    ops.q4_matmul(x, pw, sc, y=y)
+    torch.cuda.synchronize()
+
+
+def test_deterministic_reruns_bitwise():
+    K, N = 4096, 4096
+    packed, scales = inputs.realistic_weights(1001, K, N)
+    pw, sc = dev_weights(packed, scales)
+    for n in (1, 3, 16, 40, 200, 1000):
+        x = dev_x(inputs.activations(7 + n, n, K))
+        ws = ops.workspace(n, K, N)
+        a = host_bits(ops.q4_matmul(x, pw, sc, ws=ws))
+        b = host_bits(ops.q4_matmul(x, pw, sc, ws=ws))
+        assert np.array_equal(a, b), f"n={n}"
+
+
+# ------------------------------------------------------------------ full sizes
+def test_prefix_sweep_4096_sampled_columns():
+    """One n=4096 input pins every n in [1, 4096] (rows are independent):
+    each call with x[:n] is compared with the oracle's rows r[:n] on 48
+    sampled output columns, in the auto-dispatch launch configuration."""
+    K, N = 4096, 4096
+    packed, scales = inputs.realistic_weights(3001, K, N)
+    xall = inputs.activations(7 + 4096, 4096, K)
+    g = np.random.default_rng(0)
+    cols = np.sort(g.choice(N, size=48, replace=False))
+    r = oracle.matmul_cols_f64(xall, packed, scales, K, cols)
+    pw, sc = dev_weights(packed, scales)
+    xd = dev_x(xall)
+    ws = ops.workspace(4096, K, N)
+    ns = list(range(1, 17)) + [24, 32, 48, 64, 80, 96, 100, 128, 192, 256, 384, 512, 768,
+                                1000, 1024, 1536, 2048, 3072, 4095, 4096, 17]
+    for n in ns:
+        y = host_bits(ops.q4_matmul(xd[:n], pw, sc, ws=ws))
+        assert_within_tol(y[:, cols], r[:n], f"prefix n={n}")
+
+
+@pytest.mark.parametrize("K,N", [(4096, 11008), (11008, 4096), (4096, 32000), (5120, 13824),
+                                 (13824, 5120), (8192, 1024), (28672, 8192)])
+@pytest.mark.parametrize("n", [1, 16, 512])
+def test_llama_shapes_sampled(K, N, n):
+    packed, scales = inputs.realistic_weights(4000 + K % 97 + N % 89, K, N)
+    x = inputs.activations(7 + n, n, K)
+    g = np.random.default_rng(1)
+    cols = np.sort(g.choice(N, size=32, replace=False))
+    rows = np.arange(n) if n <= 16 else np.sort(g.choice(n, size=16, replace=False))
+    r = oracle.matmul_cols_f64(x[rows], packed, scales, K, cols)
+    pw, sc = dev_weights(packed, scales)
+    ws = ops.workspace(n, K, N)
+    y = host_bits(ops.q4_matmul(dev_x(x), pw, sc, ws=ws))
+    assert_within_tol(y[rows][:, cols], r, f"{K}x{N} n={n}")
+
+
+def test_cuda_graph_capture_every_variant():
+    """Calls are capturable (no allocation, no host sync inside) and the
+    replayed graph reproduces the eager result bitwise."""
+    K, N = 4096, 4096
+    packed, scales = inputs.realistic_weights(5001, K, N)
+    pw, sc = dev_weights(packed, scales)
+    ns = [1, 2, 16, 64, 300]
+    xs = [dev_x(inputs.activations(7 + n, n, K)) for n in ns]
+    ws = ops.workspace(max(ns), K, N)
+    eager = [host_bits(ops.q4_matmul(x, pw, sc, ws=ws)) for x in xs]
+    ys = [torch.empty((n, N), dtype=torch.float16, device="cuda") for n in ns]
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for x, y in zip(xs, ys):
+            ops.q4_matmul(x, pw, sc, y=y, ws=ws)
+    g.replay()
+    torch.cuda.synchronize()
+    for e, y in zip(eager, ys):
+        assert np.array_equal(e, host_bits(y))
+
+
+def test_workspace_reused_across_calls():
+    """One zero-filled, plan-sized workspace serves a sequence of split-K calls
+    of different n (the tickets reset themselves), each within tolerance."""
+    K, N = 4096, 4096
+    ws = ops.workspace(64, K, N)
+    assert ws is not None
+    packed, scales = inputs.realistic_weights(6001, K, N)
+    pw, sc = dev_weights(packed, scales)
+    cols = np.arange(0, N, 97)
+    for n in (16, 17, 40, 64, 16, 33):
+        xb = inputs.activations(n, n, K)
+        y = host_bits(ops.q4_matmul(dev_x(xb), pw, sc, ws=ws))
+        r = oracle.matmul_cols_f64(xb, packed, scales, K, cols)
+        assert_within_tol(y[:, cols], r, f"reuse n={n}")
