@@ -91,6 +91,10 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
         int s = force_split > 0 ? force_split : choose_split(tiles, kt, p.bn);
         if (s > kt) s = kt;
         if (s < 1) s = 1;
+        if (s > 1 && tiles > kMaxSplitTiles) {
+            if (force_split > 1) return RELAX_ERR_UNSUPPORTED_SHAPE;
+            s = 1;
+        }
         p.split = s;
         p.ws_bytes = tc_workspace_bytes(n, N, p.bn, s);
     } else {

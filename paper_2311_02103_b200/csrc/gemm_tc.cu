@@ -326,12 +326,13 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
     return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN>, mw, ms, mx, a));
 }
 
+// Workspace layout (fixed ticket region first, so one buffer serves every n):
+//   [0, kTicketBytes)            uint32 tickets, one per output tile (<= 1024)
+//   [kTicketBytes, +split*n*N*4) fp32 split-K partials [split][n][N]
 size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split) {
+    (void)bn;
     if (split <= 1) return 0;
-    const size_t part = static_cast<size_t>(split) * n * N * 4;
-    const size_t part_al = (part + 255) & ~static_cast<size_t>(255);
-    const size_t tiles = static_cast<size_t>((N + kTcBM - 1) / kTcBM) * ((n + bn - 1) / bn);
-    return part_al + tiles * 4;
+    return kTicketBytes + static_cast<size_t>(split) * n * N * 4;
 }
 
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
@@ -350,9 +351,8 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.kt = static_cast<int>((K + kTcWStageK - 1) / kTcWStageK);
     a.part = nullptr; a.cnt = nullptr;
     if (plan.split > 1) {
-        const size_t part = static_cast<size_t>(plan.split) * n * N * 4;
-        a.part = static_cast<float*>(ws);
-        a.cnt = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(ws) + ((part + 255) & ~static_cast<size_t>(255)));
+        a.cnt = static_cast<uint32_t*>(ws);
+        a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes);
     }
     switch (plan.bn) {
         case 16: return launch_tc_bn<16>(mw, ms, x, a, pdl, stream);

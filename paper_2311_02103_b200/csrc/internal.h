@@ -13,6 +13,8 @@ constexpr int kGemvMaxNT = 8;       // tokens per GEMV launch
 constexpr int kTcBM = 128;          // tcgen05 tile: weight rows (MMA M)
 constexpr int kTcWStageK = 256;     // k per weight (codes+scales) TMA stage
 constexpr int kTcXStageK = 64;      // k per x TMA stage / A sub-block (4 MMAs)
+constexpr size_t kTicketBytes = 4096;  // split-K tickets: fixed region at workspace offset 0
+constexpr int64_t kMaxSplitTiles = kTicketBytes / 4;
 
 enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2 };
 
