@@ -31,18 +31,26 @@ static int choose_bn(int64_t n, int64_t N) {
     if (n <= 16) return 16;
     if (n <= 32) return 32;
     if (n <= 64) return 64;
-    if (n <= 128) return 128;
     const int64_t tm = (N + kTcBM - 1) / kTcBM;
-    if (n <= 256) return tm >= kNumSMs ? 256 : 128;
+    if (n <= 128) return 128;
     const int64_t t256 = tm * ((n + 255) / 256);
     return t256 >= kNumSMs ? 256 : 128;
 }
 
-// Split-K factor that best fills whole waves of the machine (HBM-bound small
-// n); each split keeps >= 2 weight stages.
-static int choose_split(int64_t tiles, int kt, int bn) {
+// Split-K factor.  Small n (<= 64) is HBM-bound: pick the split that best
+// fills whole waves (each split keeps >= 2 weight stages).  Larger n is
+// tensor-bound and split-K only adds partial-sum traffic, so split only when
+// the tiles cover less than half a wave, and by at most 4.
+static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
     const int64_t slots = static_cast<int64_t>(kNumSMs) * ctas_per_sm_tc(bn);
     if (tiles >= slots) return 1;
+    if (n > 64) {
+        if (tiles * 2 >= kNumSMs) return 1;
+        int s = static_cast<int>((kNumSMs + tiles - 1) / tiles);
+        if (s > 4) s = 4;
+        if (s > kt / 4) s = kt / 4 < 1 ? 1 : kt / 4;
+        return s;
+    }
     int best = 1;
     double best_eff = 0.0;
     const int smax = kt / 2 < 16 ? (kt / 2 < 1 ? 1 : kt / 2) : 16;
@@ -88,7 +96,7 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
         }
         const int kt = static_cast<int>(K / kTcWStageK);
         const int64_t tiles = ((N + kTcBM - 1) / kTcBM) * ((n + p.bn - 1) / p.bn);
-        int s = force_split > 0 ? force_split : choose_split(tiles, kt, p.bn);
+        int s = force_split > 0 ? force_split : choose_split(n, tiles, kt, p.bn);
         if (s > kt) s = kt;
         if (s < 1) s = 1;
         if (s > 1 && tiles > kMaxSplitTiles) {

@@ -243,13 +243,24 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             if (*flag_slot) {
                 __threadfence();
                 if (row_ok) {
-                    for (int c = 0; c < BN; ++c) {
-                        const int64_t tok = n0 + c;
-                        if (tok >= a.n) break;
-                        float sum = 0.f;
-                        for (int s = 0; s < a.split; ++s)
-                            sum += __ldcg(a.part + (static_cast<int64_t>(s) * a.n + tok) * a.N + row);
-                        a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(sum));
+                    // fixed split order s = 0..S-1 -> deterministic; 8 tokens of
+                    // independent loads in flight per thread.
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 8) {
+                        float sum[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) sum[u] = 0.f;
+                        for (int s = 0; s < a.split; ++s) {
+                            const float* ps = a.part + (static_cast<int64_t>(s) * a.n + n0 + c0) * a.N + row;
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (n0 + c0 + u < a.n) sum[u] += __ldcg(ps + static_cast<int64_t>(u) * a.N);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const int64_t tok = n0 + c0 + u;
+                            if (tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(sum[u]));
+                        }
                     }
                 }
             }

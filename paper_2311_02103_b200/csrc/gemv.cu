@@ -239,6 +239,9 @@ static int launch_gemv_nt(const GemvArgs& a, bool pdl, cudaStream_t stream) {
 
 int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                 const uint16_t* s, uint16_t* y, int nt, bool pdl, cudaStream_t stream) {
+    // Streamed kernel (gemv_stream.cu) for the decode shapes it supports.
+    if (nt <= 2 && gemv_stream_ok(nt, K) && N >= 1)
+        return launch_gemv_stream(x, n, K, N, w, s, y, pdl, stream);
     if (nt < 1 || nt > kGemvMaxNT) nt = kGemvMaxNT;
     for (int64_t t0 = 0; t0 < n; t0 += nt) {
         const int cnt = static_cast<int>((n - t0) < nt ? (n - t0) : nt);

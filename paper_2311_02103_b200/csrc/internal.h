@@ -40,6 +40,9 @@ int launch_dequant(const uint32_t* w, const uint16_t* s, int64_t K, int64_t N,
                    uint16_t* out, cudaStream_t stream);
 int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                 const uint16_t* s, uint16_t* y, int nt, bool pdl, cudaStream_t stream);
+int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
+bool gemv_stream_ok(int nt, int64_t K);
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
               const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
               cudaStream_t stream);
