@@ -165,10 +165,11 @@ def run_ours(args, rank, world, local_rank):
     sched = {f"{K}x{N}": ops.query_schedule(n, K, N) for K, N in shapes}
 
     stream = torch.cuda.Stream(device=dev)
+    flags = ops.FLAG_NO_PDL if args.no_pdl else 0
 
     def step():
         for (name, K, N), (pk, sc), y in zip(mats, weights, ys):
-            ops.q4_matmul(xs[K], pk, sc, y=y, ws=wss[(K, N)], stream=stream)
+            ops.q4_matmul_ex(xs[K], pk, sc, y=y, ws=wss[(K, N)], flags=flags, stream=stream)
 
     # capture the step
     torch.cuda.synchronize()
@@ -276,7 +277,7 @@ def run_ours(args, rank, world, local_rank):
                    "layers_linears": len(mats), "weight_bytes": int(sum(inputs.q4_bytes(K, N) for _, K, N in mats)),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "not flushed: per-step working set %.2f GB >> 126 MB L2" % (bytes_step / 1e9),
-                   "graph": graph is not None, "pdl": True, "schedule": sched},
+                   "graph": graph is not None, "pdl": not args.no_pdl, "schedule": sched},
         "hbm_gbs": round(gbs, 1),
         "tflops": round(tflops, 3),
         "roofline": roof,
@@ -360,6 +361,7 @@ def main():
                              "llama2-7b-prefill", "llama2-13b-prefill"])
     ap.add_argument("--n", type=int, default=None, help="tokens per step (decode: 1)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.n is None:

@@ -95,11 +95,11 @@ __global__ void __launch_bounds__(MAXT, MINB) gemv_stream_kernel(const __grid_co
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nwc = a.WK * a.H;                        // consumer warps
-    uint8_t* ring = smem;
-    float* part = reinterpret_cast<float*>(smem + static_cast<size_t>(a.NS) * a.stage_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(part + static_cast<size_t>(a.rows_cta_max) * a.WK * NT);
-    uint64_t* full = bars;
-    uint64_t* empty = bars + a.NS;
+    // [barriers: 2*NS x 8 B, padded to 128][ring: NS stages][partials]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + a.NS;
+    uint8_t* ring = smem + 128;
+    float* part = reinterpret_cast<float*>(ring + static_cast<size_t>(a.NS) * a.stage_bytes);
 
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * a.N / gridDim.x;
     const int64_t row1 = static_cast<int64_t>(blockIdx.x + 1) * a.N / gridDim.x;
@@ -279,8 +279,8 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                        const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
     GsConfig c = gs_config(K, N);
-    c.smem = static_cast<size_t>(c.NS) * c.RS * (K / 2 + K / 16) +
-             static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4 + 2 * c.NS * 8;
+    c.smem = 128 + static_cast<size_t>(c.NS) * c.RS * (K / 2 + K / 16) +
+             static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
     for (int64_t t0 = 0; t0 < n; t0 += 2) {
         const int cnt = (n - t0) >= 2 ? 2 : 1;
         GsArgs a;

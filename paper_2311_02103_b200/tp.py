@@ -1,0 +1,109 @@
+"""Tensor-parallel sharding of q4f16 linears over torch.distributed.
+
+One process per GPU; the data path per rank is the C-ABI kernel
+(relax_q4_matmul) on the rank's shard, and the only exchange is one NCCL
+collective where the sharding needs one (NVLink 5 / NVSwitch on the box):
+
+  column split (N/p rows of the NK layout per rank, contiguous -- no repack):
+      y_r[n, N/p] = x[n, K] . W_r            ; optional all_gather -> y[n, N]
+  row split    (K/p slice of every row, materialised once at load time):
+      y_r[n, N]   = x_r[n, K/p] . W_r        ; all_reduce(sum) -> y[n, N]
+
+Megatron pairing for a Llama decoder block: q/k/v and gate/up column-split
+feed o and down row-split, one all_reduce after each (2 per layer).
+
+The per-rank matmul is injectable (`matmul`) so the host-side sharding and
+collective logic can be tested on CPU with the gloo backend; the product path
+uses ops.q4_matmul and has no fallback.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+GROUP = 32
+
+
+def shard_bounds(total: int, rank: int, world: int, align: int = 1):
+    """[lo, hi) of `total` for `rank`, split into `world` equal aligned parts."""
+    if total % (world * align) != 0:
+        raise ValueError(f"{total} not divisible into {world} parts aligned to {align}")
+    part = total // world
+    return rank * part, (rank + 1) * part
+
+
+def shard_columns(packed, scales, rank: int, world: int):
+    """Column split: output features [N r/p, N (r+1)/p) -- contiguous rows of
+    packed_w [N][K/8] and scales [N][K/32]."""
+    N = packed.shape[0]
+    lo, hi = shard_bounds(N, rank, world)
+    return packed[lo:hi], scales[lo:hi]
+
+
+def shard_rows(packed, scales, rank: int, world: int):
+    """Row split: reduction range k in [K r/p, K (r+1)/p); K/p must be a
+    multiple of the 32-code group (and of 256 for the tensor-core variant)."""
+    K = packed.shape[1] * 8
+    lo, hi = shard_bounds(K, rank, world, GROUP)
+    pk = packed[:, lo // 8:hi // 8]
+    sc = scales[:, lo // GROUP:hi // GROUP]
+    # materialise contiguous shards (done once, at weight-load time)
+    if hasattr(pk, "contiguous"):
+        return pk.contiguous(), sc.contiguous()
+    return np.ascontiguousarray(pk), np.ascontiguousarray(sc)
+
+
+def _default_matmul():
+    from . import ops
+    return lambda x, pk, sc: ops.q4_matmul(x, pk, sc)
+
+
+@dataclass
+class ColumnParallelQ4:
+    packed: object
+    scales: object
+    group: object = None
+    gather: bool = False
+    matmul: Optional[Callable] = None
+
+    def __call__(self, x):
+        import torch
+        import torch.distributed as dist
+        mm = self.matmul or _default_matmul()
+        y = mm(x, self.packed, self.scales)               # [n, N/p]
+        if not self.gather:
+            return y
+        world = dist.get_world_size(self.group)
+        parts = [torch.empty_like(y) for _ in range(world)]
+        dist.all_gather(parts, y.contiguous(), group=self.group)
+        return torch.cat(parts, dim=1)                    # [n, N]
+
+
+@dataclass
+class RowParallelQ4:
+    packed: object
+    scales: object
+    group: object = None
+    matmul: Optional[Callable] = None
+    reduce_fp32: bool = True
+
+    def __call__(self, x_shard):
+        import torch
+        import torch.distributed as dist
+        mm = self.matmul or _default_matmul()
+        y = mm(x_shard, self.packed, self.scales)         # partial [n, N]
+        if self.reduce_fp32:
+            y32 = y.float()
+            dist.all_reduce(y32, op=dist.ReduceOp.SUM, group=self.group)
+            return y32.to(torch.float16)
+        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
+        return y
+
+
+def split_x_for_rows(x, rank: int, world: int):
+    """The K-slice of x a row-split rank consumes."""
+    K = x.shape[1]
+    lo, hi = shard_bounds(K, rank, world, GROUP)
+    return x[:, lo:hi].contiguous()

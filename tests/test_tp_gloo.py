@@ -1,0 +1,130 @@
+"""Tensor-parallel host logic on CPU: world_size 2 over gloo (127.0.0.1).
+
+The per-rank matmul here is the CPU oracle (test-only injection); on the GPU
+box the same classes call the C-ABI kernel.  Checks (SURVEY §8(c) "TP"):
+column shards concatenated == the unsharded oracle bitwise (columns are
+independent); row-split partial sums all-reduced == unsharded oracle within
+tolerance; the Megatron pair (column -> row) matches the two-step oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2311_02103_b200 import inputs, tp
+from tests._util import assert_within_tol
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_mm(x, pk, sc):
+    xb = x.contiguous().numpy().view(np.uint16)
+    pkn = pk.contiguous().numpy().view(np.uint32)
+    scn = sc.contiguous().numpy().view(np.uint16)
+    K = xb.shape[1]
+    N = pkn.shape[0]
+    r = oracle.matmul_f64(xb, pkn, scn, K, N, nthreads=1)
+    return torch.from_numpy(oracle.round_f16(r).view(np.float16).copy())
+
+
+def t16(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.float16).copy())
+
+
+def t32(words):
+    return torch.from_numpy(np.ascontiguousarray(words).view(np.int32).copy())
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        K, N, n = 512, 256, 3
+        pk, sc = inputs.realistic_weights(5000, K, N)
+        xb = inputs.activations(5001, n, K)
+        x = t16(xb)
+        # column split + all_gather
+        cpk, csc = tp.shard_columns(t32(pk), t16(sc), rank, world)
+        col = tp.ColumnParallelQ4(cpk, csc, gather=True, matmul=oracle_mm)
+        out["col"] = col(x).numpy().view(np.uint16)
+        # row split + all_reduce
+        rpk, rsc = tp.shard_rows(t32(pk), t16(sc), rank, world)
+        row = tp.RowParallelQ4(rpk, rsc, matmul=oracle_mm)
+        out["row"] = row(tp.split_x_for_rows(x, rank, world)).numpy().view(np.uint16)
+        # Megatron pair: gate (col, K->N2) then down (row, N2->K2)
+        K2 = 256
+        gpk, gsc = inputs.realistic_weights(5002, K, 512)          # K -> 512
+        dpk, dsc = inputs.realistic_weights(5003, 512, K2)         # 512 -> K2
+        g = tp.ColumnParallelQ4(*tp.shard_columns(t32(gpk), t16(gsc), rank, world), matmul=oracle_mm)
+        d = tp.RowParallelQ4(*tp.shard_rows(t32(dpk), t16(dsc), rank, world), matmul=oracle_mm)
+        out["pair"] = d(g(x)).numpy().view(np.uint16)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def results():
+    oracle.build()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_column_split_bitwise(results):
+    K, N, n = 512, 256, 3
+    pk, sc = inputs.realistic_weights(5000, K, N)
+    xb = inputs.activations(5001, n, K)
+    want = oracle.round_f16(oracle.matmul_f64(xb, pk, sc, K, N))
+    for r in (0, 1):
+        assert np.array_equal(results[r]["col"], want)
+
+
+def test_row_split_allreduce_within_tol(results):
+    K, N, n = 512, 256, 3
+    pk, sc = inputs.realistic_weights(5000, K, N)
+    xb = inputs.activations(5001, n, K)
+    r = oracle.matmul_f64(xb, pk, sc, K, N)
+    assert np.array_equal(results[0]["row"], results[1]["row"])
+    assert_within_tol(results[0]["row"], r, "row split")
+
+
+def test_megatron_pair(results):
+    K, n = 512, 3
+    xb = inputs.activations(5001, n, K)
+    gpk, gsc = inputs.realistic_weights(5002, K, 512)
+    dpk, dsc = inputs.realistic_weights(5003, 512, 256)
+    h = oracle.round_f16(oracle.matmul_f64(xb, gpk, gsc, K, 512))
+    r = oracle.matmul_f64(h, dpk, dsc, 512, 256)
+    assert np.array_equal(results[0]["pair"], results[1]["pair"])
+    assert_within_tol(results[0]["pair"], r, "pair")
+
+
+def test_shard_bounds_errors():
+    with pytest.raises(ValueError):
+        tp.shard_bounds(100, 0, 3)
+    with pytest.raises(ValueError):
+        tp.shard_bounds(96, 0, 2, align=32)   # 48 not a multiple of 32
+    assert tp.shard_bounds(8192, 3, 8, 32) == (3072, 4096)
