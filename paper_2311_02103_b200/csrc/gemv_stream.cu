@@ -25,6 +25,7 @@
 //     WK K-columns are summed in shared memory in fixed order: deterministic;
 //   * PDL: the producer starts streaming weights before griddepcontrol.wait;
 //     only the x loads and the y stores wait for the previous kernel.
+#include <cstdlib>
 #include "internal.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
@@ -47,8 +48,8 @@ struct GsConfig {
     size_t smem;
 };
 
-constexpr int kGsMaxConsumerWarps = 16;   // WK * H <= 16 in the 2-CTA/SM build
-constexpr int kGsSmemBudget = 100 * 1024;
+constexpr int kGsMaxConsumerWarps = 16;   // consumer warps per CTA (one CTA per SM)
+constexpr size_t kGsRingBudget = 176 * 1024;
 
 __device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
@@ -89,17 +90,73 @@ __device__ __forceinline__ int reduce_row_of_lane(int lane) {
     return row;
 }
 
-template <int NT, int RPW, int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) gemv_stream_kernel(const __grid_constant__ GsArgs a) {
+// Per-lane contribution of one row: lane owns one 32-code group (16 B of
+// codes `cw`, fp16 scale `sbits`), x for that group in xr[t][0..3].
+//   ZPF = 0: exact centering -- (q - 7) as fp16 via the magic-number unpack
+//            (1 SHF + 4 LOP3 + 4 HFMA2 per 8 codes), then 8 FHFMA;
+//   ZPF = 1: factored zero point -- codes as fp16 subnormals q * 2^-24 (pure
+//            masks, 1 SHF + 4 LOP3 per 8 codes), 8 FHFMA, and per group
+//            sum (q - 7) x = 2^24 (acc_e + acc_o / 16) - 7 * sum x.
+template <int NT, int ZPF>
+__device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const uint4 (&xr)[NT][4],
+                                        const float (&m7x)[NT], float (&out)[NT]) {
+    const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+    float ge[NT], go[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) { ge[t] = 0.f; go[t] = 0.f; }
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi) {
+        uint32_t c0, c1, c2, c3;
+        if (ZPF) {
+            const uint32_t v8 = words[wi] >> 8;
+            c0 = words[wi] & 0x000F000Fu;      // (q0, q4)   * 2^-24
+            c1 = words[wi] & 0x00F000F0u;      // (q1, q5)   * 2^-20
+            c2 = v8 & 0x000F000Fu;             // (q2, q6)   * 2^-24
+            c3 = v8 & 0x00F000F0u;             // (q3, q7)   * 2^-20
+        } else {
+            __half2 cc[4];
+            unpack_centered_interleaved(words[wi], cc);
+            c0 = h2_as_u32(cc[0]); c1 = h2_as_u32(cc[1]); c2 = h2_as_u32(cc[2]); c3 = h2_as_u32(cc[3]);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const uint4 X = xr[t][wi];         // (k0,k1) (k2,k3) (k4,k5) (k6,k7)
+            float e = ge[t], o = go[t];
+            e = fhfma(lo16(c0), lo16(X.x), e);   // k0
+            o = fhfma(lo16(c1), hi16(X.x), o);   // k1
+            e = fhfma(lo16(c2), lo16(X.y), e);   // k2
+            o = fhfma(lo16(c3), hi16(X.y), o);   // k3
+            e = fhfma(hi16(c0), lo16(X.z), e);   // k4
+            o = fhfma(hi16(c1), hi16(X.z), o);   // k5
+            e = fhfma(hi16(c2), lo16(X.w), e);   // k6
+            o = fhfma(hi16(c3), hi16(X.w), o);   // k7
+            ge[t] = e;
+            go[t] = o;
+        }
+    }
+    const float sc = __half2float(__ushort_as_half(sbits));
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        if (ZPF) {
+            const float u = fmaf(go[t], 0.0625f, ge[t]);
+            out[t] = sc * fmaf(u, 16777216.0f, m7x[t]);
+        } else {
+            out[t] = sc * (ge[t] + go[t]);
+        }
+    }
+}
+
+template <int NT, int RPW, int ZPF, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) gemv_stream_kernel(const __grid_constant__ GsArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nwc = a.WK * a.H;                        // consumer warps
-    // [barriers: 2*NS x 8 B, padded to 128][ring: NS stages][partials]
+    // [barriers: 2*NS x 8 B, padded to 128][ring: NS stages + 1 KB pad][partials]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + a.NS;
     uint8_t* ring = smem + 128;
-    float* part = reinterpret_cast<float*>(ring + static_cast<size_t>(a.NS) * a.stage_bytes);
+    float* part = reinterpret_cast<float*>(ring + static_cast<size_t>(a.NS) * a.stage_bytes + 1024);
 
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * a.N / gridDim.x;
     const int64_t row1 = static_cast<int64_t>(blockIdx.x + 1) * a.N / gridDim.x;
@@ -122,10 +179,10 @@ __global__ void __launch_bounds__(MAXT, MINB) gemv_stream_kernel(const __grid_co
             const uint64_t pol = policy_evict_first();
             const uint8_t* wsrc = a.w + row0 * cb_row;
             const uint8_t* ssrc = a.s + row0 * sb_row;
-            for (int st = 0; st < nst; ++st) {
-                const int slot = st % a.NS;
-                mbar_wait(&empty[slot], ((st / a.NS) & 1) ^ 1);
-                const int r = st * a.RS;
+            int slot = 0;
+            uint32_t phase = 0;
+            for (int r = 0; r < rows; r += a.RS) {
+                mbar_wait(&empty[slot], phase ^ 1);
                 const int nr = rows - r < a.RS ? rows - r : a.RS;
                 const uint32_t bc = static_cast<uint32_t>(nr) * cb_row;
                 const uint32_t bs = static_cast<uint32_t>(nr) * sb_row;
@@ -133,6 +190,7 @@ __global__ void __launch_bounds__(MAXT, MINB) gemv_stream_kernel(const __grid_co
                 mbar_arrive_expect_tx(&full[slot], bc + bs);
                 bulk_load(dst, wsrc + static_cast<size_t>(r) * cb_row, bc, &full[slot], pol);
                 bulk_load(dst + codes_stage, ssrc + static_cast<size_t>(r) * sb_row, bs, &full[slot], pol);
+                if (++slot == a.NS) { slot = 0; phase ^= 1; }
             }
         }
     } else {
@@ -143,67 +201,62 @@ __global__ void __launch_bounds__(MAXT, MINB) gemv_stream_kernel(const __grid_co
         const bool gv = g < a.G;
         pdl_wait();
         uint4 xr[NT][4];
+        float m7x[NT];
 #pragma unroll
-        for (int t = 0; t < NT; ++t)
+        for (int t = 0; t < NT; ++t) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 xr[t][q] = gv ? reinterpret_cast<const uint4*>(a.x + static_cast<int64_t>(t) * a.K + g * 32)[q]
                               : make_uint4(0u, 0u, 0u, 0u);
-        const int rsel = reduce_row_of_lane<RPW>(lane);
-        for (int st = 0; st < nst; ++st) {
-            const int slot = st % a.NS;
-            mbar_wait(&full[slot], (st / a.NS) & 1);
-            const uint8_t* stage = ring + static_cast<size_t>(slot) * a.stage_bytes;
-            const int r_base = st * a.RS;
-            const int nr = rows - r_base < a.RS ? rows - r_base : a.RS;
-            float acc[NT][RPW];
+            float sx = 0.f;           // sum of the group's x (factored zero point)
 #pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                const int rl = h * RPW + i;
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t w4[4] = {xr[t][q].x, xr[t][q].y, xr[t][q].z, xr[t][q].w};
 #pragma unroll
-                for (int t = 0; t < NT; ++t) acc[t][i] = 0.f;
-                if (rl < nr && gv) {
-                    const uint4 cw = lds128(stage + static_cast<size_t>(rl) * cb_row + g * 16);
-                    const uint16_t sbits = *reinterpret_cast<const uint16_t*>(
-                        stage + codes_stage + static_cast<size_t>(rl) * sb_row + g * 2);
-                    const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
-                    float ga[NT][2];
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) { ga[t][0] = 0.f; ga[t][1] = 0.f; }
-#pragma unroll
-                    for (int wi = 0; wi < 4; ++wi) {
-                        __half2 cc[4];
-                        unpack_centered_interleaved(words[wi], cc);
-                        const uint32_t c0 = h2_as_u32(cc[0]), c1 = h2_as_u32(cc[1]);
-                        const uint32_t c2 = h2_as_u32(cc[2]), c3 = h2_as_u32(cc[3]);
-#pragma unroll
-                        for (int t = 0; t < NT; ++t) {
-                            const uint4 X = xr[t][wi];    // (k0,k1) (k2,k3) (k4,k5) (k6,k7)
-                            float e = ga[t][0], o = ga[t][1];
-                            e = fhfma(lo16(c0), lo16(X.x), e);   // k0
-                            o = fhfma(lo16(c1), hi16(X.x), o);   // k1
-                            e = fhfma(lo16(c2), lo16(X.y), e);   // k2
-                            o = fhfma(lo16(c3), hi16(X.y), o);   // k3
-                            e = fhfma(hi16(c0), lo16(X.z), e);   // k4
-                            o = fhfma(hi16(c1), hi16(X.z), o);   // k5
-                            e = fhfma(hi16(c2), lo16(X.w), e);   // k6
-                            o = fhfma(hi16(c3), hi16(X.w), o);   // k7
-                            ga[t][0] = e;
-                            ga[t][1] = o;
-                        }
-                    }
-                    const float sc = __half2float(__ushort_as_half(sbits));
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) acc[t][i] = sc * (ga[t][0] + ga[t][1]);
+                for (int u = 0; u < 4; ++u) {
+                    const float2 f = __half22float2(u32_as_h2(w4[u]));
+                    sx += f.x + f.y;
                 }
+            }
+            m7x[t] = -7.0f * sx;
+        }
+        const int rsel = reduce_row_of_lane<RPW>(lane);
+        const bool writer = (lane & (32 / RPW - 1)) == 0;
+        // this warp's rows inside a stage: [h*RPW, h*RPW + RPW)
+        const uint32_t coff = static_cast<uint32_t>(h * RPW) * cb_row + static_cast<uint32_t>(g) * 16u;
+        const uint32_t soff = codes_stage + static_cast<uint32_t>(h * RPW) * sb_row + static_cast<uint32_t>(g) * 2u;
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int r_base = 0; r_base < rows; r_base += a.RS) {
+            const int nr = rows - r_base < a.RS ? rows - r_base : a.RS;
+            mbar_wait(&full[slot], phase);
+            const uint8_t* stage = ring + static_cast<size_t>(slot) * a.stage_bytes;
+            float acc[NT][RPW];
+            if (h * RPW < nr) {                              // warp-uniform
+#pragma unroll
+                for (int i = 0; i < RPW; ++i) {
+                    const uint4 cw = lds128(stage + coff + i * cb_row);
+                    uint16_t sbits = *reinterpret_cast<const uint16_t*>(stage + soff + i * sb_row);
+                    if (!gv) sbits = 0;                       // lanes past K: x = 0 and s = 0
+                    float o[NT];
+                    row_dot<NT, ZPF>(cw, sbits, xr, m7x, o);
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) acc[t][i] = o[t];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) acc[t][i] = 0.f;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);      // stage bytes fully consumed
+            if (++slot == a.NS) { slot = 0; phase ^= 1; }
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const float v = reduce_rows<RPW>(acc[t], lane);
                 const int rl = h * RPW + rsel;
-                if ((lane & (32 / RPW - 1)) == 0 && rl < nr)
+                if (writer && rl < nr)
                     part[(static_cast<size_t>(r_base + rl) * a.WK + kw) * NT + t] = v;
             }
         }
@@ -219,32 +272,42 @@ __global__ void __launch_bounds__(MAXT, MINB) gemv_stream_kernel(const __grid_co
     }
 }
 
+static int gs_zpf() {
+    static int v = [] {
+        const char* e = std::getenv("RELAX_Q4_GEMV_ZPF");
+        return (e && *e == '1') ? 1 : 0;
+    }();
+    return v;
+}
+
 static GsConfig gs_config(int64_t K, int64_t N) {
     GsConfig c{};
     const int G = static_cast<int>(K / kGroup);
     c.WK = (G + 31) / 32;
-    c.H = 1;
-    while (c.WK * c.H * 2 <= kGsMaxConsumerWarps && c.H < 16) c.H *= 2;
-    const double row_bytes = 0.5625 * static_cast<double>(K);
-    int rpw = static_cast<int>(32768.0 / (c.H * row_bytes));
-    c.RPW = rpw >= 4 ? 4 : rpw >= 2 ? 2 : 1;
+    c.H = kGsMaxConsumerWarps / c.WK;
+    if (c.H < 1) c.H = 1;
+    const size_t row_bytes = static_cast<size_t>(K / 2 + K / 16);
+    c.RPW = 4;
+    while (c.RPW > 1 && 2 * static_cast<size_t>(c.H * c.RPW) * row_bytes > kGsRingBudget) c.RPW /= 2;
     c.RS = c.H * c.RPW;
-    const size_t stage = static_cast<size_t>(c.RS) * (K / 2 + K / 16);
-    int ns = static_cast<int>(kGsSmemBudget / stage);
-    c.NS = ns < 2 ? 2 : ns > 6 ? 6 : ns;
+    const size_t stage = static_cast<size_t>(c.RS) * row_bytes;
+    int ns = static_cast<int>(kGsRingBudget / stage);
+    c.NS = ns < 2 ? 2 : ns > 8 ? 8 : ns;
     c.threads = (c.WK * c.H + 1) * 32;
     c.grid = static_cast<int>(N < kNumSMs ? N : kNumSMs);
     c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
+    c.smem = 128 + static_cast<size_t>(c.NS) * stage + 1024 +
+             static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
     return c;
 }
 
 bool gemv_stream_ok(int nt, int64_t K) {
     if (nt < 1 || nt > 2 || K % 256 != 0) return false;
-    const int G = static_cast<int>(K / kGroup);
-    return (G + 31) / 32 <= 31;   // <= 1024 threads incl. the producer warp
+    const GsConfig c = gs_config(K, kNumSMs);
+    return c.threads <= 1024 && c.smem <= 200 * 1024;
 }
 
-template <int NT, int RPW>
+template <int NT, int RPW, int ZPF>
 static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c.grid);
@@ -257,30 +320,38 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (c.threads <= 544) {
-        auto k = gemv_stream_kernel<NT, RPW, 544, 2>;
+        auto k = gemv_stream_kernel<NT, RPW, ZPF, 544>;
         static bool set = false;
         if (!set) {
-            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
             if (e != cudaSuccess) return static_cast<int>(e);
             set = true;
         }
         return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
     }
-    auto k = gemv_stream_kernel<NT, RPW, 1024, 1>;
+    auto k = gemv_stream_kernel<NT, RPW, ZPF, 1024>;
     static bool set = false;
     if (!set) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
         if (e != cudaSuccess) return static_cast<int>(e);
         set = true;
     }
     return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
 }
 
+template <int NT, int ZPF>
+static int launch_gs_nt(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
+    switch (c.RPW) {
+        case 4: return launch_gs_t<NT, 4, ZPF>(a, c, pdl, stream);
+        case 2: return launch_gs_t<NT, 2, ZPF>(a, c, pdl, stream);
+        default: return launch_gs_t<NT, 1, ZPF>(a, c, pdl, stream);
+    }
+}
+
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                        const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
-    GsConfig c = gs_config(K, N);
-    c.smem = 128 + static_cast<size_t>(c.NS) * c.RS * (K / 2 + K / 16) +
-             static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
+    const GsConfig c = gs_config(K, N);
+    const int zpf = gs_zpf();
     for (int64_t t0 = 0; t0 < n; t0 += 2) {
         const int cnt = (n - t0) >= 2 ? 2 : 1;
         GsArgs a;
@@ -295,13 +366,8 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
         a.rows_cta_max = c.rows_cta_max;
         int rc;
-        if (cnt == 1) {
-            rc = c.RPW == 4 ? launch_gs_t<1, 4>(a, c, pdl, stream)
-               : c.RPW == 2 ? launch_gs_t<1, 2>(a, c, pdl, stream) : launch_gs_t<1, 1>(a, c, pdl, stream);
-        } else {
-            rc = c.RPW == 4 ? launch_gs_t<2, 4>(a, c, pdl, stream)
-               : c.RPW == 2 ? launch_gs_t<2, 2>(a, c, pdl, stream) : launch_gs_t<2, 1>(a, c, pdl, stream);
-        }
+        if (cnt == 1) rc = zpf ? launch_gs_nt<1, 1>(a, c, pdl, stream) : launch_gs_nt<1, 0>(a, c, pdl, stream);
+        else rc = zpf ? launch_gs_nt<2, 1>(a, c, pdl, stream) : launch_gs_nt<2, 0>(a, c, pdl, stream);
         if (rc != 0) return rc;
     }
     return 0;
