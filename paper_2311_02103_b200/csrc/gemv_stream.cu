@@ -146,7 +146,7 @@ __device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const u
     }
 }
 
-template <int NT, int RPW, int ZPF, int MAXT>
+template <int NT, int RPW, int ZPF, int FULLG, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) gemv_stream_kernel(const __grid_constant__ GsArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(MAXT, 1) gemv_stream_kernel(const __grid_const
                 for (int i = 0; i < RPW; ++i) {
                     const uint4 cw = lds128(stage + coff + i * cb_row);
                     uint16_t sbits = *reinterpret_cast<const uint16_t*>(stage + soff + i * sb_row);
-                    if (!gv) sbits = 0;                       // lanes past K: x = 0 and s = 0
+                    if (!FULLG && !gv) sbits = 0;             // lanes past K: x = 0 and s = 0
                     float o[NT];
                     row_dot<NT, ZPF>(cw, sbits, xr, m7x, o);
 #pragma unroll
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(MAXT, 1) gemv_stream_kernel(const __grid_const
 static int gs_zpf() {
     static int v = [] {
         const char* e = std::getenv("RELAX_Q4_GEMV_ZPF");
-        return (e && *e == '1') ? 1 : 0;
+        return (e && *e == '0') ? 0 : 1;   // factored zero point by default
     }();
     return v;
 }
@@ -288,6 +288,8 @@ static GsConfig gs_config(int64_t K, int64_t N) {
     if (c.H < 1) c.H = 1;
     const size_t row_bytes = static_cast<size_t>(K / 2 + K / 16);
     c.RPW = 4;
+    if (const char* e = std::getenv("RELAX_Q4_GS_H")) { const int v = std::atoi(e); if (v >= 1 && v * c.WK <= 31) c.H = v; }
+    if (const char* e = std::getenv("RELAX_Q4_GS_RPW")) { const int v = std::atoi(e); if (v == 1 || v == 2 || v == 4 || v == 8) c.RPW = v; }
     while (c.RPW > 1 && 2 * static_cast<size_t>(c.H * c.RPW) * row_bytes > kGsRingBudget) c.RPW /= 2;
     c.RS = c.H * c.RPW;
     const size_t stage = static_cast<size_t>(c.RS) * row_bytes;
@@ -307,7 +309,7 @@ bool gemv_stream_ok(int nt, int64_t K) {
     return c.threads <= 1024 && c.smem <= 200 * 1024;
 }
 
-template <int NT, int RPW, int ZPF>
+template <int NT, int RPW, int ZPF, int FULLG>
 static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c.grid);
@@ -320,7 +322,7 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (c.threads <= 544) {
-        auto k = gemv_stream_kernel<NT, RPW, ZPF, 544>;
+        auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 544>;
         static bool set = false;
         if (!set) {
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
@@ -329,7 +331,7 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
         }
         return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
     }
-    auto k = gemv_stream_kernel<NT, RPW, ZPF, 1024>;
+    auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 1024>;
     static bool set = false;
     if (!set) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
@@ -339,13 +341,20 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
     return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
 }
 
-template <int NT, int ZPF>
+template <int NT, int ZPF, int FULLG>
 static int launch_gs_nt(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
     switch (c.RPW) {
-        case 4: return launch_gs_t<NT, 4, ZPF>(a, c, pdl, stream);
-        case 2: return launch_gs_t<NT, 2, ZPF>(a, c, pdl, stream);
-        default: return launch_gs_t<NT, 1, ZPF>(a, c, pdl, stream);
+        case 8: return launch_gs_t<NT, 8, ZPF, FULLG>(a, c, pdl, stream);
+        case 4: return launch_gs_t<NT, 4, ZPF, FULLG>(a, c, pdl, stream);
+        case 2: return launch_gs_t<NT, 2, ZPF, FULLG>(a, c, pdl, stream);
+        default: return launch_gs_t<NT, 1, ZPF, FULLG>(a, c, pdl, stream);
     }
+}
+
+template <int NT, int ZPF>
+static int launch_gs_z(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
+    return (a.G % 32 == 0) ? launch_gs_nt<NT, ZPF, 1>(a, c, pdl, stream)
+                           : launch_gs_nt<NT, ZPF, 0>(a, c, pdl, stream);
 }
 
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
@@ -366,8 +375,8 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
         a.rows_cta_max = c.rows_cta_max;
         int rc;
-        if (cnt == 1) rc = zpf ? launch_gs_nt<1, 1>(a, c, pdl, stream) : launch_gs_nt<1, 0>(a, c, pdl, stream);
-        else rc = zpf ? launch_gs_nt<2, 1>(a, c, pdl, stream) : launch_gs_nt<2, 0>(a, c, pdl, stream);
+        if (cnt == 1) rc = zpf ? launch_gs_z<1, 1>(a, c, pdl, stream) : launch_gs_z<1, 0>(a, c, pdl, stream);
+        else rc = zpf ? launch_gs_z<2, 1>(a, c, pdl, stream) : launch_gs_z<2, 0>(a, c, pdl, stream);
         if (rc != 0) return rc;
     }
     return 0;
