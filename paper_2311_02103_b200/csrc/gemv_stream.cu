@@ -49,7 +49,17 @@ struct GsConfig {
 };
 
 constexpr int kGsMaxConsumerWarps = 16;   // consumer warps per CTA (one CTA per SM)
-constexpr size_t kGsRingBudget = 176 * 1024;
+// Ring budget per CTA: <= ~100 KB so that the next GEMV's CTA (programmatic
+// dependent launch) fits on the SM beside this one and prefetches its whole
+// share of weights while this kernel finishes.
+static size_t gs_ring_budget() {
+    static size_t v = [] {
+        const char* e = std::getenv("RELAX_Q4_GS_RING_KB");
+        const int kb = e ? std::atoi(e) : 0;
+        return static_cast<size_t>(kb >= 16 && kb <= 190 ? kb : 96) * 1024;
+    }();
+    return v;
+}
 
 __device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
@@ -147,7 +157,7 @@ __device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const u
 }
 
 template <int NT, int RPW, int ZPF, int FULLG, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) gemv_stream_kernel(const __grid_constant__ GsArgs a) {
+__global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kernel(const __grid_constant__ GsArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -290,10 +300,10 @@ static GsConfig gs_config(int64_t K, int64_t N) {
     c.RPW = 4;
     if (const char* e = std::getenv("RELAX_Q4_GS_H")) { const int v = std::atoi(e); if (v >= 1 && v * c.WK <= 31) c.H = v; }
     if (const char* e = std::getenv("RELAX_Q4_GS_RPW")) { const int v = std::atoi(e); if (v == 1 || v == 2 || v == 4 || v == 8) c.RPW = v; }
-    while (c.RPW > 1 && 2 * static_cast<size_t>(c.H * c.RPW) * row_bytes > kGsRingBudget) c.RPW /= 2;
+    while (c.RPW > 1 && 2 * static_cast<size_t>(c.H * c.RPW) * row_bytes > gs_ring_budget()) c.RPW /= 2;
     c.RS = c.H * c.RPW;
     const size_t stage = static_cast<size_t>(c.RS) * row_bytes;
-    int ns = static_cast<int>(kGsRingBudget / stage);
+    int ns = static_cast<int>(gs_ring_budget() / stage);
     c.NS = ns < 2 ? 2 : ns > 8 ? 8 : ns;
     c.threads = (c.WK * c.H + 1) * 32;
     c.grid = static_cast<int>(N < kNumSMs ? N : kNumSMs);
@@ -331,7 +341,7 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
         }
         return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
     }
-    auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 1024>;
+    auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 1024>;   // K > 16K: one CTA per SM
     static bool set = false;
     if (!set) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
