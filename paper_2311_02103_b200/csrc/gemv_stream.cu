@@ -27,6 +27,7 @@
 //     only the x loads and the y stores wait for the previous kernel.
 #include <cstdlib>
 #include "internal.h"
+#include "relax_q4.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
 
@@ -41,7 +42,25 @@ struct GsArgs {
     int K, G, WK, H, RS, NS;
     uint32_t stage_bytes;  // RS * (K/2 + K/16)
     int rows_cta_max;
+    uint32_t trace_seq;    // 0 = no trace, else launch sequence number
 };
+
+// ---- optional per-CTA timeline (RELAX_Q4_TRACE=1; include/relax_q4_debug.h)
+constexpr int kTraceMax = 1 << 16;                // records
+struct TraceRec { uint32_t seq, cta, smid, pad; uint64_t t0, t_wait, t_first, t_end; };
+__device__ TraceRec g_trace[kTraceMax];
+__device__ uint32_t g_trace_n;
+
+__device__ __forceinline__ uint64_t gtime() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
 
 struct GsConfig {
     int WK, H, RPW, RS, NS, threads, rows_cta_max, grid;
@@ -176,6 +195,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
     const uint32_t sb_row = static_cast<uint32_t>(a.K / 16);
     const uint32_t codes_stage = static_cast<uint32_t>(a.RS) * cb_row;
 
+    const uint64_t t_start = a.trace_seq ? gtime() : 0;
+    __shared__ uint64_t tr_wait, tr_first;
     if (threadIdx.x == 0) {
         for (int i = 0; i < a.NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], nwc); }
         fence_mbar_init();
@@ -210,6 +231,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         const int g = kw * 32 + lane;
         const bool gv = g < a.G;
         pdl_wait();
+        if (a.trace_seq && warp == 0 && lane == 0) tr_wait = gtime();
         uint4 xr[NT][4];
         float m7x[NT];
 #pragma unroll
@@ -240,6 +262,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         for (int r_base = 0; r_base < rows; r_base += a.RS) {
             const int nr = rows - r_base < a.RS ? rows - r_base : a.RS;
             mbar_wait(&full[slot], phase);
+            if (a.trace_seq && r_base == 0 && warp == 0 && lane == 0) tr_first = gtime();
             const uint8_t* stage = ring + static_cast<size_t>(slot) * a.stage_bytes;
             float acc[NT][RPW];
             if (h * RPW < nr) {                              // warp-uniform
@@ -280,6 +303,24 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
         a.y[static_cast<int64_t>(t) * a.N + row0 + rl] = __half_as_ushort(__float2half_rn(sum));
     }
+    if (a.trace_seq) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t i = atomicAdd(&g_trace_n, 1u);
+            if (i < kTraceMax) {
+                TraceRec r;
+                r.seq = a.trace_seq; r.cta = blockIdx.x; r.smid = smid(); r.pad = 0;
+                r.t0 = t_start; r.t_wait = tr_wait; r.t_first = tr_first; r.t_end = gtime();
+                g_trace[i] = r;
+            }
+        }
+    }
+}
+
+static uint32_t g_launch_seq = 0;
+static bool gs_trace() {
+    static bool v = [] { const char* e = std::getenv("RELAX_Q4_TRACE"); return e && *e == '1'; }();
+    return v;
 }
 
 static int gs_zpf() {
@@ -384,6 +425,7 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.WK = c.WK; a.H = c.H; a.RS = c.RS; a.NS = c.NS;
         a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
         a.rows_cta_max = c.rows_cta_max;
+        a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
         int rc;
         if (cnt == 1) rc = zpf ? launch_gs_z<1, 1>(a, c, pdl, stream) : launch_gs_z<1, 0>(a, c, pdl, stream);
         else rc = zpf ? launch_gs_z<2, 1>(a, c, pdl, stream) : launch_gs_z<2, 0>(a, c, pdl, stream);
@@ -393,3 +435,17 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
 }
 
 }  // namespace rq4
+
+extern "C" RELAX_API int relax_debug_trace_read(void* host, size_t max_records, size_t* n_records, int reset) {
+    uint32_t n = 0;
+    if (cudaMemcpyFromSymbol(&n, rq4::g_trace_n, sizeof n) != cudaSuccess) return RELAX_ERR_CUDA;
+    if (n > static_cast<uint32_t>(rq4::kTraceMax)) n = rq4::kTraceMax;
+    const size_t m = n < max_records ? n : max_records;
+    if (m && cudaMemcpyFromSymbol(host, rq4::g_trace, m * sizeof(rq4::TraceRec)) != cudaSuccess) return RELAX_ERR_CUDA;
+    if (n_records) *n_records = m;
+    if (reset) {
+        const uint32_t z = 0;
+        if (cudaMemcpyToSymbol(rq4::g_trace_n, &z, sizeof z) != cudaSuccess) return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
