@@ -78,7 +78,8 @@ enum relax_variant {
 };
 
 /* Flags for relax_q4_matmul_ex. */
-#define RELAX_FLAG_NO_PDL 1u  /* launch without programmatic dependent launch */
+#define RELAX_FLAG_NO_PDL 1u            /* launch without programmatic dependent launch */
+#define RELAX_FLAG_SPLIT_WORKSPACE 2u   /* TC split-K through the workspace, not a cluster */
 
 /* Upper-bound workspace plan (lifted workspace P:438-441).
  * Host only, pure: no CUDA call, no allocation.

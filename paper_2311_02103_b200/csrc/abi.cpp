@@ -37,13 +37,13 @@ static int choose_bn(int64_t n, int64_t N) {
     return t256 >= kNumSMs ? 256 : 128;
 }
 
-// Split-K factor.  Small n (<= 64) is HBM-bound: pick the split that best
-// fills whole waves (each split keeps >= 2 weight stages).  Larger n is
-// tensor-bound and split-K only adds partial-sum traffic, so split only when
+// Split-K factor.  Small n (<= 64) is HBM-bound: aim for about one CTA per
+// SM (RELAX_Q4_TC_CTAS_PER_SM scales the target), so that the next kernel's
+// CTAs fit beside this one (PDL) and every CTA streams a long K range.  Larger
+// n is tensor-bound and split-K only adds reduction work, so split only when
 // the tiles cover less than half a wave, and by at most 4.
 static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
-    const int64_t slots = static_cast<int64_t>(kNumSMs) * ctas_per_sm_tc(bn);
-    if (tiles >= slots) return 1;
+    (void)bn;
     if (n > 64) {
         if (tiles * 2 >= kNumSMs) return 1;
         int s = static_cast<int>((kNumSMs + tiles - 1) / tiles);
@@ -51,20 +51,21 @@ static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
         if (s > kt / 4) s = kt / 4 < 1 ? 1 : kt / 4;
         return s;
     }
-    int best = 1;
-    double best_eff = 0.0;
-    const int smax = kt / 2 < 16 ? (kt / 2 < 1 ? 1 : kt / 2) : 16;
-    for (int s = 1; s <= smax; ++s) {
-        const int64_t ctas = tiles * s;
-        const int64_t waves = (ctas + slots - 1) / slots;
-        const double eff = static_cast<double>(ctas) / static_cast<double>(waves * slots);
-        if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
-    }
-    return best;
+    static double f = [] {
+        const char* e = std::getenv("RELAX_Q4_TC_CTAS_PER_SM");
+        const double v = e ? std::atof(e) : 0.0;
+        return v > 0.1 && v <= 4.0 ? v : 1.0;
+    }();
+    const double target = f * kNumSMs;
+    int s = static_cast<int>(target / static_cast<double>(tiles) + 0.5);
+    if (s < 1) s = 1;
+    if (s > 2 * kMaxClusterSplit) s = 2 * kMaxClusterSplit;
+    if (s > kt) s = kt;
+    return s;
 }
 
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split, int force_bn,
-              Plan* out) {
+              Plan* out, bool force_ws) {
     if (n < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
     if (K % kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
     Plan p;
@@ -104,7 +105,10 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
             s = 1;
         }
         p.split = s;
-        p.ws_bytes = tc_workspace_bytes(n, N, p.bn, s);
+        // split-K partials: reduced in a thread-block cluster through DSMEM when
+        // the split fits a portable cluster (<= 8), else in the workspace.
+        p.cluster = (s > 1 && s <= 8 && !force_ws) ? 1 : 0;
+        p.ws_bytes = p.cluster ? 0 : tc_workspace_bytes(n, N, p.bn, s);
     } else {
         return RELAX_ERR_INVALID_ARG;
     }
@@ -169,8 +173,13 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
         return RELAX_ERR_ALIAS;
     Plan plan;
     // Without a workspace the schedule is workspace-free (split-K = 1).
-    const int fs = (ws_bytes == 0 && split_k == 0) ? 1 : split_k;
-    int rc = make_plan(n, K, N, variant, fs, bn, &plan);
+    const bool force_ws = (flags & RELAX_FLAG_SPLIT_WORKSPACE) != 0;
+    int rc = make_plan(n, K, N, variant, split_k, bn, &plan, force_ws);
+    if (rc == RELAX_OK && plan.ws_bytes > 0 && ws_bytes == 0 && !force_ws && split_k == 0) {
+        // no workspace given: fall back to the largest cluster-reduced split
+        int s = plan.split < 8 ? plan.split : 8;
+        rc = make_plan(n, K, N, variant, s, bn, &plan, false);
+    }
     if (rc != RELAX_OK) return rc;
     if (plan.ws_bytes > ws_bytes) return RELAX_ERR_WORKSPACE;
     rc = check_device();
@@ -205,7 +214,7 @@ int relax_plan_workspace(int64_t n_max, int64_t K, int64_t N, size_t* ws_bytes) 
     size_t best = 0;
     for (int64_t n = 1; n <= hi; ++n) {
         rq4::Plan p;
-        const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p);
+        const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
         if (rc != RELAX_OK) return rc;
         if (p.ws_bytes > best) best = p.ws_bytes;
     }
@@ -216,7 +225,7 @@ int relax_plan_workspace(int64_t n_max, int64_t K, int64_t N, size_t* ws_bytes) 
 int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile, int* split_k,
                          size_t* ws_bytes) {
     rq4::Plan p;
-    const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p);
+    const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
     if (rc != RELAX_OK) return rc;
     if (variant) *variant = p.variant;
     if (tile) *tile = p.variant == rq4::kVariantGemv ? p.nt : p.bn;

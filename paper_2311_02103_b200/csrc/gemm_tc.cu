@@ -12,17 +12,21 @@
 //                         scales (128 rows x 16 B) per 256-k stage
 //   warp 2   x producer : TMA of x (BN rows x 64 k, SW128) per 64-k sub-block;
 //                         out-of-range tokens / k are zero-filled by TMA
-//   warps 4-7 transform : thread m owns weight row m (= TMEM lane m); reads its
-//                         row's codes from SMEM, dequantises bit-exactly to
-//                         fp16 in registers and writes the A operand straight
-//                         into TMEM (tcgen05.st 32x32b) -- A never touches HBM
-//                         or SMEM in fp16
+//   warps 4-11 transform: warp (q, h), thread m = 32q + lane owns weight row m
+//                         (= TMEM lane m) and dequantises the 64-k sub-blocks of
+//                         parity h: reads its row's codes from SMEM, bit-exact
+//                         fp16 in registers, tcgen05.st 32x32b straight into a
+//                         TMEM A ring -- A never touches HBM or SMEM in fp16;
+//                         the first ring-full is done before x even arrives
 //   warp 1   MMA issuer : one thread issues tcgen05.mma.kind::f16 with A from
 //                         TMEM, B (x) from SMEM, fp32 D in TMEM
-//   warps 4-7 epilogue  : tcgen05.ld of D, fp32 -> fp16 RNE, store y; with
-//                         split-K, fp32 partials go to the workspace and the
-//                         last CTA of a tile (atomic ticket) sums them in fixed
-//                         split order -> deterministic.
+//   warps 4-7 epilogue  : tcgen05.ld of D, fp32 -> fp16 RNE, store y.
+//   split-K             : cluster mode -- the S CTAs of a tile form a thread-
+//                         block cluster and reduce through DSMEM in fixed rank
+//                         order; workspace mode (S > 8 or forced) -- fp32
+//                         partials in the caller's workspace, the last CTA of a
+//                         tile (atomic ticket) sums them in fixed split order.
+//                         Both deterministic.
 #include <cuda.h>
 #include <cstdio>
 #include "internal.h"
@@ -31,41 +35,48 @@
 
 namespace rq4 {
 
-constexpr int kTcThreads = 256;
+constexpr int kTcThreads = 384;        // 12 warps, see the role map above
 constexpr int kWStages = 4;            // 256-k codes+scales stages in flight
-constexpr int kAStages = 4;            // 64-k x / A sub-blocks in flight
 constexpr uint32_t kCodesStageBytes = kTcBM * (kTcWStageK / 2);     // 16 KB
 constexpr uint32_t kScalesStageBytes = kTcBM * (kTcWStageK / kGroup) * 2;  // 2 KB
+constexpr int kSubPerStage = kTcWStageK / kTcXStageK;                // 4
 
 struct TcArgs {
     int64_t n, K, N;
     uint16_t* y;
-    float* part;          // [split][n][N] fp32 partials (split > 1)
-    uint32_t* cnt;        // [tiles_m * tiles_n] tickets, zero between calls
+    float* part;          // workspace split-K: [split][n][N] fp32 partials
+    uint32_t* cnt;        // workspace split-K: per-tile tickets, zero between calls
     int split;
     int kt;               // number of 256-k W stages covering K
+    int cluster;          // 1: split-K partials reduced through DSMEM of the cluster
 };
 
 template <int BN>
 struct TcCfg {
+    static constexpr int kCtasPerSm = BN <= 64 ? 2 : 1;
+    static constexpr uint32_t kTmemCols = BN <= 64 ? 256 : 512;
+    static constexpr uint32_t kA0 = (BN < 32 ? 32 : BN);                 // TMEM col of A ring
+    static constexpr int kAStages = static_cast<int>((kTmemCols - kA0) / 32);   // 64-k A slots
     static constexpr uint32_t kXStageBytes = BN * 128;
-    static constexpr uint32_t kA0 = (BN < 32 ? 32 : BN);                   // TMEM col of A ring
-    static constexpr uint32_t kColsNeeded = kA0 + kAStages * 32;
-    static constexpr uint32_t kTmemCols = kColsNeeded <= 32 ? 32 : kColsNeeded <= 64 ? 64
-                                        : kColsNeeded <= 128 ? 128 : kColsNeeded <= 256 ? 256 : 512;
+    static constexpr uint32_t kXBudget = BN <= 64 ? 32 * 1024 : 128 * 1024;
+    static constexpr int kXRaw = static_cast<int>(kXBudget / kXStageBytes);
+    static constexpr int kXStages = kXRaw < kAStages ? kXRaw : kAStages;
     static constexpr uint32_t kOffCodes = 0;
     static constexpr uint32_t kOffScales = kOffCodes + kWStages * kCodesStageBytes;
     static constexpr uint32_t kOffX = kOffScales + kWStages * kScalesStageBytes;
-    static constexpr uint32_t kOffBar = kOffX + kAStages * kXStageBytes;
-    static constexpr uint32_t kNumBars = 2 * kWStages + 2 * kAStages + 1;
+    static constexpr uint32_t kOffBar = kOffX + kXStages * kXStageBytes;
+    static constexpr uint32_t kNumBars = 2 * kWStages + 2 * kAStages + 2 * kXStages + 1;
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
+    static_assert(128u * BN * 4u <= kOffBar, "cluster reduction buffer must fit in the rings");
 };
 
 template <int BN>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, TcCfg<BN>::kCtasPerSm)
 tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
              const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TcArgs a) {
     using Cfg = TcCfg<BN>;
+    constexpr int AS = Cfg::kAStages;
+    constexpr int XS = Cfg::kXStages;
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for the 128B-swizzle atoms.
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -74,10 +85,12 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     uint8_t* x_sm = smem + Cfg::kOffX;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kOffBar);
     uint64_t* w_full = bars;
-    uint64_t* w_empty = bars + kWStages;
-    uint64_t* ax_full = bars + 2 * kWStages;
-    uint64_t* ax_empty = bars + 2 * kWStages + kAStages;
-    uint64_t* acc_full = bars + 2 * kWStages + 2 * kAStages;
+    uint64_t* w_empty = w_full + kWStages;
+    uint64_t* a_full = w_empty + kWStages;
+    uint64_t* a_empty = a_full + AS;
+    uint64_t* x_full = a_empty + AS;
+    uint64_t* x_empty = x_full + XS;
+    uint64_t* acc_full = x_empty + XS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
     uint32_t* flag_slot = tmem_slot + 1;
 
@@ -89,13 +102,14 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const int ks0 = static_cast<int>(static_cast<int64_t>(z) * a.kt / a.split);
     const int ks1 = static_cast<int>(static_cast<int64_t>(z + 1) * a.kt / a.split);
     const int nst = ks1 - ks0;              // >= 1 (split <= kt)
-    const int nsub = nst * (kTcWStageK / kTcXStageK);
+    const int nsub = nst * kSubPerStage;
 
     pdl_launch_dependents();
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 4); }
-        for (int i = 0; i < kAStages; ++i) { mbar_init(&ax_full[i], 1 + 4); mbar_init(&ax_empty[i], 1); }
+        for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 8); }
+        for (int i = 0; i < AS; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
+        for (int i = 0; i < XS; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
         mbar_init(acc_full, 1);
         fence_mbar_init();
     }
@@ -130,17 +144,17 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             }
         }
     } else if (warp == 2) {
-        // ---------------- x producer
+        // ---------------- x producer: the only input that depends on the previous kernel
         if (elect_one()) {
             pdl_wait();
             const uint64_t pol = policy_evict_last();
             for (int j = 0; j < nsub; ++j) {
-                const int slot = j % kAStages;
-                const uint32_t ph = (j / kAStages) & 1;
-                mbar_wait(&ax_empty[slot], ph ^ 1);
-                mbar_arrive_expect_tx(&ax_full[slot], Cfg::kXStageBytes);
-                const int32_t k = (ks0 * (kTcWStageK / kTcXStageK) + j) * kTcXStageK;
-                tma_load_2d(x_sm + slot * Cfg::kXStageBytes, &tm_x, &ax_full[slot], k,
+                const int slot = j % XS;
+                const uint32_t ph = (j / XS) & 1;
+                mbar_wait(&x_empty[slot], ph ^ 1);
+                mbar_arrive_expect_tx(&x_full[slot], Cfg::kXStageBytes);
+                const int32_t k = (ks0 * kSubPerStage + j) * kTcXStageK;
+                tma_load_2d(x_sm + slot * Cfg::kXStageBytes, &tm_x, &x_full[slot], k,
                             static_cast<int32_t>(n0), pol);
             }
         }
@@ -149,24 +163,30 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (elect_one()) {
             constexpr uint32_t idesc = idesc_f16_f32(kTcBM, BN);
             for (int j = 0; j < nsub; ++j) {
-                const int slot = j % kAStages;
-                const uint32_t ph = (j / kAStages) & 1;
-                mbar_wait(&ax_full[slot], ph);
+                const int as = j % AS;
+                const int xs = j % XS;
+                mbar_wait(&a_full[as], (j / AS) & 1);
+                mbar_wait(&x_full[xs], (j / XS) & 1);
                 tc_fence_after();
-                const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + slot * Cfg::kXStageBytes));
+                const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * Cfg::kXStageBytes));
 #pragma unroll
                 for (int kk = 0; kk < kTcXStageK / 16; ++kk) {
-                    tc_mma_ts(tmem_base, tmem_base + Cfg::kA0 + slot * 32 + kk * 8,
+                    tc_mma_ts(tmem_base, tmem_base + Cfg::kA0 + as * 32 + kk * 8,
                               bdesc + static_cast<uint64_t>(kk * 2),  // +32 B along K in the atom
                               idesc, (j | kk) != 0 ? 1u : 0u);
                 }
-                tc_commit(&ax_empty[slot]);
+                tc_commit(&a_empty[as]);
+                tc_commit(&x_empty[xs]);
             }
             tc_commit(acc_full);
         }
     } else if (warp >= 4) {
-        // ---------------- transform: dequantise row m into the TMEM A ring
-        const int q = warp & 3;
+        // ---------------- transform: 8 warps; warp (q, h) dequantises rows 32q..32q+31
+        // of the sub-blocks with parity h into the TMEM A ring.  Slots are free
+        // up front, so the first AS sub-blocks are dequantised before x arrives.
+        const int tw = warp - 4;
+        const int q = tw & 3;
+        const int h = tw >> 2;
         const int m = q * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         for (int i = 0; i < nst; ++i) {
@@ -176,13 +196,15 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             const uint4 sv = *reinterpret_cast<const uint4*>(scales_sm + ws * kScalesStageBytes + m * 16);
             const uint32_t sw[4] = {sv.x, sv.y, sv.z, sv.w};     // 8 scales, 2 per word
 #pragma unroll
-            for (int sub = 0; sub < kTcWStageK / kTcXStageK; ++sub) {
-                const int j = i * (kTcWStageK / kTcXStageK) + sub;
-                const int as = j % kAStages;
+            for (int u = 0; u < 2; ++u) {
+                const int sub = h + 2 * u;
+                const int j = i * kSubPerStage + sub;
+                const int as = j % AS;
                 const uint4 c0 = *reinterpret_cast<const uint4*>(crow + (((2 * sub) ^ (m & 7)) << 4));
                 const uint4 c1 = *reinterpret_cast<const uint4*>(crow + (((2 * sub + 1) ^ (m & 7)) << 4));
-                const __half s_lo = __ushort_as_half(lo16(sw[sub]));   // group 2*sub
-                const __half s_hi = __ushort_as_half(hi16(sw[sub]));   // group 2*sub+1
+                const uint32_t swu = sub == 0 ? sw[0] : sub == 1 ? sw[1] : sub == 2 ? sw[2] : sw[3];
+                const __half s_lo = __ushort_as_half(lo16(swu));   // group 2*sub
+                const __half s_hi = __ushort_as_half(hi16(swu));   // group 2*sub+1
                 const __half2 s2a = __halves2half2(s_lo, s_lo);
                 const __half2 s2b = __halves2half2(s_hi, s_hi);
                 uint32_t v[32];
@@ -197,74 +219,118 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                     dequant_word_natural(c1.z, s2b, o); v[24] = o[0]; v[25] = o[1]; v[26] = o[2]; v[27] = o[3];
                     dequant_word_natural(c1.w, s2b, o); v[28] = o[0]; v[29] = o[1]; v[30] = o[2]; v[31] = o[3];
                 }
-                mbar_wait(&ax_empty[as], ((j / kAStages) & 1) ^ 1);
+                mbar_wait(&a_empty[as], ((j / AS) & 1) ^ 1);
                 tc_fence_after();
                 tmem_st_32x32b_x32(tmem_base + lane_base + Cfg::kA0 + as * 32, v);
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&ax_full[as]);
+                if (lane == 0) mbar_arrive(&a_full[as]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&w_empty[ws]);
         }
+    }
 
-        // ---------------- epilogue
-        mbar_wait(acc_full, 0);
-        tc_fence_after();
-        pdl_wait();
-        const int64_t row = m0 + m;
-        const bool row_ok = row < a.N;
-        const bool split = a.split > 1;
+    // ------------------------------------------------------------ epilogue
+    const bool epi = warp >= 4 && warp < 8;          // TMEM lanes 32q..32q+31
+    const int q = warp & 3;
+    const int m = q * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const int64_t row = m0 + m;
+    const bool row_ok = row < a.N;
+    if (a.split == 1 || !a.cluster) {
+        if (epi) {
+            mbar_wait(acc_full, 0);
+            tc_fence_after();
+            pdl_wait();
+            const bool split = a.split > 1;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t v[16];
-            tmem_ld_32x32b_x16(tmem_base + lane_base + c0, v);
-            tc_wait_ld();
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tmem_base + lane_base + c0, v);
+                tc_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int64_t tok = n0 + c0 + i;
-                if (row_ok && tok < a.n) {
-                    const float f = __uint_as_float(v[i]);
-                    if (split) a.part[(static_cast<int64_t>(z) * a.n + tok) * a.N + row] = f;
-                    else a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(f));
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t tok = n0 + c0 + i;
+                    if (row_ok && tok < a.n) {
+                        const float f = __uint_as_float(v[i]);
+                        if (split) a.part[(static_cast<int64_t>(z) * a.n + tok) * a.N + row] = f;
+                        else a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(f));
+                    }
                 }
             }
-        }
-        if (split) {
-            __threadfence();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (warp == 4 && lane == 0) {
-                const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;
-                const uint32_t old = atomicInc(a.cnt + tile, static_cast<uint32_t>(a.split - 1));
-                *flag_slot = (old == static_cast<uint32_t>(a.split - 1)) ? 1u : 0u;
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (*flag_slot) {
+            if (split) {
+                // workspace split-K: the last CTA of the tile (atomic ticket) sums
+                // the partials in fixed split order.
                 __threadfence();
-                if (row_ok) {
-                    // fixed split order s = 0..S-1 -> deterministic; 8 tokens of
-                    // independent loads in flight per thread.
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (warp == 4 && lane == 0) {
+                    const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;
+                    const uint32_t old = atomicInc(a.cnt + tile, static_cast<uint32_t>(a.split - 1));
+                    *flag_slot = (old == static_cast<uint32_t>(a.split - 1)) ? 1u : 0u;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (*flag_slot) {
+                    __threadfence();
+                    if (row_ok) {
 #pragma unroll 1
-                    for (int c0 = 0; c0 < BN; c0 += 8) {
-                        float sum[8];
+                        for (int c0 = 0; c0 < BN; c0 += 8) {
+                            float sum[8];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) sum[u] = 0.f;
-                        for (int s = 0; s < a.split; ++s) {
-                            const float* ps = a.part + (static_cast<int64_t>(s) * a.n + n0 + c0) * a.N + row;
+                            for (int u = 0; u < 8; ++u) sum[u] = 0.f;
+                            for (int s = 0; s < a.split; ++s) {
+                                const float* ps = a.part + (static_cast<int64_t>(s) * a.n + n0 + c0) * a.N + row;
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                if (n0 + c0 + u < a.n) sum[u] += __ldcg(ps + static_cast<int64_t>(u) * a.N);
-                        }
+                                for (int u = 0; u < 8; ++u)
+                                    if (n0 + c0 + u < a.n) sum[u] += __ldcg(ps + static_cast<int64_t>(u) * a.N);
+                            }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const int64_t tok = n0 + c0 + u;
-                            if (tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(sum[u]));
+                            for (int u = 0; u < 8; ++u) {
+                                const int64_t tok = n0 + c0 + u;
+                                if (tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(sum[u]));
+                            }
                         }
                     }
                 }
             }
         }
+    } else {
+        // Cluster split-K: each CTA parks its fp32 accumulator tile in its own
+        // shared memory ([BN][128], reusing the drained rings), then CTA r of the
+        // cluster sums element range r of the tile over all S CTAs through
+        // distributed shared memory in fixed rank order (deterministic, no HBM
+        // workspace).
+        float* red = reinterpret_cast<float*>(smem);
+        if (epi) {
+            mbar_wait(acc_full, 0);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tmem_base + lane_base + c0, v);
+                tc_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) red[(c0 + i) * kTcBM + m] = __uint_as_float(v[i]);
+            }
+        }
+        cluster_arrive_release();
+        cluster_wait_acquire();
+        pdl_wait();
+        const uint32_t S = static_cast<uint32_t>(a.split);
+        const uint32_t r = cluster_ctarank();
+        constexpr uint32_t E = kTcBM * BN;
+        const uint32_t e0 = r * E / S, e1 = (r + 1) * E / S;
+        const uint32_t red_addr = smem_u32(red);
+        for (uint32_t e = e0 + threadIdx.x; e < e1; e += kTcThreads) {
+            float sum = 0.f;
+            for (uint32_t s = 0; s < S; ++s) sum += ld_dsmem_f32(mapa_shared(red_addr + e * 4u, s));
+            const int64_t tok = n0 + static_cast<int64_t>(e / kTcBM);
+            const int64_t rr = m0 + static_cast<int64_t>(e % kTcBM);
+            if (tok < a.n && rr < a.N) a.y[tok * a.N + rr] = __half_as_ushort(__float2half_rn(sum));
+        }
+        cluster_arrive_release();
+        cluster_wait_acquire();
     }
 
     tc_fence_before();
@@ -321,6 +387,8 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
         cudaError_t e = cudaFuncSetAttribute(tc_q4_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(Cfg::kSmemBytes));
         if (e != cudaSuccess) return static_cast<int>(e);
+        e = cudaFuncSetAttribute(tc_q4_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return static_cast<int>(e);
         attr_set = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -329,11 +397,18 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
     cfg.blockDim = dim3(kTcThreads);
     cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (a.cluster && a.split > 1) {
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 1;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = static_cast<unsigned>(a.split);
+        cfg.numAttrs = 2;
+    }
     return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN>, mw, ms, mx, a));
 }
 
@@ -361,7 +436,8 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.split = plan.split;
     a.kt = static_cast<int>((K + kTcWStageK - 1) / kTcWStageK);
     a.part = nullptr; a.cnt = nullptr;
-    if (plan.split > 1) {
+    a.cluster = plan.cluster;
+    if (plan.split > 1 && !plan.cluster) {
         a.cnt = static_cast<uint32_t*>(ws);
         a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes);
     }

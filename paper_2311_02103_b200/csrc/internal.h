@@ -15,6 +15,7 @@ constexpr int kTcWStageK = 256;     // k per weight (codes+scales) TMA stage
 constexpr int kTcXStageK = 64;      // k per x TMA stage / A sub-block (4 MMAs)
 constexpr size_t kTicketBytes = 4096;  // split-K tickets: fixed region at workspace offset 0
 constexpr int64_t kMaxSplitTiles = kTicketBytes / 4;
+constexpr int kMaxClusterSplit = 16;   // non-portable cluster size limit on sm_100
 
 enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2 };
 
@@ -23,6 +24,7 @@ struct Plan {
     int nt = 0;          // GEMV: tokens per launch
     int bn = 0;          // TC: token tile (MMA N)
     int split = 1;       // TC: split-K factor
+    int cluster = 0;     // TC: split-K reduced in a thread-block cluster (DSMEM), no workspace
     int grid = 0;
     size_t ws_bytes = 0; // workspace bytes this plan needs
 };
@@ -30,7 +32,7 @@ struct Plan {
 // Host-pure dispatch (a1): variant, tiles, split-K and workspace for (n,K,N).
 // `force_variant` / `force_split` / `force_bn` override (0 = choose).
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split,
-              int force_bn, Plan* out);
+              int force_bn, Plan* out, bool force_ws);
 size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split);
 int gemv_max_n();                   // GEMV/TC threshold (env RELAX_Q4_GEMV_MAX_N)
 bool gemv_fits(int nt, int64_t K);

@@ -32,6 +32,7 @@ STATUS = {
 }
 VARIANT_AUTO, VARIANT_GEMV, VARIANT_TC = 0, 1, 2
 FLAG_NO_PDL = 1
+FLAG_SPLIT_WORKSPACE = 2
 
 # every symbol include/relax_q4.h declares
 EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",

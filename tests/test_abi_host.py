@@ -74,12 +74,16 @@ def test_validation_codes(L):
 
 
 def test_workspace_too_small_is_reported(L):
-    # n=16 on a 4096x4096 weight uses split-K: a 16-byte workspace is too small
-    sched = ops.query_schedule(16, 4096, 4096)
-    assert sched["variant"] == "tc" and sched["split_k"] > 1 and sched["ws_bytes"] > 16
-    assert call(L, n=16, K=4096, N=4096, y=A + 64 * MB, ws=A + 128 * MB, wsb=16) == 5
-    # without a workspace the schedule is workspace-free, so it proceeds
-    assert call(L, n=16, K=4096, N=4096, y=A + 64 * MB) == 6
+    # n=16 on a skinny 8192x1024 weight (8 row tiles) splits K 18 ways: more
+    # than a portable cluster, so the partials go through the workspace and a
+    # 16-byte workspace is too small
+    sched = ops.query_schedule(16, 8192, 1024)
+    assert sched["variant"] == "tc" and sched["split_k"] > 8 and sched["ws_bytes"] > 16
+    assert call(L, n=16, K=8192, N=1024, y=A + 64 * MB, ws=A + 128 * MB, wsb=16) == 5
+    # without a workspace the schedule is workspace-free (cluster split), so it proceeds
+    assert call(L, n=16, K=8192, N=1024, y=A + 64 * MB) == 6
+    # 4096x4096 at n=16 splits within a cluster: no workspace at all
+    assert ops.query_schedule(16, 4096, 4096)["ws_bytes"] == 0
     # forced TC on a K that is not a multiple of 256
     assert L.relax_q4_matmul_ex(A, 16, 4128, 256, A + 8 * MB, A + 16 * MB, A + 64 * MB, 0, 0,
                                 2, 0, 0, 0, None) == 2

@@ -23,17 +23,17 @@ def _built():
     ops.lib()
 
 
-def run(x_bits, packed, scales, variant=0, split_k=0, bn=0, ws_n_max=None):
+def run(x_bits, packed, scales, variant=0, split_k=0, bn=0, ws_n_max=None, flags=0):
     x = dev_x(x_bits)
     pw, sc = dev_weights(packed, scales)
     n, K = x.shape
     N = pw.shape[0]
     ws = None
-    if split_k > 1 or ws_n_max:
+    if (split_k > 1 and flags & ops.FLAG_SPLIT_WORKSPACE) or ws_n_max:
         nb = max(ops.plan_workspace(ws_n_max or n, K, N), split_k * n * N * 4 + 4096)
         ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
     y = torch.full((n, N), float("nan"), dtype=torch.float16, device="cuda")
-    ops.q4_matmul_ex(x, pw, sc, y=y, ws=ws, variant=variant, split_k=split_k, bn=bn)
+    ops.q4_matmul_ex(x, pw, sc, y=y, ws=ws, variant=variant, split_k=split_k, bn=bn, flags=flags)
     torch.cuda.synchronize()
     return host_bits(y)
 
@@ -76,14 +76,17 @@ def test_config1_auto(kind, n):
     assert_within_tol(y, r, f"c1 {kind} n={n}")
 
 
-VARIANTS = [("gemv", 1, 0, 0), ("tc16", 2, 1, 16), ("tc32", 2, 1, 32), ("tc64", 2, 1, 64),
-            ("tc128", 2, 1, 128), ("tc256", 2, 1, 256), ("tc16s3", 2, 3, 16), ("tc64s2", 2, 2, 64),
-            ("tc128s2", 2, 2, 128)]
+WSF = 2   # RELAX_FLAG_SPLIT_WORKSPACE
+VARIANTS = [("gemv", 1, 0, 0, 0), ("tc16", 2, 1, 16, 0), ("tc32", 2, 1, 32, 0), ("tc64", 2, 1, 64, 0),
+            ("tc128", 2, 1, 128, 0), ("tc256", 2, 1, 256, 0),
+            ("tc16s3c", 2, 3, 16, 0), ("tc64s2c", 2, 2, 64, 0), ("tc128s2c", 2, 2, 128, 0),
+            ("tc256s3c", 2, 3, 256, 0),
+            ("tc16s3w", 2, 3, 16, WSF), ("tc64s2w", 2, 2, 64, WSF), ("tc128s2w", 2, 2, 128, WSF)]
 
 
-@pytest.mark.parametrize("name,variant,split,bn", VARIANTS)
+@pytest.mark.parametrize("name,variant,split,bn,flags", VARIANTS)
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 9, 16, 17, 33, 64, 100, 129, 257, 300])
-def test_every_variant_ragged(name, variant, split, bn, n):
+def test_every_variant_ragged(name, variant, split, bn, flags, n):
     """Several M tiles and a ragged tail (N = 328 = 2*128 + 72), 3 weight
     stages of 256 k (K = 768), ragged token tiles."""
     if name == "gemv" and n > 17:
@@ -92,12 +95,12 @@ def test_every_variant_ragged(name, variant, split, bn, n):
     packed, scales = inputs.realistic_weights(2000, K, N)
     x = inputs.activations(7 + n, n, K)
     r = oracle.matmul_f64(x, packed, scales, K, N)
-    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn, flags=flags)
     assert_within_tol(y, r, f"{name} n={n}")
 
 
-@pytest.mark.parametrize("name,variant,split,bn", VARIANTS)
-def test_one_hot_extraction_bitwise(name, variant, split, bn):
+@pytest.mark.parametrize("name,variant,split,bn,flags", VARIANTS)
+def test_one_hot_extraction_bitwise(name, variant, split, bn, flags):
     """x row i = e_{k_i} -> y[i,:] == W[k_i,:] bitwise (exact product, exact
     zero sums, one rounding of an fp16 value)."""
     K, N = 512, 256
@@ -107,13 +110,13 @@ def test_one_hot_extraction_bitwise(name, variant, split, bn):
     for i, k in enumerate(ks):
         x[i, k] = 0x3C00
     W = oracle.dequant(packed, scales, K, N)          # [N][K]
-    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn, flags=flags)
     for i, k in enumerate(ks):
         assert np.array_equal(y[i], W[:, k]), f"{name}: row for k={k}"
 
 
-@pytest.mark.parametrize("name,variant,split,bn", VARIANTS)
-def test_identity_scale_integer_exact(name, variant, split, bn):
+@pytest.mark.parametrize("name,variant,split,bn,flags", VARIANTS)
+def test_identity_scale_integer_exact(name, variant, split, bn, flags):
     """scales = 1, x in {-1,0,1}: every partial sum is an integer < 2^24, so y
     is exact in any summation order."""
     K, N, n = 1024, 200, 12
@@ -124,13 +127,13 @@ def test_identity_scale_integer_exact(name, variant, split, bn):
     x = xi.astype(np.float16).view(np.uint16)
     r = oracle.matmul_f64(x, packed, scales, K, N)
     assert np.all(np.abs(r) <= 2048)
-    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn, flags=flags)
     assert np.array_equal(y.view(np.float16).astype(np.float64), r)
 
 
 @pytest.mark.parametrize("case", ["codes7", "scales0", "x0"])
-@pytest.mark.parametrize("name,variant,split,bn", VARIANTS[:3])
-def test_zero_invariants(case, name, variant, split, bn):
+@pytest.mark.parametrize("name,variant,split,bn,flags", VARIANTS[:3])
+def test_zero_invariants(case, name, variant, split, bn, flags):
     K, N, n = 512, 256, 5
     packed, scales = inputs.stress_weights(2200, K, N)
     x = inputs.activations(2201, n, K)
@@ -140,7 +143,7 @@ def test_zero_invariants(case, name, variant, split, bn):
         scales = np.zeros_like(scales)
     else:
         x = np.zeros_like(x)
-    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn)
+    y = run(x, packed, scales, variant=variant, split_k=split, bn=bn, flags=flags)
     if case == "codes7" and name == "gemv":
         # The GEMV factors the zero point (sum (q-7)x = sum qx - 7 sum x,
         # DESIGN.md §3 reading 6): for all-7 codes it leaves an fp32 rounding
@@ -237,14 +240,16 @@ def test_cuda_graph_capture_every_variant():
 
 def test_workspace_reused_across_calls():
     """One zero-filled, plan-sized workspace serves a sequence of split-K calls
-    of different n (the tickets reset themselves), each within tolerance."""
-    K, N = 4096, 4096
+    of different n (the tickets reset themselves), each within tolerance.
+    8192x1024 (8 row tiles) splits K more than a portable cluster, so the
+    automatic schedule reduces through the workspace."""
+    K, N = 8192, 1024
     ws = ops.workspace(64, K, N)
     assert ws is not None
     packed, scales = inputs.realistic_weights(6001, K, N)
     pw, sc = dev_weights(packed, scales)
-    cols = np.arange(0, N, 97)
-    for n in (16, 17, 40, 64, 16, 33):
+    cols = np.arange(0, N, 37)
+    for n in (16, 17, 40, 64, 16, 33, 5):
         xb = inputs.activations(n, n, K)
         y = host_bits(ops.q4_matmul(dev_x(xb), pw, sc, ws=ws))
         r = oracle.matmul_cols_f64(xb, packed, scales, K, cols)
