@@ -22,6 +22,8 @@
 //     griddepcontrol.wait (weights never depend on the previous kernel), so
 //     back-to-back GEMVs overlap their latency ramps.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include "internal.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
@@ -239,7 +241,16 @@ static int launch_gemv_nt(const GemvArgs& a, bool pdl, cudaStream_t stream) {
 
 int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                 const uint16_t* s, uint16_t* y, int nt, bool pdl, cudaStream_t stream) {
-    // Streamed kernel (gemv_stream.cu) for the decode shapes it supports.
+    // Lane-per-row kernel (gemv_row.cu) or the group-per-lane streamed kernel
+    // (gemv_stream.cu) for the decode shapes they support.
+    static int impl = [] {
+        const char* e = std::getenv("RELAX_Q4_GEMV_IMPL");
+        if (e && std::strcmp(e, "stream") == 0) return 1;
+        if (e && std::strcmp(e, "row") == 0) return 2;
+        return 0;
+    }();
+    if (n == 1 && impl != 1 && gemv_row_ok(K) && impl == 2)
+        return launch_gemv_row(x, n, K, N, w, s, y, pdl, stream);
     if (nt <= 2 && gemv_stream_ok(nt, K) && N >= 1)
         return launch_gemv_stream(x, n, K, N, w, s, y, pdl, stream);
     if (nt < 1 || nt > kGemvMaxNT) nt = kGemvMaxNT;

@@ -45,6 +45,9 @@ int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                        const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 bool gemv_stream_ok(int nt, int64_t K);
+int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+                    const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
+bool gemv_row_ok(int64_t K);
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
               const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
               cudaStream_t stream);
