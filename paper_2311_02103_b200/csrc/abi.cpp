@@ -20,7 +20,7 @@ int gemv_max_n() {
             const int x = std::atoi(e);
             if (x >= 0) return x;
         }
-        return 4;   // measured crossover: DESIGN.md §6
+        return 2;   // measured crossover (profiles/sweep_cross_r01.jsonl): DESIGN.md §6
     }();
     return v;
 }
@@ -59,7 +59,7 @@ static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
     const double target = f * kNumSMs;
     int s = static_cast<int>(target / static_cast<double>(tiles) + 0.5);
     if (s < 1) s = 1;
-    if (s > 2 * kMaxClusterSplit) s = 2 * kMaxClusterSplit;
+    if (s > 8) s = 8;            // portable cluster: DSMEM reduction, no workspace
     if (s > kt) s = kt;
     return s;
 }

@@ -74,15 +74,15 @@ def test_validation_codes(L):
 
 
 def test_workspace_too_small_is_reported(L):
-    # n=16 on a skinny 8192x1024 weight (8 row tiles) splits K 18 ways: more
-    # than a portable cluster, so the partials go through the workspace and a
-    # 16-byte workspace is too small
+    # a forced split-K through the workspace (RELAX_FLAG_SPLIT_WORKSPACE) needs
+    # split * n * N * 4 B + tickets: a 16-byte workspace is too small
+    assert L.relax_q4_matmul_ex(A, 16, 8192, 1024, A + 8 * MB, A + 16 * MB, A + 64 * MB,
+                                A + 128 * MB, 16, 2, 8, 16, 2, None) == 5
+    # the automatic schedule splits K inside a thread-block cluster (DSMEM
+    # reduction): no workspace at all, so a workspace-free call proceeds
     sched = ops.query_schedule(16, 8192, 1024)
-    assert sched["variant"] == "tc" and sched["split_k"] > 8 and sched["ws_bytes"] > 16
-    assert call(L, n=16, K=8192, N=1024, y=A + 64 * MB, ws=A + 128 * MB, wsb=16) == 5
-    # without a workspace the schedule is workspace-free (cluster split), so it proceeds
+    assert sched["variant"] == "tc" and sched["split_k"] > 1 and sched["ws_bytes"] == 0
     assert call(L, n=16, K=8192, N=1024, y=A + 64 * MB) == 6
-    # 4096x4096 at n=16 splits within a cluster: no workspace at all
     assert ops.query_schedule(16, 4096, 4096)["ws_bytes"] == 0
     # forced TC on a K that is not a multiple of 256
     assert L.relax_q4_matmul_ex(A, 16, 4128, 256, A + 8 * MB, A + 16 * MB, A + 64 * MB, 0, 0,
@@ -131,6 +131,8 @@ def test_dispatch_shape_specialisation():
     """n decides the variant: GEMV at decode, tensor cores for
     prefill; K % 256 != 0 keeps GEMV at any n."""
     assert ops.query_schedule(1, 4096, 4096)["variant"] == "gemv"
+    assert ops.query_schedule(2, 4096, 4096)["variant"] == "gemv"
+    assert ops.query_schedule(3, 4096, 4096)["variant"] == "tc"
     s = ops.query_schedule(4096, 4096, 4096)
     assert s["variant"] == "tc" and s["tile"] in (128, 256) and s["split_k"] == 1
     assert ops.query_schedule(512, 4128, 4096)["variant"] == "gemv"

@@ -239,18 +239,16 @@ def test_cuda_graph_capture_every_variant():
 
 
 def test_workspace_reused_across_calls():
-    """One zero-filled, plan-sized workspace serves a sequence of split-K calls
-    of different n (the tickets reset themselves), each within tolerance.
-    8192x1024 (8 row tiles) splits K more than a portable cluster, so the
-    automatic schedule reduces through the workspace."""
+    """One zero-filled workspace serves a sequence of forced workspace split-K
+    calls of different n (the tickets reset themselves), each within tolerance."""
     K, N = 8192, 1024
-    ws = ops.workspace(64, K, N)
-    assert ws is not None
-    packed, scales = inputs.realistic_weights(6001, K, N)
-    pw, sc = dev_weights(packed, scales)
+    pw_np, sc_np = inputs.realistic_weights(6001, K, N)
+    pw, sc = dev_weights(pw_np, sc_np)
+    ws = torch.zeros(4096 + 12 * 64 * N * 4, dtype=torch.uint8, device="cuda")
     cols = np.arange(0, N, 37)
-    for n in (16, 17, 40, 64, 16, 33, 5):
+    for n, split in ((16, 12), (17, 9), (40, 12), (64, 10), (16, 12), (33, 11), (5, 12)):
         xb = inputs.activations(n, n, K)
-        y = host_bits(ops.q4_matmul(dev_x(xb), pw, sc, ws=ws))
-        r = oracle.matmul_cols_f64(xb, packed, scales, K, cols)
-        assert_within_tol(y[:, cols], r, f"reuse n={n}")
+        y = host_bits(ops.q4_matmul_ex(dev_x(xb), pw, sc, ws=ws, variant=ops.VARIANT_TC,
+                                       split_k=split, flags=ops.FLAG_SPLIT_WORKSPACE))
+        r = oracle.matmul_cols_f64(xb, pw_np, sc_np, K, cols)
+        assert_within_tol(y[:, cols], r, f"reuse n={n} split={split}")
