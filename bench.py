@@ -54,13 +54,24 @@ def load_peaks():
             "src": "fallback"}
 
 
-def layer_set(workload: str):
+def layer_set(workload: str, fused: bool = False):
+    """The linears of one token.  fused=True stacks the rows of q/k/v and of
+    gate/up (the NK layout makes that a concatenation) into one call each --
+    same weights, same bytes, 4 dependent calls per layer instead of 7."""
     model = workload.rsplit("-", 1)[0]          # llama2-7b-decode -> llama2-7b
     spec = inputs.LLAMA_SETS[model]
     mats = []
     for li in range(spec["layers"]):
-        for name, K, N in spec["mats"]:
-            mats.append((f"L{li}.{name}", K, N))
+        if fused:
+            d = {name: (K, N) for name, K, N in spec["mats"]}
+            K = d["q"][0]
+            mats.append((f"L{li}.qkv", K, d["q"][1] + d["k"][1] + d["v"][1]))
+            mats.append((f"L{li}.o", *d["o"]))
+            mats.append((f"L{li}.gate_up", K, d["gate"][1] + d["up"][1]))
+            mats.append((f"L{li}.down", *d["down"]))
+        else:
+            for name, K, N in spec["mats"]:
+                mats.append((f"L{li}.{name}", K, N))
     K, N = spec["lm_head"]
     mats.append(("lm_head", K, N))
     return model, mats
@@ -136,7 +147,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     ops.lib()
-    model, mats = layer_set(args.workload)
+    model, mats = layer_set(args.workload, args.fused)
     n = args.n
     t_gen = time.time()
     # One realistic weight per distinct shape (seed 1000*config + index),
@@ -273,7 +284,8 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "q4f16 (int4 codes x fp16 -> fp32 accumulate, fp16 out)",
         "data": "synthetic (seeded realistic q4f16 weights, N(0,1) fp16 x)",
-        "config": {"workload": args.workload, "model": model, "tokens_per_step": n,
+        "config": {"workload": args.workload + ("-fused-qkv-gateup" if args.fused else ""),
+                   "model": model, "tokens_per_step": n,
                    "layers_linears": len(mats), "weight_bytes": int(sum(inputs.q4_bytes(K, N) for _, K, N in mats)),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "not flushed: per-step working set %.2f GB >> 126 MB L2" % (bytes_step / 1e9),
@@ -362,6 +374,8 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="tokens per step (decode: 1)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="stack q/k/v and gate/up rows into one call each (same weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.n is None:
