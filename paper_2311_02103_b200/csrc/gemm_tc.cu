@@ -43,6 +43,7 @@ constexpr int kSubPerStage = kTcWStageK / kTcXStageK;                // 4
 
 struct TcArgs {
     int64_t n, K, N;
+    const uint16_t* xptr;  // x fp16 [n][K] (the permuted-x producer reads it directly)
     uint16_t* y;
     float* part;          // workspace split-K: [split][n][N] fp32 partials
     uint32_t* cnt;        // workspace split-K: per-tile tickets, zero between calls
@@ -53,6 +54,10 @@ struct TcArgs {
 
 template <int BN>
 struct TcCfg {
+    // BN <= 64: x is staged by a whole warp with LDG + PRMT + STS into the
+    // SW128 B layout, k permuted to match dequant_word_interleaved (no byte
+    // permutes in the transform).  BN >= 128: x by TMA, natural k order.
+    static constexpr bool kPermX = BN <= 64;
     static constexpr int kCtasPerSm = BN <= 64 ? 2 : 1;
     static constexpr uint32_t kTmemCols = BN <= 64 ? 256 : 512;
     static constexpr uint32_t kA0 = (BN < 32 ? 32 : BN);                 // TMEM col of A ring
@@ -145,7 +150,31 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         }
     } else if (warp == 2) {
         // ---------------- x producer: the only input that depends on the previous kernel
-        if (elect_one()) {
+        if constexpr (Cfg::kPermX) {
+            pdl_wait();
+            for (int j = 0; j < nsub; ++j) {
+                const int slot = j % XS;
+                const uint32_t ph = (j / XS) & 1;
+                mbar_wait(&x_empty[slot], ph ^ 1);
+                const int64_t kbase = static_cast<int64_t>(ks0 * kSubPerStage + j) * kTcXStageK;
+                uint8_t* xt = x_sm + slot * Cfg::kXStageBytes;
+#pragma unroll
+                for (int it = 0; it < (BN * 8) / 32; ++it) {
+                    const int idx = it * 32 + lane;
+                    const int r = idx >> 3;           // token row in the tile
+                    const int c = idx & 7;            // 16-B chunk (8 k) in the 64-k row
+                    const int64_t tok = n0 + r;
+                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                    if (tok < a.n)
+                        v = *reinterpret_cast<const uint4*>(a.xptr + tok * a.K + kbase + c * 8);
+                    *reinterpret_cast<uint4*>(xt + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)) =
+                        permute_x8(v);
+                }
+                fence_proxy_async_smem();             // generic-proxy writes -> UMMA (async proxy)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&x_full[slot]);
+            }
+        } else if (elect_one()) {
             pdl_wait();
             const uint64_t pol = policy_evict_last();
             for (int j = 0; j < nsub; ++j) {
@@ -207,21 +236,18 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                 const __half s_hi = __ushort_as_half(hi16(swu));   // group 2*sub+1
                 const __half2 s2a = __halves2half2(s_lo, s_lo);
                 const __half2 s2b = __halves2half2(s_hi, s_hi);
-                uint32_t v[32];
-                {
-                    uint32_t o[4];
-                    dequant_word_natural(c0.x, s2a, o); v[0] = o[0]; v[1] = o[1]; v[2] = o[2]; v[3] = o[3];
-                    dequant_word_natural(c0.y, s2a, o); v[4] = o[0]; v[5] = o[1]; v[6] = o[2]; v[7] = o[3];
-                    dequant_word_natural(c0.z, s2a, o); v[8] = o[0]; v[9] = o[1]; v[10] = o[2]; v[11] = o[3];
-                    dequant_word_natural(c0.w, s2a, o); v[12] = o[0]; v[13] = o[1]; v[14] = o[2]; v[15] = o[3];
-                    dequant_word_natural(c1.x, s2b, o); v[16] = o[0]; v[17] = o[1]; v[18] = o[2]; v[19] = o[3];
-                    dequant_word_natural(c1.y, s2b, o); v[20] = o[0]; v[21] = o[1]; v[22] = o[2]; v[23] = o[3];
-                    dequant_word_natural(c1.z, s2b, o); v[24] = o[0]; v[25] = o[1]; v[26] = o[2]; v[27] = o[3];
-                    dequant_word_natural(c1.w, s2b, o); v[28] = o[0]; v[29] = o[1]; v[30] = o[2]; v[31] = o[3];
+                const uint32_t words[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+                uint32_t v[8][4];
+#pragma unroll
+                for (int w = 0; w < 8; ++w) {
+                    if constexpr (Cfg::kPermX) dequant_word_interleaved(words[w], w < 4 ? s2a : s2b, v[w]);
+                    else dequant_word_natural(words[w], w < 4 ? s2a : s2b, v[w]);
                 }
                 mbar_wait(&a_empty[as], ((j / AS) & 1) ^ 1);
                 tc_fence_after();
-                tmem_st_32x32b_x32(tmem_base + lane_base + Cfg::kA0 + as * 32, v);
+                const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) tmem_st_32x32b_x4(acol + 4 * w, v[w][0], v[w][1], v[w][2], v[w][3]);
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -432,7 +458,7 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
                      kTcWStageK / kGroup, kTcBM, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
     TcArgs a;
-    a.n = n; a.K = K; a.N = N; a.y = y;
+    a.n = n; a.K = K; a.N = N; a.y = y; a.xptr = x;
     a.split = plan.split;
     a.kt = static_cast<int>((K + kTcWStageK - 1) / kTcWStageK);
     a.part = nullptr; a.cnt = nullptr;

@@ -57,4 +57,23 @@ __device__ __forceinline__ void dequant_word_natural(uint32_t v, __half2 s2, uin
     }
 }
 
+// Tensor-core unpack without byte permutes: W for the 8 codes of one word,
+// bit-exact, as 4 half2 in the interleaved order (W0,W4) (W1,W5) (W2,W6)
+// (W3,W7) -- the TMEM A columns then hold k in the order 0,4,1,5,2,6,3,7 of
+// every 8, and the B operand (x) is written with the same permutation.
+// Cost: 1 SHF + 4 LOP3 (ALU) + 4 HFMA2 + 4 HMUL2.
+__device__ __forceinline__ void dequant_word_interleaved(uint32_t v, __half2 s2, uint32_t (&out)[4]) {
+    __half2 c[4];
+    unpack_centered_interleaved(v, c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = h2_as_u32(__hmul2(c[i], s2));
+}
+
+// x permutation matching dequant_word_interleaved: 8 fp16 (k0..k7 as 4 half2
+// words w0=(k0,k1) w1=(k2,k3) w2=(k4,k5) w3=(k6,k7)) -> (k0,k4)(k1,k5)(k2,k6)(k3,k7).
+__device__ __forceinline__ uint4 permute_x8(uint4 v) {
+    return make_uint4(prmt(v.x, v.z, 0x5410u), prmt(v.x, v.z, 0x7632u),
+                      prmt(v.y, v.w, 0x5410u), prmt(v.y, v.w, 0x7632u));
+}
+
 }  // namespace rq4
