@@ -10,8 +10,11 @@
 // features), MMA N = BN tokens, K = 16 per instruction.
 //   warp 0   W producer : TMA of packed codes (128 rows x 128 B, SW128) and
 //                         scales (128 rows x 16 B) per 256-k stage
-//   warp 2   x producer : TMA of x (BN rows x 64 k, SW128) per 64-k sub-block;
+//   warp 3   x producer : TMA of x (BN rows x 64 k, SW128) per 64-k sub-block;
 //                         out-of-range tokens / k are zero-filled by TMA
+//                         (warp 3 also allocates/frees TMEM)
+//   warp 2   x permuter : BN <= 64 only -- reorders k inside every 16-B chunk
+//                         to match the PRMT-free interleaved dequant
 //   warps 4-11 transform: warp (q, h), thread m = 32q + lane owns weight row m
 //                         (= TMEM lane m) and dequantises the 64-k sub-blocks of
 //                         parity h: reads its row's codes from SMEM, bit-exact
@@ -70,7 +73,7 @@ struct TcCfg {
     static constexpr uint32_t kOffScales = kOffCodes + kWStages * kCodesStageBytes;
     static constexpr uint32_t kOffX = kOffScales + kWStages * kScalesStageBytes;
     static constexpr uint32_t kOffBar = kOffX + kXStages * kXStageBytes;
-    static constexpr uint32_t kNumBars = 2 * kWStages + 2 * kAStages + 2 * kXStages + 1;
+    static constexpr uint32_t kNumBars = 2 * kWStages + 2 * kAStages + 3 * kXStages + 1;
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
     static_assert(128u * BN * 4u <= kOffBar, "cluster reduction buffer must fit in the rings");
 };
@@ -95,7 +98,8 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     uint64_t* a_empty = a_full + AS;
     uint64_t* x_full = a_empty + AS;
     uint64_t* x_empty = x_full + XS;
-    uint64_t* acc_full = x_empty + XS;
+    uint64_t* x_perm = x_empty + XS;
+    uint64_t* acc_full = x_perm + XS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
     uint32_t* flag_slot = tmem_slot + 1;
 
@@ -114,7 +118,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     if (threadIdx.x == 0) {
         for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 8); }
         for (int i = 0; i < AS; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
-        for (int i = 0; i < XS; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+        for (int i = 0; i < XS; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); mbar_init(&x_perm[i], 1); }
         mbar_init(acc_full, 1);
         fence_mbar_init();
     }
@@ -148,33 +152,9 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                             kb * (kTcWStageK / kGroup), static_cast<int32_t>(m0), pol);
             }
         }
-    } else if (warp == 2) {
-        // ---------------- x producer: the only input that depends on the previous kernel
-        if constexpr (Cfg::kPermX) {
-            pdl_wait();
-            for (int j = 0; j < nsub; ++j) {
-                const int slot = j % XS;
-                const uint32_t ph = (j / XS) & 1;
-                mbar_wait(&x_empty[slot], ph ^ 1);
-                const int64_t kbase = static_cast<int64_t>(ks0 * kSubPerStage + j) * kTcXStageK;
-                uint8_t* xt = x_sm + slot * Cfg::kXStageBytes;
-#pragma unroll
-                for (int it = 0; it < (BN * 8) / 32; ++it) {
-                    const int idx = it * 32 + lane;
-                    const int r = idx >> 3;           // token row in the tile
-                    const int c = idx & 7;            // 16-B chunk (8 k) in the 64-k row
-                    const int64_t tok = n0 + r;
-                    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-                    if (tok < a.n)
-                        v = *reinterpret_cast<const uint4*>(a.xptr + tok * a.K + kbase + c * 8);
-                    *reinterpret_cast<uint4*>(xt + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)) =
-                        permute_x8(v);
-                }
-                fence_proxy_async_smem();             // generic-proxy writes -> UMMA (async proxy)
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&x_full[slot]);
-            }
-        } else if (elect_one()) {
+    } else if (warp == 3) {
+        // ---------------- x producer (TMA): the only input that depends on the previous kernel
+        if (elect_one()) {
             pdl_wait();
             const uint64_t pol = policy_evict_last();
             for (int j = 0; j < nsub; ++j) {
@@ -187,6 +167,26 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                             static_cast<int32_t>(n0), pol);
             }
         }
+    } else if (warp == 2) {
+        // ---------------- x permuter (BN <= 64): reorder the 8 k of every 16-B
+        // chunk in place to (0,4,1,5,2,6,3,7) so B matches the A columns of
+        // dequant_word_interleaved.  The 128B swizzle moves whole 16-B chunks,
+        // so the in-chunk permutation is layout-independent.
+        if constexpr (Cfg::kPermX) {
+            for (int j = 0; j < nsub; ++j) {
+                const int slot = j % XS;
+                mbar_wait(&x_full[slot], (j / XS) & 1);
+                uint4* xt = reinterpret_cast<uint4*>(x_sm + slot * Cfg::kXStageBytes);
+#pragma unroll
+                for (int it = 0; it < (BN * 8) / 32; ++it) {
+                    uint4* p = xt + it * 32 + lane;
+                    *p = permute_x8(*p);
+                }
+                fence_proxy_async_smem();             // generic-proxy writes -> UMMA (async proxy)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&x_perm[slot]);
+            }
+        }
     } else if (warp == 1) {
         // ---------------- MMA issuer
         if (elect_one()) {
@@ -195,7 +195,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                 const int as = j % AS;
                 const int xs = j % XS;
                 mbar_wait(&a_full[as], (j / AS) & 1);
-                mbar_wait(&x_full[xs], (j / XS) & 1);
+                mbar_wait(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], (j / XS) & 1);
                 tc_fence_after();
                 const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * Cfg::kXStageBytes));
 #pragma unroll
