@@ -347,7 +347,9 @@ static GsConfig gs_config(int64_t K, int64_t N) {
     int ns = static_cast<int>(gs_ring_budget() / stage);
     c.NS = ns < 2 ? 2 : ns > 8 ? 8 : ns;
     c.threads = (c.WK * c.H + 1) * 32;
-    c.grid = static_cast<int>(N < kNumSMs ? N : kNumSMs);
+    int mult = 1;
+    if (const char* e = std::getenv("RELAX_Q4_GS_GRID_MULT")) { const int v = std::atoi(e); if (v >= 1 && v <= 4) mult = v; }
+    c.grid = static_cast<int>(N < kNumSMs * mult ? N : kNumSMs * mult);
     c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
     c.smem = 128 + static_cast<size_t>(c.NS) * stage + 1024 +
              static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
