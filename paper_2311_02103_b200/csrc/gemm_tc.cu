@@ -140,9 +140,9 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         // ---------------- W producer (weights never depend on the previous kernel)
         if (elect_one()) {
             const uint64_t pol = policy_evict_first();
-            for (int i = 0; i < nst; ++i) {
-                const int slot = i % kWStages;
-                const uint32_t ph = (i / kWStages) & 1;
+            int slot = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < nst; ++i, slot = (slot + 1 == kWStages) ? 0 : slot + 1, ph ^= (slot == 0)) {
                 mbar_wait(&w_empty[slot], ph ^ 1);
                 mbar_arrive_expect_tx(&w_full[slot], kCodesStageBytes + kScalesStageBytes);
                 const int kb = ks0 + i;
@@ -157,9 +157,9 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (elect_one()) {
             pdl_wait();
             const uint64_t pol = policy_evict_last();
-            for (int j = 0; j < nsub; ++j) {
-                const int slot = j % XS;
-                const uint32_t ph = (j / XS) & 1;
+            int slot = 0;
+            uint32_t ph = 0;
+            for (int j = 0; j < nsub; ++j, slot = (slot + 1 == XS) ? 0 : slot + 1, ph ^= (slot == 0)) {
                 mbar_wait(&x_empty[slot], ph ^ 1);
                 mbar_arrive_expect_tx(&x_full[slot], Cfg::kXStageBytes);
                 const int32_t k = (ks0 * kSubPerStage + j) * kTcXStageK;
@@ -173,9 +173,10 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         // dequant_word_interleaved.  The 128B swizzle moves whole 16-B chunks,
         // so the in-chunk permutation is layout-independent.
         if constexpr (Cfg::kPermX) {
-            for (int j = 0; j < nsub; ++j) {
-                const int slot = j % XS;
-                mbar_wait(&x_full[slot], (j / XS) & 1);
+            int slot = 0;
+            uint32_t ph = 0;
+            for (int j = 0; j < nsub; ++j, slot = (slot + 1 == XS) ? 0 : slot + 1, ph ^= (slot == 0)) {
+                mbar_wait(&x_full[slot], ph);
                 uint4* xt = reinterpret_cast<uint4*>(x_sm + slot * Cfg::kXStageBytes);
 #pragma unroll
                 for (int it = 0; it < (BN * 8) / 32; ++it) {
@@ -191,11 +192,12 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         // ---------------- MMA issuer
         if (elect_one()) {
             constexpr uint32_t idesc = idesc_f16_f32(kTcBM, BN);
-            for (int j = 0; j < nsub; ++j) {
-                const int as = j % AS;
-                const int xs = j % XS;
-                mbar_wait(&a_full[as], (j / AS) & 1);
-                mbar_wait(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], (j / XS) & 1);
+            int as = 0, xs = 0;
+            uint32_t aph = 0, xph = 0;
+            for (int j = 0; j < nsub; ++j, as = (as + 1 == AS) ? 0 : as + 1, aph ^= (as == 0),
+                                           xs = (xs + 1 == XS) ? 0 : xs + 1, xph ^= (xs == 0)) {
+                mbar_wait(&a_full[as], aph);
+                mbar_wait(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], xph);
                 tc_fence_after();
                 const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * Cfg::kXStageBytes));
 #pragma unroll
@@ -218,20 +220,19 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         const int h = tw >> 2;
         const int m = q * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        int ws = 0, as = h;                 // this warp's sub-blocks: j = h, h+2, h+4, ...
+        uint32_t wph = 0, aph = 0;
         for (int i = 0; i < nst; ++i) {
-            const int ws = i % kWStages;
-            mbar_wait(&w_full[ws], (i / kWStages) & 1);
+            mbar_wait(&w_full[ws], wph);
             const uint8_t* crow = codes_sm + ws * kCodesStageBytes + m * 128;
             const uint4 sv = *reinterpret_cast<const uint4*>(scales_sm + ws * kScalesStageBytes + m * 16);
             const uint32_t sw[4] = {sv.x, sv.y, sv.z, sv.w};     // 8 scales, 2 per word
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int sub = h + 2 * u;
-                const int j = i * kSubPerStage + sub;
-                const int as = j % AS;
                 const uint4 c0 = *reinterpret_cast<const uint4*>(crow + (((2 * sub) ^ (m & 7)) << 4));
                 const uint4 c1 = *reinterpret_cast<const uint4*>(crow + (((2 * sub + 1) ^ (m & 7)) << 4));
-                const uint32_t swu = sub == 0 ? sw[0] : sub == 1 ? sw[1] : sub == 2 ? sw[2] : sw[3];
+                const uint32_t swu = h == 0 ? (u == 0 ? sw[0] : sw[2]) : (u == 0 ? sw[1] : sw[3]);
                 const __half s_lo = __ushort_as_half(lo16(swu));   // group 2*sub
                 const __half s_hi = __ushort_as_half(hi16(swu));   // group 2*sub+1
                 const __half2 s2a = __halves2half2(s_lo, s_lo);
@@ -243,7 +244,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                     if constexpr (Cfg::kPermX) dequant_word_interleaved(words[w], w < 4 ? s2a : s2b, v[w]);
                     else dequant_word_natural(words[w], w < 4 ? s2a : s2b, v[w]);
                 }
-                mbar_wait(&a_empty[as], ((j / AS) & 1) ^ 1);
+                mbar_wait(&a_empty[as], aph ^ 1);
                 tc_fence_after();
                 const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32;
 #pragma unroll
@@ -252,9 +253,12 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[as]);
+                as += 2;
+                if (as >= AS) { as -= AS; aph ^= 1; }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&w_empty[ws]);
+            if (++ws == kWStages) { ws = 0; wph ^= 1; }
         }
     }
 
