@@ -38,7 +38,8 @@
 
 namespace rq4 {
 
-constexpr int kTcThreads = 384;        // 12 warps, see the role map above
+constexpr int kTcTransformWarps = 16;  // 4 TMEM lane quarters x 2 sub-block parities x 2 k-halves
+constexpr int kTcThreads = (4 + kTcTransformWarps) * 32;   // 20 warps, see the role map above
 constexpr int kWStages = 4;            // 256-k codes+scales stages in flight
 constexpr uint32_t kCodesStageBytes = kTcBM * (kTcWStageK / 2);     // 16 KB
 constexpr uint32_t kScalesStageBytes = kTcBM * (kTcWStageK / kGroup) * 2;  // 2 KB
@@ -116,8 +117,8 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     pdl_launch_dependents();
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 8); }
-        for (int i = 0; i < AS; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
+        for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], kTcTransformWarps); }
+        for (int i = 0; i < AS; ++i) { mbar_init(&a_full[i], kTcTransformWarps / 2); mbar_init(&a_empty[i], 1); }
         for (int i = 0; i < XS; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); mbar_init(&x_perm[i], 1); }
         mbar_init(acc_full, 1);
         fence_mbar_init();
@@ -216,8 +217,9 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         // of the sub-blocks with parity h into the TMEM A ring.  Slots are free
         // up front, so the first AS sub-blocks are dequantised before x arrives.
         const int tw = warp - 4;
-        const int q = tw & 3;
-        const int h = tw >> 2;
+        const int q = tw & 3;                 // TMEM lanes 32q..32q+31 = rows
+        const int h = (tw >> 2) & 1;          // sub-block parity
+        const int kh = tw >> 3;               // k-half (32 k = 4 words) of the sub-block
         const int m = q * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int ws = 0, as = h;                 // this warp's sub-blocks: j = h, h+2, h+4, ...
@@ -225,30 +227,27 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         for (int i = 0; i < nst; ++i) {
             mbar_wait(&w_full[ws], wph);
             const uint8_t* crow = codes_sm + ws * kCodesStageBytes + m * 128;
-            const uint4 sv = *reinterpret_cast<const uint4*>(scales_sm + ws * kScalesStageBytes + m * 16);
-            const uint32_t sw[4] = {sv.x, sv.y, sv.z, sv.w};     // 8 scales, 2 per word
+            const uint32_t* srow = reinterpret_cast<const uint32_t*>(scales_sm + ws * kScalesStageBytes + m * 16);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int sub = h + 2 * u;
-                const uint4 c0 = *reinterpret_cast<const uint4*>(crow + (((2 * sub) ^ (m & 7)) << 4));
-                const uint4 c1 = *reinterpret_cast<const uint4*>(crow + (((2 * sub + 1) ^ (m & 7)) << 4));
-                const uint32_t swu = h == 0 ? (u == 0 ? sw[0] : sw[2]) : (u == 0 ? sw[1] : sw[3]);
-                const __half s_lo = __ushort_as_half(lo16(swu));   // group 2*sub
-                const __half s_hi = __ushort_as_half(hi16(swu));   // group 2*sub+1
-                const __half2 s2a = __halves2half2(s_lo, s_lo);
-                const __half2 s2b = __halves2half2(s_hi, s_hi);
-                const uint32_t words[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-                uint32_t v[8][4];
+                const int chunk = 2 * sub + kh;     // 16-B chunk = 32 codes = one group
+                const uint4 c = *reinterpret_cast<const uint4*>(crow + ((chunk ^ (m & 7)) << 4));
+                const uint32_t sp = srow[sub];      // scales of groups 2*sub, 2*sub+1
+                const __half sh = __ushort_as_half(kh ? hi16(sp) : lo16(sp));
+                const __half2 s2 = __halves2half2(sh, sh);
+                const uint32_t words[4] = {c.x, c.y, c.z, c.w};
+                uint32_t v[4][4];
 #pragma unroll
-                for (int w = 0; w < 8; ++w) {
-                    if constexpr (Cfg::kPermX) dequant_word_interleaved(words[w], w < 4 ? s2a : s2b, v[w]);
-                    else dequant_word_natural(words[w], w < 4 ? s2a : s2b, v[w]);
+                for (int w = 0; w < 4; ++w) {
+                    if constexpr (Cfg::kPermX) dequant_word_interleaved(words[w], s2, v[w]);
+                    else dequant_word_natural(words[w], s2, v[w]);
                 }
                 mbar_wait(&a_empty[as], aph ^ 1);
                 tc_fence_after();
-                const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32;
+                const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32 + kh * 16;
 #pragma unroll
-                for (int w = 0; w < 8; ++w) tmem_st_32x32b_x4(acol + 4 * w, v[w][0], v[w][1], v[w][2], v[w][3]);
+                for (int w = 0; w < 4; ++w) tmem_st_32x32b_x4(acol + 4 * w, v[w][0], v[w][1], v[w][2], v[w][3]);
                 tc_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -263,7 +262,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     }
 
     // ------------------------------------------------------------ epilogue
-    const bool epi = warp >= 4 && warp < 8;          // TMEM lanes 32q..32q+31
+    const bool epi = warp >= 4 && warp < 8;          // TMEM lanes 32q..32q+31 (transform warps 0-3)
     const int q = warp & 3;
     const int m = q * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
