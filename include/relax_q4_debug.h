@@ -13,6 +13,10 @@
 extern "C" {
 #endif
 RELAX_API int relax_debug_trace_read(void* host, size_t max_records, size_t* n_records, int reset);
+/* Tensor-core kernel: per-CTA {cta, smid, nsub, pad, t0, t_end (ns), wait
+ * cycles of: W producer, x producer, x permuter, transform (W data), transform
+ * (A slot), MMA (A ready), MMA (x ready), epilogue} -- 96-byte records. */
+RELAX_API int relax_debug_tctrace_read(void* host, size_t max_records, size_t* n_records, int reset);
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,9 @@
 //                         Both deterministic.
 #include <cuda.h>
 #include <cstdio>
+#include <cstdlib>
 #include "internal.h"
+#include "relax_q4.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
 
@@ -45,6 +47,24 @@ constexpr uint32_t kCodesStageBytes = kTcBM * (kTcWStageK / 2);     // 16 KB
 constexpr uint32_t kScalesStageBytes = kTcBM * (kTcWStageK / kGroup) * 2;  // 2 KB
 constexpr int kSubPerStage = kTcWStageK / kTcXStageK;                // 4
 
+// ---- optional per-CTA role timing (RELAX_Q4_TRACE=1): wait cycles per role
+struct TcTrace { uint32_t cta, smid, nsub, pad; uint64_t t0, t_end;
+                 uint64_t w_prod, x_prod, perm, tr_w, tr_a, mma_a, mma_x, epi; };
+constexpr int kTcTraceMax = 1 << 14;
+__device__ TcTrace g_tctrace[kTcTraceMax];
+__device__ uint32_t g_tctrace_n;
+
+template <bool T>
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, uint64_t& acc) {
+    if (T) {
+        const uint64_t c0 = clock64();
+        mbar_wait(bar, parity);
+        acc += clock64() - c0;
+    } else {
+        mbar_wait(bar, parity);
+    }
+}
+
 struct TcArgs {
     int64_t n, K, N;
     const uint16_t* xptr;  // x fp16 [n][K] (the permuted-x producer reads it directly)
@@ -54,6 +74,7 @@ struct TcArgs {
     int split;
     int kt;               // number of 256-k W stages covering K
     int cluster;          // 1: split-K partials reduced through DSMEM of the cluster
+    int trace;            // record role wait cycles (debug)
 };
 
 template <int BN>
@@ -113,6 +134,10 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const int ks1 = static_cast<int>(static_cast<int64_t>(z + 1) * a.kt / a.split);
     const int nst = ks1 - ks0;              // >= 1 (split <= kt)
     const int nsub = nst * kSubPerStage;
+    __shared__ uint64_t tr_slots[8];
+    if (threadIdx.x < 8) tr_slots[threadIdx.x] = 0;
+    const uint64_t t_start = a.trace ? globaltimer() : 0;
+    uint64_t wacc = 0, wacc2 = 0;
 
     pdl_launch_dependents();
 
@@ -144,7 +169,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             int slot = 0;
             uint32_t ph = 0;
             for (int i = 0; i < nst; ++i, slot = (slot + 1 == kWStages) ? 0 : slot + 1, ph ^= (slot == 0)) {
-                mbar_wait(&w_empty[slot], ph ^ 1);
+                if (a.trace) mbar_wait_t<true>(&w_empty[slot], ph ^ 1, wacc); else mbar_wait(&w_empty[slot], ph ^ 1);
                 mbar_arrive_expect_tx(&w_full[slot], kCodesStageBytes + kScalesStageBytes);
                 const int kb = ks0 + i;
                 tma_load_2d(codes_sm + slot * kCodesStageBytes, &tm_w, &w_full[slot],
@@ -161,7 +186,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             int slot = 0;
             uint32_t ph = 0;
             for (int j = 0; j < nsub; ++j, slot = (slot + 1 == XS) ? 0 : slot + 1, ph ^= (slot == 0)) {
-                mbar_wait(&x_empty[slot], ph ^ 1);
+                if (a.trace) mbar_wait_t<true>(&x_empty[slot], ph ^ 1, wacc); else mbar_wait(&x_empty[slot], ph ^ 1);
                 mbar_arrive_expect_tx(&x_full[slot], Cfg::kXStageBytes);
                 const int32_t k = (ks0 * kSubPerStage + j) * kTcXStageK;
                 tma_load_2d(x_sm + slot * Cfg::kXStageBytes, &tm_x, &x_full[slot], k,
@@ -177,7 +202,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             int slot = 0;
             uint32_t ph = 0;
             for (int j = 0; j < nsub; ++j, slot = (slot + 1 == XS) ? 0 : slot + 1, ph ^= (slot == 0)) {
-                mbar_wait(&x_full[slot], ph);
+                if (a.trace) mbar_wait_t<true>(&x_full[slot], ph, wacc); else mbar_wait(&x_full[slot], ph);
                 uint4* xt = reinterpret_cast<uint4*>(x_sm + slot * Cfg::kXStageBytes);
 #pragma unroll
                 for (int it = 0; it < (BN * 8) / 32; ++it) {
@@ -197,8 +222,13 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             uint32_t aph = 0, xph = 0;
             for (int j = 0; j < nsub; ++j, as = (as + 1 == AS) ? 0 : as + 1, aph ^= (as == 0),
                                            xs = (xs + 1 == XS) ? 0 : xs + 1, xph ^= (xs == 0)) {
-                mbar_wait(&a_full[as], aph);
-                mbar_wait(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], xph);
+                if (a.trace) {
+                    mbar_wait_t<true>(&a_full[as], aph, wacc);
+                    mbar_wait_t<true>(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], xph, wacc2);
+                } else {
+                    mbar_wait(&a_full[as], aph);
+                    mbar_wait(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], xph);
+                }
                 tc_fence_after();
                 const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * Cfg::kXStageBytes));
 #pragma unroll
@@ -225,7 +255,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         int ws = 0, as = h;                 // this warp's sub-blocks: j = h, h+2, h+4, ...
         uint32_t wph = 0, aph = 0;
         for (int i = 0; i < nst; ++i) {
-            mbar_wait(&w_full[ws], wph);
+            if (a.trace) mbar_wait_t<true>(&w_full[ws], wph, wacc); else mbar_wait(&w_full[ws], wph);
             const uint8_t* crow = codes_sm + ws * kCodesStageBytes + m * 128;
             const uint32_t* srow = reinterpret_cast<const uint32_t*>(scales_sm + ws * kScalesStageBytes + m * 16);
 #pragma unroll
@@ -243,7 +273,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                     if constexpr (Cfg::kPermX) dequant_word_interleaved(words[w], s2, v[w]);
                     else dequant_word_natural(words[w], s2, v[w]);
                 }
-                mbar_wait(&a_empty[as], aph ^ 1);
+                if (a.trace) mbar_wait_t<true>(&a_empty[as], aph ^ 1, wacc2); else mbar_wait(&a_empty[as], aph ^ 1);
                 tc_fence_after();
                 const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32 + kh * 16;
 #pragma unroll
@@ -261,6 +291,13 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         }
     }
 
+    if (a.trace && lane == 0) {
+        if (warp == 0) tr_slots[0] = wacc;                    // W producer: waits for free W slots
+        if (warp == 3) tr_slots[1] = wacc;                    // x producer: waits for free x slots
+        if (warp == 2) tr_slots[2] = wacc;                    // permuter: waits for x data
+        if (warp == 4) { tr_slots[3] = wacc; tr_slots[4] = wacc2; }   // transform: W data / A slot
+        if (warp == 1) { tr_slots[5] = wacc; tr_slots[6] = wacc2; }   // MMA: A ready / x ready
+    }
     // ------------------------------------------------------------ epilogue
     const bool epi = warp >= 4 && warp < 8;          // TMEM lanes 32q..32q+31 (transform warps 0-3)
     const int q = warp & 3;
@@ -366,6 +403,18 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     __syncthreads();
     tc_fence_after();
     if (warp == 3) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    if (a.trace && threadIdx.x == 0) {
+        const uint32_t i = atomicAdd(&g_tctrace_n, 1u);
+        if (i < kTcTraceMax) {
+            TcTrace r;
+            r.cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+            uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); r.smid = sm;
+            r.nsub = nsub; r.pad = 0; r.t0 = t_start; r.t_end = globaltimer();
+            r.w_prod = tr_slots[0]; r.x_prod = tr_slots[1]; r.perm = tr_slots[2];
+            r.tr_w = tr_slots[3]; r.tr_a = tr_slots[4]; r.mma_a = tr_slots[5]; r.mma_x = tr_slots[6]; r.epi = 0;
+            g_tctrace[i] = r;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -466,6 +515,8 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.kt = static_cast<int>((K + kTcWStageK - 1) / kTcWStageK);
     a.part = nullptr; a.cnt = nullptr;
     a.cluster = plan.cluster;
+    static int tr = [] { const char* e = std::getenv("RELAX_Q4_TRACE"); return (e && *e == '1') ? 1 : 0; }();
+    a.trace = tr;
     if (plan.split > 1 && !plan.cluster) {
         a.cnt = static_cast<uint32_t*>(ws);
         a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes);
@@ -481,3 +532,17 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
 }
 
 }  // namespace rq4
+
+extern "C" RELAX_API int relax_debug_tctrace_read(void* host, size_t max_records, size_t* n_records, int reset) {
+    uint32_t n = 0;
+    if (cudaMemcpyFromSymbol(&n, rq4::g_tctrace_n, sizeof n) != cudaSuccess) return RELAX_ERR_CUDA;
+    if (n > static_cast<uint32_t>(rq4::kTcTraceMax)) n = rq4::kTcTraceMax;
+    const size_t m = n < max_records ? n : max_records;
+    if (m && cudaMemcpyFromSymbol(host, rq4::g_tctrace, m * sizeof(rq4::TcTrace)) != cudaSuccess) return RELAX_ERR_CUDA;
+    if (n_records) *n_records = m;
+    if (reset) {
+        const uint32_t z = 0;
+        if (cudaMemcpyToSymbol(rq4::g_tctrace_n, &z, sizeof z) != cudaSuccess) return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
