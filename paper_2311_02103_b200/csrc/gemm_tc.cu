@@ -40,7 +40,8 @@
 
 namespace rq4 {
 
-constexpr int kTcTransformWarps = 16;  // 4 TMEM lane quarters x 2 sub-block parities x 2 k-halves
+constexpr int kTcTransformWarps = 8;   // 4 TMEM lane quarters x 2 sub-block parities (x 2 k-halves if 16)
+constexpr int kTcKHPerWarp = 16 / kTcTransformWarps;   // 32-k halves of a sub-block per warp
 constexpr int kTcThreads = (4 + kTcTransformWarps) * 32;   // 20 warps, see the role map above
 constexpr int kWStages = 4;            // 256-k codes+scales stages in flight
 constexpr uint32_t kCodesStageBytes = kTcBM * (kTcWStageK / 2);     // 16 KB
@@ -137,7 +138,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     __shared__ uint64_t tr_slots[8];
     if (threadIdx.x < 8) tr_slots[threadIdx.x] = 0;
     const uint64_t t_start = a.trace ? globaltimer() : 0;
-    uint64_t wacc = 0, wacc2 = 0;
+    uint64_t wacc = 0, wacc2 = 0, wacc3 = 0, wacc4 = 0;
 
     pdl_launch_dependents();
 
@@ -249,7 +250,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         const int tw = warp - 4;
         const int q = tw & 3;                 // TMEM lanes 32q..32q+31 = rows
         const int h = (tw >> 2) & 1;          // sub-block parity
-        const int kh = tw >> 3;               // k-half (32 k = 4 words) of the sub-block
+        const int kh0 = (tw >> 3) * kTcKHPerWarp;   // first k-half (32 k = 4 words) of the sub-block
         const int m = q * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int ws = 0, as = h;                 // this warp's sub-blocks: j = h, h+2, h+4, ...
@@ -261,24 +262,38 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int sub = h + 2 * u;
-                const int chunk = 2 * sub + kh;     // 16-B chunk = 32 codes = one group
-                const uint4 c = *reinterpret_cast<const uint4*>(crow + ((chunk ^ (m & 7)) << 4));
-                const uint32_t sp = srow[sub];      // scales of groups 2*sub, 2*sub+1
-                const __half sh = __ushort_as_half(kh ? hi16(sp) : lo16(sp));
-                const __half2 s2 = __halves2half2(sh, sh);
-                const uint32_t words[4] = {c.x, c.y, c.z, c.w};
-                uint32_t v[4][4];
+                uint32_t v[kTcKHPerWarp][4][4];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    if constexpr (Cfg::kPermX) dequant_word_interleaved(words[w], s2, v[w]);
-                    else dequant_word_natural(words[w], s2, v[w]);
+                for (int e = 0; e < kTcKHPerWarp; ++e) {
+                    const int kh = kh0 + e;
+                    const int chunk = 2 * sub + kh;     // 16-B chunk = 32 codes = one group
+                    const uint4 c = *reinterpret_cast<const uint4*>(crow + ((chunk ^ (m & 7)) << 4));
+                    const uint32_t sp = srow[sub];      // scales of groups 2*sub, 2*sub+1
+                    const __half sh = __ushort_as_half(kh ? hi16(sp) : lo16(sp));
+                    const __half2 s2 = __halves2half2(sh, sh);
+                    const uint32_t words[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        if constexpr (Cfg::kPermX) dequant_word_interleaved(words[w], s2, v[e][w]);
+                        else dequant_word_natural(words[w], s2, v[e][w]);
+                    }
                 }
                 if (a.trace) mbar_wait_t<true>(&a_empty[as], aph ^ 1, wacc2); else mbar_wait(&a_empty[as], aph ^ 1);
                 tc_fence_after();
-                const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32 + kh * 16;
 #pragma unroll
-                for (int w = 0; w < 4; ++w) tmem_st_32x32b_x4(acol + 4 * w, v[w][0], v[w][1], v[w][2], v[w][3]);
-                tc_wait_st();
+                for (int e = 0; e < kTcKHPerWarp; ++e) {
+                    const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32 + (kh0 + e) * 16;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        tmem_st_32x32b_x4(acol + 4 * w, v[e][w][0], v[e][w][1], v[e][w][2], v[e][w][3]);
+                }
+                if (a.trace) {
+                    const uint64_t c0 = clock64();
+                    tc_wait_st();
+                    wacc3 += clock64() - c0;
+                } else {
+                    tc_wait_st();
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[as]);
@@ -295,7 +310,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (warp == 0) tr_slots[0] = wacc;                    // W producer: waits for free W slots
         if (warp == 3) tr_slots[1] = wacc;                    // x producer: waits for free x slots
         if (warp == 2) tr_slots[2] = wacc;                    // permuter: waits for x data
-        if (warp == 4) { tr_slots[3] = wacc; tr_slots[4] = wacc2; }   // transform: W data / A slot
+        if (warp == 4) { tr_slots[3] = wacc; tr_slots[4] = wacc2; tr_slots[7] = wacc3; }   // transform: W data / A slot / wait::st
         if (warp == 1) { tr_slots[5] = wacc; tr_slots[6] = wacc2; }   // MMA: A ready / x ready
     }
     // ------------------------------------------------------------ epilogue
@@ -411,7 +426,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             uint32_t sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); r.smid = sm;
             r.nsub = nsub; r.pad = 0; r.t0 = t_start; r.t_end = globaltimer();
             r.w_prod = tr_slots[0]; r.x_prod = tr_slots[1]; r.perm = tr_slots[2];
-            r.tr_w = tr_slots[3]; r.tr_a = tr_slots[4]; r.mma_a = tr_slots[5]; r.mma_x = tr_slots[6]; r.epi = 0;
+            r.tr_w = tr_slots[3]; r.tr_a = tr_slots[4]; r.mma_a = tr_slots[5]; r.mma_x = tr_slots[6]; r.epi = tr_slots[7];
             g_tctrace[i] = r;
         }
     }
