@@ -267,7 +267,7 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / peaks["hbm_gbs"], 4), "peak_src": f"{peaks['src']} hbm copy"}
     roof["traffic"] = traffic_per_launch(args.workload, n)
-    roof["kernel"] = "gemv_q4_kernel<1>" if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" \
+    roof["kernel"] = "gemv_stream_kernel (streamed GEMV)" if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" \
         else "tc_q4_kernel"
     roof["per"] = "average over all launches of the step (every launch is this kernel family)"
     launches = sum(1 if sched[f"{K}x{N}"]["variant"] == "tc" else -(-n // 8) for _, K, N in mats)

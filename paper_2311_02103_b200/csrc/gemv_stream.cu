@@ -181,10 +181,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nwc = a.WK * a.H;                        // consumer warps
-    // [barriers: 2*NS x 8 B, padded to 128][ring: NS stages + 1 KB pad][partials]
+    // [barriers: 2*NS x 8 B, padded to 256][ring: NS stages + 1 KB pad][partials]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + a.NS;
-    uint8_t* ring = smem + 128;
+    uint8_t* ring = smem + 256;
     float* part = reinterpret_cast<float*>(ring + static_cast<size_t>(a.NS) * a.stage_bytes + 1024);
 
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * a.N / gridDim.x;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
     const uint64_t t_start = a.trace_seq ? gtime() : 0;
     __shared__ uint64_t tr_wait, tr_first;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < a.NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], nwc); }
+        for (int i = 0; i < a.NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], a.WK); }
         fence_mbar_init();
     }
     __syncthreads();
@@ -254,43 +254,39 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         }
         const int rsel = reduce_row_of_lane<RPW>(lane);
         const bool writer = (lane & (32 / RPW - 1)) == 0;
-        // this warp's rows inside a stage: [h*RPW, h*RPW + RPW)
-        const uint32_t coff = static_cast<uint32_t>(h * RPW) * cb_row + static_cast<uint32_t>(g) * 16u;
-        const uint32_t soff = codes_stage + static_cast<uint32_t>(h * RPW) * sb_row + static_cast<uint32_t>(g) * 2u;
-        int slot = 0;
+        // Stages (RPW rows each) go round-robin to the H row groups: warp (h, kw)
+        // consumes stages h, h+H, ... and each stage is released by its WK
+        // warps alone, so the producer refills slots at a fine grain.
+        const uint32_t coff = static_cast<uint32_t>(g) * 16u;
+        const uint32_t soff = codes_stage + static_cast<uint32_t>(g) * 2u;
+        int slot = h;                                    // requires H <= NS
         uint32_t phase = 0;
-        for (int r_base = 0; r_base < rows; r_base += a.RS) {
+        for (int st = h; st < nst; st += a.H) {
+            const int r_base = st * a.RS;
             const int nr = rows - r_base < a.RS ? rows - r_base : a.RS;
             mbar_wait(&full[slot], phase);
             if (a.trace_seq && r_base == 0 && warp == 0 && lane == 0) tr_first = gtime();
             const uint8_t* stage = ring + static_cast<size_t>(slot) * a.stage_bytes;
             float acc[NT][RPW];
-            if (h * RPW < nr) {                              // warp-uniform
 #pragma unroll
-                for (int i = 0; i < RPW; ++i) {
-                    const uint4 cw = lds128(stage + coff + i * cb_row);
-                    uint16_t sbits = *reinterpret_cast<const uint16_t*>(stage + soff + i * sb_row);
-                    if (!FULLG && !gv) sbits = 0;             // lanes past K: x = 0 and s = 0
-                    float o[NT];
-                    row_dot<NT, ZPF>(cw, sbits, xr, m7x, o);
+            for (int i = 0; i < RPW; ++i) {
+                const uint4 cw = lds128(stage + coff + i * cb_row);
+                uint16_t sbits = *reinterpret_cast<const uint16_t*>(stage + soff + i * sb_row);
+                if (!FULLG && !gv) sbits = 0;                 // lanes past K: x = 0 and s = 0
+                float o[NT];
+                row_dot<NT, ZPF>(cw, sbits, xr, m7x, o);
 #pragma unroll
-                    for (int t = 0; t < NT; ++t) acc[t][i] = o[t];
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < RPW; ++i)
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) acc[t][i] = 0.f;
+                for (int t = 0; t < NT; ++t) acc[t][i] = o[t];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);      // stage bytes fully consumed
-            if (++slot == a.NS) { slot = 0; phase ^= 1; }
+            slot += a.H;
+            if (slot >= a.NS) { slot -= a.NS; phase ^= 1; }
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const float v = reduce_rows<RPW>(acc[t], lane);
-                const int rl = h * RPW + rsel;
-                if (writer && rl < nr)
-                    part[(static_cast<size_t>(r_base + rl) * a.WK + kw) * NT + t] = v;
+                if (writer && rsel < nr)
+                    part[(static_cast<size_t>(r_base + rsel) * a.WK + kw) * NT + t] = v;
             }
         }
     }
@@ -341,17 +337,21 @@ static GsConfig gs_config(int64_t K, int64_t N) {
     c.RPW = 4;
     if (const char* e = std::getenv("RELAX_Q4_GS_H")) { const int v = std::atoi(e); if (v >= 1 && v * c.WK <= 31) c.H = v; }
     if (const char* e = std::getenv("RELAX_Q4_GS_RPW")) { const int v = std::atoi(e); if (v == 1 || v == 2 || v == 4 || v == 8) c.RPW = v; }
-    while (c.RPW > 1 && 2 * static_cast<size_t>(c.H * c.RPW) * row_bytes > gs_ring_budget()) c.RPW /= 2;
-    c.RS = c.H * c.RPW;
+    // at least max(H, 3) stages of RPW rows must fit the ring
+    const int nsmin = c.H < 3 ? 3 : c.H;
+    while (c.RPW > 1 && static_cast<size_t>(nsmin) * c.RPW * row_bytes > gs_ring_budget()) c.RPW /= 2;
+    c.RS = c.RPW;
     const size_t stage = static_cast<size_t>(c.RS) * row_bytes;
     int ns = static_cast<int>(gs_ring_budget() / stage);
-    c.NS = ns < 2 ? 2 : ns > 8 ? 8 : ns;
+    if (ns < nsmin) c.H = ns < 1 ? 1 : ns;          // (only for huge K with RPW = 1)
+    c.NS = ns < 2 ? 2 : ns > 16 ? 16 : ns;
+    if (c.NS < c.H) c.H = c.NS;
     c.threads = (c.WK * c.H + 1) * 32;
     int mult = 1;
     if (const char* e = std::getenv("RELAX_Q4_GS_GRID_MULT")) { const int v = std::atoi(e); if (v >= 1 && v <= 4) mult = v; }
     c.grid = static_cast<int>(N < kNumSMs * mult ? N : kNumSMs * mult);
     c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
-    c.smem = 128 + static_cast<size_t>(c.NS) * stage + 1024 +
+    c.smem = 256 + static_cast<size_t>(c.NS) * stage + 1024 +
              static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
     return c;
 }
