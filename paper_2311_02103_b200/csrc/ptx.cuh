@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
+#include <cstdio>
 
 namespace rq4 {
 
@@ -77,8 +78,23 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
 #ifdef RQ4_DEBUG_HANG
+    // debug builds: short suspend hint and a spin bound, so a protocol bug
+    // traps (a CUDA error naming the kernel) instead of hanging the GPU.
     uint64_t spins = 0;
-#endif
+    while (true) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(addr), "r"(parity), "r"(1000u) : "memory");
+        if (done) break;
+        if (++spins > (1ull << 22)) {
+            printf("rq4 hang: block %d thread %d bar %u parity %u\n", blockIdx.x, threadIdx.x, addr, parity);
+            __trap();
+        }
+    }
+#else
     while (true) {
         uint32_t done;
         asm volatile(
@@ -87,10 +103,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done) : "r"(addr), "r"(parity), "r"(1000000u) : "memory");
         if (done) break;
-#ifdef RQ4_DEBUG_HANG
-        if (++spins > (1ull << 26)) __trap();
-#endif
     }
+#endif
 }
 
 // ----------------------------------------------------------------- TMA
