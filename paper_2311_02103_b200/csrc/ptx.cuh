@@ -101,7 +101,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             "{\n\t.reg .pred p;\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done) : "r"(addr), "r"(parity), "r"(1000000u) : "memory");
+            : "=r"(done) : "r"(addr), "r"(parity), "r"(2000u) : "memory");
         if (done) break;
     }
 #endif
