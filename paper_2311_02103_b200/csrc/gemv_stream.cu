@@ -75,7 +75,7 @@ static size_t gs_ring_budget() {
     static size_t v = [] {
         const char* e = std::getenv("RELAX_Q4_GS_RING_KB");
         const int kb = e ? std::atoi(e) : 0;
-        return static_cast<size_t>(kb >= 16 && kb <= 190 ? kb : 96) * 1024;
+        return static_cast<size_t>(kb >= 72 && kb <= 190 ? kb : 96) * 1024;
     }();
     return v;
 }
@@ -353,6 +353,9 @@ static GsConfig gs_config(int64_t K, int64_t N) {
     c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
     c.smem = 256 + static_cast<size_t>(c.NS) * stage + 1024 +
              static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
+    // At most two GEMV CTAs per SM (the running kernel and the next one under
+    // PDL): a third co-resident kernel was observed to stall the chain.
+    if (c.smem < 80 * 1024) c.smem = 80 * 1024;
     return c;
 }
 
