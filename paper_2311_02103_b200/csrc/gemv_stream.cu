@@ -75,7 +75,7 @@ static size_t gs_ring_budget() {
     static size_t v = [] {
         const char* e = std::getenv("RELAX_Q4_GS_RING_KB");
         const int kb = e ? std::atoi(e) : 0;
-        return static_cast<size_t>(kb >= 72 && kb <= 190 ? kb : 96) * 1024;
+        return static_cast<size_t>(kb >= 72 && kb <= 190 ? kb : 104) * 1024;
     }();
     return v;
 }
