@@ -54,12 +54,31 @@ def load_peaks():
             "src": "fallback"}
 
 
-def layer_set(workload: str, fused: bool = False):
+def tp_shard(name: str, K: int, N: int, p: int):
+    """Rank-local shape of one linear under Megatron tensor parallelism of
+    degree p: q/k/v, gate/up and lm_head split their output
+    features (column split), o and down split their reduction dim (row split,
+    followed by an all_reduce of the partial y)."""
+    if p == 1:
+        return K, N
+    if name in ("o", "down"):
+        assert K % p == 0
+        return K // p, N
+    assert N % p == 0
+    return K, N // p
+
+
+def layer_set(workload: str, fused: bool = False, tp: int = 1):
     """The linears of one token.  fused=True stacks the rows of q/k/v and of
     gate/up (the NK layout makes that a concatenation) into one call each --
-    same weights, same bytes, 4 dependent calls per layer instead of 7."""
+    same weights, same bytes, 4 dependent calls per layer instead of 7.
+    tp=p gives rank 0's shard shapes of a p-way tensor-parallel layer set."""
     model = workload.rsplit("-", 1)[0]          # llama2-7b-decode -> llama2-7b
     spec = inputs.LLAMA_SETS[model]
+    if tp > 1:
+        spec = dict(spec)
+        spec["mats"] = [(nm, *tp_shard(nm, K, N, tp)) for nm, K, N in spec["mats"]]
+        spec["lm_head"] = tp_shard("lm_head", *spec["lm_head"], tp)
     mats = []
     for li in range(spec["layers"]):
         if fused:
@@ -147,7 +166,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     ops.lib()
-    model, mats = layer_set(args.workload, args.fused)
+    model, mats = layer_set(args.workload, args.fused, args.tp_shard)
     n = args.n
     t_gen = time.time()
     # One realistic weight per distinct shape (seed 1000*config + index),
@@ -284,7 +303,8 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "q4f16 (int4 codes x fp16 -> fp32 accumulate, fp16 out)",
         "data": "synthetic (seeded realistic q4f16 weights, N(0,1) fp16 x)",
-        "config": {"workload": args.workload + ("-fused-qkv-gateup" if args.fused else ""),
+        "config": {"workload": args.workload + ("-fused-qkv-gateup" if args.fused else "")
+                   + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else ""),
                    "model": model, "tokens_per_step": n,
                    "layers_linears": len(mats), "weight_bytes": int(sum(inputs.q4_bytes(K, N) for _, K, N in mats)),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
@@ -374,6 +394,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="tokens per step (decode: 1)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--tp-shard", type=int, default=1,
+                    help="run rank 0's shard of a p-way tensor-parallel layer set on this GPU "
+                         "(per-GPU compute-only time; no collective)")
     ap.add_argument("--fused", action="store_true",
                     help="stack q/k/v and gate/up rows into one call each (same weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
