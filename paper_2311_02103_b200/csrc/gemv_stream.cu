@@ -26,6 +26,7 @@
 //   * PDL: the producer starts streaming weights before griddepcontrol.wait;
 //     only the x loads and the y stores wait for the previous kernel.
 #include <cstdlib>
+#include <cstdio>
 #include "internal.h"
 #include "relax_q4.h"
 #include "ptx.cuh"
@@ -346,6 +347,10 @@ static GsConfig gs_config(int64_t K, int64_t N) {
     if (ns < nsmin) c.H = ns < 1 ? 1 : ns;          // (only for huge K with RPW = 1)
     c.NS = ns < 2 ? 2 : ns > 16 ? 16 : ns;
     if (c.NS < c.H) c.H = c.NS;
+    // NS a multiple of H: stage s -> slot s % NS then always belongs to row
+    // group s % H, i.e. every group owns a private sub-ring of NS/H slots
+    // (the classic one-consumer ring protocol per group).
+    c.NS -= c.NS % c.H;
     c.threads = (c.WK * c.H + 1) * 32;
     int mult = 1;
     if (const char* e = std::getenv("RELAX_Q4_GS_GRID_MULT")) { const int v = std::atoi(e); if (v >= 1 && v <= 4) mult = v; }
@@ -416,6 +421,9 @@ static int launch_gs_z(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                        const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
     const GsConfig c = gs_config(K, N);
+    if (std::getenv("RELAX_Q4_GS_PRINT"))
+        fprintf(stderr, "gemv_stream K=%lld N=%lld WK=%d H=%d RPW=%d RS=%d NS=%d threads=%d grid=%d smem=%zu\n",
+                (long long)K, (long long)N, c.WK, c.H, c.RPW, c.RS, c.NS, c.threads, c.grid, c.smem);
     const int zpf = gs_zpf();
     for (int64_t t0 = 0; t0 < n; t0 += 2) {
         const int cnt = (n - t0) >= 2 ? 2 : 1;
