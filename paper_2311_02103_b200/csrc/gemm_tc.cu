@@ -477,8 +477,8 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
     if (rc) return rc;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(tc_q4_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(Cfg::kSmemBytes));
+        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(tc_q4_kernel<BN>),
+                                        static_cast<int>(Cfg::kSmemBytes));
         if (e != cudaSuccess) return static_cast<int>(e);
         e = cudaFuncSetAttribute(tc_q4_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return static_cast<int>(e);

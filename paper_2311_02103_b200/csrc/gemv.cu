@@ -220,9 +220,7 @@ static int launch_gemv_nt(const GemvArgs& a, bool pdl, cudaStream_t stream) {
     if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidConfiguration);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemv_q4_kernel<NT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(227 * 1024));
+        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(gemv_q4_kernel<NT>), 227 * 1024);
         if (e != cudaSuccess) return static_cast<int>(e);
         attr_set = true;
     }

@@ -233,7 +233,7 @@ int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const ui
         if (fullc) {
             static bool set = false;
             if (!set) {
-                e = cudaFuncSetAttribute(gemv_row_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                e = set_kernel_smem(reinterpret_cast<const void*>(gemv_row_kernel<1>), 227 * 1024);
                 if (e != cudaSuccess) return static_cast<int>(e);
                 set = true;
             }
@@ -241,7 +241,7 @@ int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const ui
         } else {
             static bool set = false;
             if (!set) {
-                e = cudaFuncSetAttribute(gemv_row_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                e = set_kernel_smem(reinterpret_cast<const void*>(gemv_row_kernel<0>), 227 * 1024);
                 if (e != cudaSuccess) return static_cast<int>(e);
                 set = true;
             }

@@ -76,7 +76,7 @@ static size_t gs_ring_budget() {
     static size_t v = [] {
         const char* e = std::getenv("RELAX_Q4_GS_RING_KB");
         const int kb = e ? std::atoi(e) : 0;
-        return static_cast<size_t>(kb >= 72 && kb <= 190 ? kb : 104) * 1024;
+        return static_cast<size_t>(kb >= 72 && kb <= 190 ? kb : 112) * 1024;
     }();
     return v;
 }
@@ -386,7 +386,7 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
         auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 544>;
         static bool set = false;
         if (!set) {
-            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+            cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(k), 210 * 1024);
             if (e != cudaSuccess) return static_cast<int>(e);
             set = true;
         }
@@ -395,7 +395,7 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
     auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 1024>;   // K > 16K: one CTA per SM
     static bool set = false;
     if (!set) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(k), 210 * 1024);
         if (e != cudaSuccess) return static_cast<int>(e);
         set = true;
     }

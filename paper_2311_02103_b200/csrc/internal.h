@@ -17,6 +17,19 @@ constexpr size_t kTicketBytes = 4096;  // split-K tickets: fixed region at works
 constexpr int64_t kMaxSplitTiles = kTicketBytes / 4;
 constexpr int kMaxClusterSplit = 16;   // non-portable cluster size limit on sm_100
 
+// Per-kernel attributes set once before the first launch: the dynamic
+// shared-memory limit, and the maximum shared-memory carveout.  A fixed
+// carveout matters under programmatic dependent launch: an SM whose carveout
+// was sized for one kernel cannot take a CTA of the next kernel that needs a
+// different split until it drains, which serialised the chain and let the
+// next kernel pack two CTAs onto half the SMs.
+inline cudaError_t set_kernel_smem(const void* fn, int dyn_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                static_cast<int>(cudaSharedmemCarveoutMaxShared));
+}
+
 enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2 };
 
 struct Plan {

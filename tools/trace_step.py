@@ -75,7 +75,8 @@ def main():
         us = lambda v: (v - T0) / 1e3  # noqa: E731
         line = (f"{s:>4} {K:>5}x{N:<6} {len(q):>4} | {us(q['t0'].min()):7.2f} {us(q['t0'].max()):7.2f} | "
                 f"{np.median(q['tw'] - q['t0']) / 1e3:9.2f} {np.median(q['tf'] - q['t0']) / 1e3:9.2f} | "
-                f"{us(q['te'].min()):7.2f} {us(q['te'].max()):7.2f} | {np.median(q['te'] - q['tw']) / 1e3:7.2f}")
+                f"{us(q['te'].min()):7.2f} {us(q['te'].max()):7.2f} | {np.median(q['te'] - q['tw']) / 1e3:7.2f}"
+                f"  sm/cta {len(set(q['smid'].tolist()))}/{np.bincount(q['smid']).max()}")
         print(line)
         prev_end = q["te"].max()
     tot = (r["te"].max() - T0) / 1e3
