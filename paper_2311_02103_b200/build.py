@@ -24,7 +24,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "librelax_q4.so")
 
-SOURCES = ["abi.cpp", "gemv.cu", "gemv_stream.cu", "gemv_row.cu", "gemm_tc.cu"]
+SOURCES = ["abi.cpp", "gemv.cu", "gemv_stream.cu", "gemv_mma.cu", "gemv_row.cu", "gemm_tc.cu"]
 HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -452,19 +452,31 @@ static EncodeTiledFn get_encode_fn() {
     return fn;
 }
 
-static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
-                       uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
-                       CUtensorMapSwizzle sw) {
+// Tiled tensor map of rank 2..3 (dims innermost first; strides in bytes for
+// dims 1..rank-1).  Out-of-bounds box elements are zero-filled and still
+// counted in the mbarrier transaction bytes.
+int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
+                    const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                    CUtensorMapSwizzle sw) {
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return static_cast<int>(cudaErrorInitializationError);
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {row_bytes};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+    cuuint64_t d[3], st[2];
+    cuuint32_t bx[3], estr[3] = {1, 1, 1};
+    for (int i = 0; i < rank; ++i) { d[i] = dims[i]; bx[i] = box[i]; }
+    for (int i = 0; i + 1 < rank; ++i) st[i] = strides[i];
+    CUresult r = enc(m, dt, static_cast<cuuint32_t>(rank), const_cast<void*>(base), d, st, bx, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
+}
+
+static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                       uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                       CUtensorMapSwizzle sw) {
+    const uint64_t dims[2] = {inner, outer};
+    const uint64_t strides[1] = {row_bytes};
+    const uint32_t box[2] = {box_inner, box_outer};
+    return make_tensor_map(m, dt, 2, base, dims, strides, box, sw);
 }
 
 template <int BN>

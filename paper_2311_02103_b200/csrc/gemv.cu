@@ -239,17 +239,22 @@ static int launch_gemv_nt(const GemvArgs& a, bool pdl, cudaStream_t stream) {
 
 int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                 const uint16_t* s, uint16_t* y, int nt, bool pdl, cudaStream_t stream) {
-    // Lane-per-row kernel (gemv_row.cu) or the group-per-lane streamed kernel
-    // (gemv_stream.cu) for the decode shapes they support.
+    // Decode kernels: the streamed CUDA-core GEMV (gemv_stream.cu, default),
+    // the warp-MMA GEMV (gemv_mma.cu, measured slower so far: DESIGN.md §5.2),
+    // the lane-per-row GEMV (gemv_row.cu), then the generic one below.
+    // RELAX_Q4_GEMV_IMPL=stream|mma|row|v1 pins one (tests and measurements).
     static int impl = [] {
         const char* e = std::getenv("RELAX_Q4_GEMV_IMPL");
-        if (e && std::strcmp(e, "stream") == 0) return 1;
+        if (e && std::strcmp(e, "mma") == 0) return 1;
         if (e && std::strcmp(e, "row") == 0) return 2;
+        if (e && std::strcmp(e, "v1") == 0) return 3;
         return 0;
     }();
-    if (n == 1 && impl != 1 && gemv_row_ok(K) && impl == 2)
+    if (n == 1 && impl == 2 && gemv_row_ok(K))
         return launch_gemv_row(x, n, K, N, w, s, y, pdl, stream);
-    if (nt <= 2 && gemv_stream_ok(nt, K) && N >= 1)
+    if (impl == 1 && nt <= 2 && gemv_mma_ok(n >= 2 ? 2 : 1, K, N))
+        return launch_gemv_mma(x, n, K, N, w, s, y, pdl, stream);
+    if (impl <= 1 && nt <= 2 && gemv_stream_ok(nt, K) && N >= 1)
         return launch_gemv_stream(x, n, K, N, w, s, y, pdl, stream);
     if (nt < 1 || nt > kGemvMaxNT) nt = kGemvMaxNT;
     for (int64_t t0 = 0; t0 < n; t0 += nt) {

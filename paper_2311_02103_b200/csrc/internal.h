@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace rq4 {
@@ -58,6 +59,12 @@ int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                        const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 bool gemv_stream_ok(int nt, int64_t K);
+int launch_gemv_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+                    const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
+bool gemv_mma_ok(int nt, int64_t K, int64_t N);
+int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
+                    const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                    CUtensorMapSwizzle sw);
 int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                     const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 bool gemv_row_ok(int64_t K);
