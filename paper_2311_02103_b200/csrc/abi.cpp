@@ -28,29 +28,49 @@ int gemv_max_n() {
 static int ctas_per_sm_tc(int bn) { return bn <= 64 ? 2 : 1; }
 
 static int choose_bn(int64_t n, int64_t N) {
+    (void)N;
     if (n <= 16) return 16;
     if (n <= 32) return 32;
     if (n <= 64) return 64;
-    const int64_t tm = (N + kTcBM - 1) / kTcBM;
-    if (n <= 128) return 128;
-    const int64_t t256 = tm * ((n + 255) / 256);
-    return t256 >= kNumSMs ? 256 : 128;
+    return 128;                  // n > 64: refined jointly with the split (choose_tc_large)
 }
 
-// Split-K factor.  Small n (<= 64) is HBM-bound: aim for about one CTA per
+// n > 64 (tensor-bound): pick the token tile BN in {128, 256} and the split-K
+// factor s <= 8 together, minimising a wave-quantised time model fitted to
+// the measured sweeps (profiles/sweep_c3_*.jsonl):
+//   waves = ceil(tiles * s / 148)           (one CTA per SM at BN >= 128)
+//   t(us) = waves * (ceil(kt / s) * step + fixed) + [s > 1] * 3
+//   step  = 0.92 / 1.3 us per 256-k stage, fixed = 5.7 / 8.0 us at BN = 128 / 256.
+// Split-K only within one wave: a multi-wave grid of split-K clusters was
+// measured far slower than the model (cluster placement), so s > 1 requires
+// tiles * s <= 148.  The model only ranks schedules; results never depend on
+// it (every BN/split meets the same tolerance).
+static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out) {
+    const int64_t tm = (N + kTcBM - 1) / kTcBM;
+    double best = 1e300;
+    int bb = 128, bs = 1;
+    for (int bn : {128, 256}) {
+        const int64_t tiles = tm * ((n + bn - 1) / bn);
+        const double step = bn == 256 ? 1.3 : 0.92;
+        const double fixed = bn == 256 ? 8.0 : 5.7;
+        for (int s = 1; s <= 8 && s <= kt; ++s) {
+            if (s > 1 && (tiles > kMaxSplitTiles || tiles * s > kNumSMs)) break;
+            const int64_t waves = (tiles * s + kNumSMs - 1) / kNumSMs;
+            const int ks = (kt + s - 1) / s;
+            const double t = static_cast<double>(waves) * (ks * step + fixed) + (s > 1 ? 3.0 : 0.0);
+            if (t < best * 0.999) { best = t; bb = bn; bs = s; }
+        }
+    }
+    *bn_out = bb;
+    *s_out = bs;
+}
+
+// Split-K factor for small n (<= 64, HBM-bound): aim for about one CTA per
 // SM (RELAX_Q4_TC_CTAS_PER_SM scales the target), so that the next kernel's
-// CTAs fit beside this one (PDL) and every CTA streams a long K range.  Larger
-// n is tensor-bound and split-K only adds reduction work, so split only when
-// the tiles cover less than half a wave, and by at most 4.
+// CTAs fit beside this one (PDL) and every CTA streams a long K range.
 static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
     (void)bn;
-    if (n > 64) {
-        if (tiles * 2 >= kNumSMs) return 1;
-        int s = static_cast<int>((kNumSMs + tiles - 1) / tiles);
-        if (s > 4) s = 4;
-        if (s > kt / 4) s = kt / 4 < 1 ? 1 : kt / 4;
-        return s;
-    }
+    (void)n;
     static double f = [] {
         const char* e = std::getenv("RELAX_Q4_TC_CTAS_PER_SM");
         const double v = e ? std::atof(e) : 0.0;
@@ -88,16 +108,21 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
     } else if (v == kVariantTc) {
         if (!tc_ok) return RELAX_ERR_UNSUPPORTED_SHAPE;
         p.variant = kVariantTc;
+        const int kt = static_cast<int>(K / kTcWStageK);
+        int auto_split = 0;
         if (force_bn) {
             if (force_bn != 16 && force_bn != 32 && force_bn != 64 && force_bn != 128 && force_bn != 256)
                 return RELAX_ERR_INVALID_ARG;
             p.bn = force_bn;
+        } else if (n > 64 && force_split <= 0) {
+            choose_tc_large(n, N, kt, &p.bn, &auto_split);
         } else {
             p.bn = choose_bn(n, N);
         }
-        const int kt = static_cast<int>(K / kTcWStageK);
         const int64_t tiles = ((N + kTcBM - 1) / kTcBM) * ((n + p.bn - 1) / p.bn);
-        int s = force_split > 0 ? force_split : choose_split(n, tiles, kt, p.bn);
+        int s = force_split > 0 ? force_split
+              : auto_split > 0 ? auto_split
+              : n > 64 ? 1 : choose_split(n, tiles, kt, p.bn);
         if (s > kt) s = kt;
         if (s < 1) s = 1;
         if (s > 1 && tiles > kMaxSplitTiles) {
