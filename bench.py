@@ -285,7 +285,10 @@ def run_ours(args, rank, world, local_rank):
     else:
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / peaks["hbm_gbs"], 4), "peak_src": f"{peaks['src']} hbm copy"}
-    roof["traffic"] = traffic_per_launch(args.workload, n)
+    label = (args.workload + ("-fused-qkv-gateup" if args.fused else "")
+             + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else ""))
+    roof["traffic"] = traffic_per_launch(label, n)
+    roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
     roof["kernel"] = "gemv_stream_kernel (streamed GEMV)" if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" \
         else "tc_q4_kernel"
     roof["per"] = "average over all launches of the step (every launch is this kernel family)"
@@ -303,8 +306,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "q4f16 (int4 codes x fp16 -> fp32 accumulate, fp16 out)",
         "data": "synthetic (seeded realistic q4f16 weights, N(0,1) fp16 x)",
-        "config": {"workload": args.workload + ("-fused-qkv-gateup" if args.fused else "")
-                   + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else ""),
+        "config": {"workload": label,
                    "model": model, "tokens_per_step": n,
                    "layers_linears": len(mats), "weight_bytes": int(sum(inputs.q4_bytes(K, N) for _, K, N in mats)),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
