@@ -126,14 +126,15 @@ __device__ __forceinline__ int reduce_row_of_lane(int lane) {
 //            (1 SHF + 4 LOP3 + 4 HFMA2 per 8 codes), then 8 FHFMA;
 //   ZPF = 1: factored zero point -- codes as fp16 subnormals q * 2^-24 (pure
 //            masks, 1 SHF + 4 LOP3 per 8 codes), 8 FHFMA, and per group
-//            sum (q - 7) x = 2^24 (acc_e + acc_o / 16) - 7 * sum x.
+//            2^-24 sum (q - 7) x = acc_e + acc_o / 16, with acc_e started at
+//            m7x = -7 * 2^-24 * sum x; the 2^24 is applied once per output.
 template <int NT, int ZPF>
 __device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const uint4 (&xr)[NT][4],
                                         const float (&m7x)[NT], float (&out)[NT]) {
     const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
     float ge[NT], go[NT];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) { ge[t] = 0.f; go[t] = 0.f; }
+    for (int t = 0; t < NT; ++t) { ge[t] = ZPF ? m7x[t] : 0.f; go[t] = 0.f; }
 #pragma unroll
     for (int wi = 0; wi < 4; ++wi) {
         uint32_t c0, c1, c2, c3;
@@ -168,8 +169,7 @@ __device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const u
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
         if (ZPF) {
-            const float u = fmaf(go[t], 0.0625f, ge[t]);
-            out[t] = sc * fmaf(u, 16777216.0f, m7x[t]);
+            out[t] = sc * fmaf(go[t], 0.0625f, ge[t]);          // units of 2^-24
         } else {
             out[t] = sc * (ge[t] + go[t]);
         }
@@ -251,8 +251,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
                     sx += f.x + f.y;
                 }
             }
-            m7x[t] = -7.0f * sx;
+            m7x[t] = ZPF ? -7.0f * 5.9604644775390625e-08f * sx : 0.f;   // -7 * 2^-24 * sum x
         }
+        if (a.trace_seq && warp == 0 && lane == 0) tr_first = gtime();   // x in registers
         const int rsel = reduce_row_of_lane<RPW>(lane);
         const bool writer = (lane & (32 / RPW - 1)) == 0;
         // Stages (RPW rows each) go round-robin to the H row groups: warp (h, kw)
@@ -266,7 +267,6 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
             const int r_base = st * a.RS;
             const int nr = rows - r_base < a.RS ? rows - r_base : a.RS;
             mbar_wait(&full[slot], phase);
-            if (a.trace_seq && r_base == 0 && warp == 0 && lane == 0) tr_first = gtime();
             const uint8_t* stage = ring + static_cast<size_t>(slot) * a.stage_bytes;
             float acc[NT][RPW];
 #pragma unroll
@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         const int t = o - rl * NT;
         float sum = 0.f;
         for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
+        if (ZPF) sum *= 16777216.0f;                        // exact power-of-two rescale
         a.y[static_cast<int64_t>(t) * a.N + row0 + rl] = __half_as_ushort(__float2half_rn(sum));
     }
     if (a.trace_seq) {
