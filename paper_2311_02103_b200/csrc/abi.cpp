@@ -65,16 +65,17 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
     *s_out = bs;
 }
 
-// Split-K factor for small n (<= 64, HBM-bound): aim for about one CTA per
-// SM (RELAX_Q4_TC_CTAS_PER_SM scales the target), so that the next kernel's
-// CTAs fit beside this one (PDL) and every CTA streams a long K range.
+// Split-K factor for small n (<= 64, HBM-bound): aim for about two CTAs per
+// SM -- the occupancy of the BN <= 64 tiles -- so every SM streams with two
+// pipelines (RELAX_Q4_TC_CTAS_PER_SM scales the target; measured 1.0 vs 2.0
+// in DESIGN.md §6: 2.0 is 3-20% faster on every 7B shape at n = 3..64).
 static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
     (void)bn;
     (void)n;
     static double f = [] {
         const char* e = std::getenv("RELAX_Q4_TC_CTAS_PER_SM");
         const double v = e ? std::atof(e) : 0.0;
-        return v > 0.1 && v <= 4.0 ? v : 1.0;
+        return v > 0.1 && v <= 4.0 ? v : 2.0;
     }();
     const double target = f * kNumSMs;
     int s = static_cast<int>(target / static_cast<double>(tiles) + 0.5);
