@@ -129,6 +129,66 @@ RELAX_API int relax_q4_matmul_ex(const void* x, int64_t n, int64_t K, int64_t N,
                        void* workspace, size_t ws_bytes, int variant, int split_k,
                        int bn, unsigned flags, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Fused neighbours: the dequant-matmul with the element-wise
+ * operators of a Llama decoder block fused into it, the way FuseOps /
+ * FuseTensorIR fold element-wise producers and consumers into the tensor
+ * program of the matmul ("absorb ... downstream ElementWise",
+ * SPEC S:472).  Fusion preserves the semantics of the unfused fp16 program
+ * (P:483-494), so each operator is defined exactly as the unfused kernel
+ * chain computes it, fp16 at every tensor boundary (DESIGN.md §3 readings
+ * 16-18):
+ *
+ *   RELAX_OP_RMSNORM_X  (prologue on x, Llama RMSNorm)
+ *       r_t     = 1 / sqrt(mean_k x[t][k]^2 + eps)          (fp32)
+ *       xn[t,k] = fp16_RNE(fp16_RNE(x[t][k] * r_t) * gamma[k])
+ *       and the matmul consumes xn instead of x.
+ *   RELAX_OP_SILU_MUL   (epilogue, SwiGLU): the weight rows are interleaved
+ *       pairs -- row 2j is gate_j, row 2j+1 is up_j (a one-time repack of the
+ *       two matrices, F3) -- and with g = fp16_RNE(acc[2j]), u = fp16_RNE(acc[2j+1])
+ *       y[t][j] = fp16_RNE(silu(g) * u),  silu(g) = g / (1 + exp(-g))  (fp32)
+ *       so y has N/2 columns.
+ *   RELAX_OP_RESIDUAL   (epilogue, residual add), applied last:
+ *       y[t][j] = fp16_RNE(v + residual[t][j]),  v = the fp16 output so far.
+ *
+ * Combinations are allowed; the order is prologue, matmul, SiLU-mul, residual.
+ */
+#define RELAX_OP_RMSNORM_X 1u
+#define RELAX_OP_SILU_MUL 2u
+#define RELAX_OP_RESIDUAL 4u
+
+typedef struct relax_q4_fusion {
+    uint32_t ops;             /* RELAX_OP_* bitmask (0 = plain matmul) */
+    float rms_eps;            /* RMSNORM_X: epsilon (>= 0, finite) */
+    const void* rms_weight;   /* RMSNORM_X: device fp16 [K] (gamma), 16-byte aligned */
+    const void* residual;     /* RESIDUAL: device fp16 [n][N_out], 16-byte aligned; may be
+                                 exactly y (in-place add) but not partially overlap it */
+} relax_q4_fusion;
+
+/* Workspace plan of relax_q4_matmul_fused for n <= n_max: the plain plan plus
+ * n_max*K*2 bytes for the normalised x when RMSNORM_X is requested and some
+ * n <= n_max takes the tensor-core path (the decode GEMV normalises in
+ * registers).  Same guarantee and zero-fill contract as relax_plan_workspace.
+ * Errors: as relax_plan_workspace, plus RELAX_ERR_INVALID_ARG for unknown ops
+ * bits and RELAX_ERR_UNSUPPORTED_SHAPE when ops != 0 and K % 256 != 0 or
+ * (SILU_MUL) N is odd. */
+RELAX_API int relax_plan_workspace_fused(int64_t n_max, int64_t K, int64_t N, uint32_t ops,
+                                         size_t* ws_bytes);
+
+/* y = ops(x, W): the fused form above; with fusion == NULL or ops == 0 it is
+ * relax_q4_matmul_ws.
+ *   y         device fp16 [n][N_out], N_out = N/2 with SILU_MUL, else N
+ *   fusion    host pointer to the descriptor (read during the call only)
+ * Errors: as relax_q4_matmul_ws, plus RELAX_ERR_INVALID_ARG (unknown ops bits,
+ * missing rms_weight/residual, eps < 0 or not finite), RELAX_ERR_MISALIGNED,
+ * RELAX_ERR_ALIAS (residual partially overlapping y, or y overlapping x,
+ * gamma, weights), RELAX_ERR_UNSUPPORTED_SHAPE (ops != 0 needs K % 256 == 0;
+ * SILU_MUL needs N even). */
+RELAX_API int relax_q4_matmul_fused(const void* x, int64_t n, int64_t K, int64_t N,
+                                    const uint32_t* packed_w, const void* scales, void* y,
+                                    const relax_q4_fusion* fusion, void* workspace,
+                                    size_t ws_bytes, void* stream);
+
 /* Host-only report of the schedule relax_q4_matmul_ws would use for (n,K,N):
  * out pointers may be NULL.  variant: enum relax_variant; tile: GEMV tokens
  * per launch or TC token tile; split_k: TC split factor; ws_bytes: bytes

@@ -24,8 +24,8 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "librelax_q4.so")
 
-SOURCES = ["abi.cpp", "gemv.cu", "gemv_stream.cu", "gemv_mma.cu", "gemv_row.cu", "gemm_tc.cu"]
-HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh"]
+SOURCES = ["abi.cpp", "gemv.cu", "gemv_stream.cu", "gemv_mma.cu", "gemv_row.cu", "gemm_tc.cu", "fused.cu"]
+HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh", "fusion.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

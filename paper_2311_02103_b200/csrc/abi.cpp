@@ -2,6 +2,7 @@
 // shape-specialised dispatch on the runtime token count n (P:409-413,
 // P:432-433), the upper-bound workspace plan, and the
 // launches.  No exceptions cross this boundary; nothing here allocates.
+#include <cmath>
 #include "relax_q4.h"
 
 #include <cstdlib>
@@ -226,9 +227,130 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
     return RELAX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Fused neighbours (relax_q4_matmul_fused; include/relax_q4.h).  The plain
+// plan picks the variant; RMSNORM_X on the tensor-core path writes the
+// normalised x into the workspace after the plan's own bytes.
+static constexpr uint32_t kOpsAll = RELAX_OP_RMSNORM_X | RELAX_OP_SILU_MUL | RELAX_OP_RESIDUAL;
+
+static size_t align16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
+
+static int fused_shape_check(int64_t K, int64_t N, uint32_t ops) {
+    if (ops & ~kOpsAll) return RELAX_ERR_INVALID_ARG;
+    if (ops != 0 && K % kTcWStageK != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if ((ops & RELAX_OP_SILU_MUL) && (N % 2) != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    return RELAX_OK;
+}
+
+static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
+                      const void* scales, void* y, const relax_q4_fusion* fz, void* ws, size_t ws_bytes,
+                      void* stream) {
+    const uint32_t ops = fz ? fz->ops : 0u;
+    if (ops == 0) return matmul_impl(x, n, K, N, packed_w, scales, y, ws, ws_bytes, 0, 0, 0, 0u, stream);
+    if (n < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
+    if (K % kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    int rc = fused_shape_check(K, N, ops);
+    if (rc != RELAX_OK) return rc;
+    if ((ops & RELAX_OP_RMSNORM_X) && (!fz->rms_weight || !(fz->rms_eps >= 0.f) || !std::isfinite(fz->rms_eps)))
+        return RELAX_ERR_INVALID_ARG;
+    if ((ops & RELAX_OP_RESIDUAL) && !fz->residual) return RELAX_ERR_INVALID_ARG;
+    if (n == 0) return RELAX_OK;
+    if (!x || !packed_w || !scales || !y) return RELAX_ERR_INVALID_ARG;
+    if (ws_bytes > 0 && !ws) return RELAX_ERR_INVALID_ARG;
+    const void* gamma = (ops & RELAX_OP_RMSNORM_X) ? fz->rms_weight : nullptr;
+    const void* res = (ops & RELAX_OP_RESIDUAL) ? fz->residual : nullptr;
+    if (!aligned16(x) || !aligned16(packed_w) || !aligned16(scales) || !aligned16(y) ||
+        (ws && !aligned16(ws)) || (gamma && !aligned16(gamma)) || (res && !aligned16(res)))
+        return RELAX_ERR_MISALIGNED;
+    const int64_t Nout = (ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
+    const size_t xb = static_cast<size_t>(n) * K * 2, yb = static_cast<size_t>(n) * Nout * 2;
+    const size_t wb = static_cast<size_t>(N) * K / 2, sb = static_cast<size_t>(N) * (K / kGroup) * 2;
+    const size_t gb = gamma ? static_cast<size_t>(K) * 2 : 0;
+    if (overlap(y, yb, x, xb) || overlap(y, yb, packed_w, wb) || overlap(y, yb, scales, sb) ||
+        overlap(y, yb, gamma, gb) || overlap(y, yb, ws, ws_bytes) || overlap(ws, ws_bytes, x, xb) ||
+        overlap(ws, ws_bytes, packed_w, wb) || overlap(ws, ws_bytes, scales, sb) ||
+        overlap(ws, ws_bytes, gamma, gb) || overlap(ws, ws_bytes, res, res ? yb : 0) ||
+        (res && res != y && overlap(y, yb, res, yb)))
+        return RELAX_ERR_ALIAS;
+    Plan plan;
+    rc = make_plan(n, K, N, kVariantAuto, 0, 0, &plan, false);
+    if (rc == RELAX_OK && plan.ws_bytes > 0 && ws_bytes < plan.ws_bytes) {
+        const int sp = plan.split < 8 ? plan.split : 8;
+        rc = make_plan(n, K, N, kVariantAuto, sp, 0, &plan, false);
+    }
+    if (rc != RELAX_OK) return rc;
+    const bool tc_norm = plan.variant == kVariantTc && (ops & RELAX_OP_RMSNORM_X);
+    const size_t xn_off = align16(plan.ws_bytes);
+    const size_t need = tc_norm ? xn_off + xb : plan.ws_bytes;
+    if (need > ws_bytes) return RELAX_ERR_WORKSPACE;
+    if (plan.variant == kVariantGemv && !gemv_stream_ok(plan.nt < 2 ? plan.nt : 2, K))
+        return RELAX_ERR_UNSUPPORTED_SHAPE;
+    rc = check_device();
+    if (rc != RELAX_OK) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Fusion fu;
+    fu.ops = ops;
+    fu.eps = (ops & RELAX_OP_RMSNORM_X) ? fz->rms_eps : 0.f;
+    fu.gamma = static_cast<const uint16_t*>(gamma);
+    fu.res = static_cast<const uint16_t*>(res);
+    int e;
+    if (plan.variant == kVariantGemv) {
+        e = launch_gemv_stream(static_cast<const uint16_t*>(x), n, K, N, packed_w,
+                               static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), true, st, fu);
+    } else {
+        const uint16_t* xin = static_cast<const uint16_t*>(x);
+        e = 0;
+        if (tc_norm) {
+            uint16_t* xn = reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(ws) + xn_off);
+            e = launch_rmsnorm(xin, n, K, fu.gamma, fu.eps, xn, true, st);
+            xin = xn;
+        }
+        if (e == 0)
+            e = launch_tc(xin, n, K, N, packed_w, static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y),
+                          plan, ws, true, st, fu);
+    }
+    if (e != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
 }  // namespace rq4
 
 extern "C" {
+
+int relax_plan_workspace_fused(int64_t n_max, int64_t K, int64_t N, uint32_t ops, size_t* ws_bytes) {
+    if (!ws_bytes || n_max < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
+    if (K % rq4::kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    int rc = rq4::fused_shape_check(K, N, ops);
+    if (rc != RELAX_OK) return rc;
+    const int64_t n_cap = static_cast<int64_t>(rq4::kNumSMs) * 256;
+    const int64_t hi = n_max < n_cap ? n_max : n_cap;
+    const bool norm = (ops & RELAX_OP_RMSNORM_X) != 0;
+    size_t best = 0;
+    for (int64_t n = 1; n <= hi; ++n) {
+        rq4::Plan p;
+        rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
+        if (rc != RELAX_OK) return rc;
+        size_t need = p.ws_bytes;
+        if (norm && p.variant == rq4::kVariantTc) need = rq4::align16(p.ws_bytes) + static_cast<size_t>(n) * K * 2;
+        if (need > best) best = need;
+    }
+    if (norm && n_max > hi) {
+        // beyond n_cap every schedule is split-free (no plan bytes) and takes the TC path
+        const size_t need = static_cast<size_t>(n_max) * K * 2;
+        if (need > best) best = need;
+    }
+    *ws_bytes = best;
+    return RELAX_OK;
+}
+
+int relax_q4_matmul_fused(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
+                          const void* scales, void* y, const relax_q4_fusion* fusion, void* workspace,
+                          size_t ws_bytes, void* stream) {
+    return rq4::fused_impl(x, n, K, N, packed_w, scales, y, fusion, workspace, ws_bytes, stream);
+}
 
 int relax_plan_workspace(int64_t n_max, int64_t K, int64_t N, size_t* ws_bytes) {
     if (!ws_bytes || n_max < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;

@@ -37,6 +37,7 @@
 #include "relax_q4.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
+#include "fusion.cuh"
 
 namespace rq4 {
 
@@ -76,7 +77,28 @@ struct TcArgs {
     int kt;               // number of 256-k W stages covering K
     int cluster;          // 1: split-K partials reduced through DSMEM of the cluster
     int trace;            // record role wait cycles (debug)
+    uint32_t ops;         // fused epilogue (RELAX_OP_SILU_MUL / RESIDUAL; RMSNORM_X runs before)
+    const uint16_t* res;  // RESIDUAL: fp16 [n][Nout]
+    int64_t Nout;         // N/2 with SILU_MUL, else N (row stride of y)
 };
+
+// Final store of output element (tok, row) with value f (fp32 sum) under the
+// fused epilogue.  SILU_MUL pairs rows (2j, 2j+1), which sit in adjacent
+// lanes of the calling warp: every lane of `mask` must call this (the pair
+// exchange is a shuffle), and only the even row of a valid pair stores.
+__device__ __forceinline__ void tc_store(const TcArgs& a, unsigned mask, int64_t tok, int64_t row, float f,
+                                         bool valid) {
+    if (a.ops & RELAX_OP_SILU_MUL) {
+        const float fp = __shfl_xor_sync(mask, f, 1);
+        if (valid && (row & 1) == 0) {
+            const int64_t idx = tok * a.Nout + row / 2;
+            a.y[idx] = epilogue_value(silu_mul_value(f, fp), a.ops, a.res, idx);
+        }
+    } else if (valid) {
+        const int64_t idx = tok * a.Nout + row;
+        a.y[idx] = epilogue_value(__half_as_ushort(__float2half_rn(f)), a.ops, a.res, idx);
+    }
+}
 
 template <int BN>
 struct TcCfg {
@@ -334,10 +356,11 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int64_t tok = n0 + c0 + i;
-                    if (row_ok && tok < a.n) {
-                        const float f = __uint_as_float(v[i]);
-                        if (split) a.part[(static_cast<int64_t>(z) * a.n + tok) * a.N + row] = f;
-                        else a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(f));
+                    const float f = __uint_as_float(v[i]);
+                    if (split) {
+                        if (row_ok && tok < a.n) a.part[(static_cast<int64_t>(z) * a.n + tok) * a.N + row] = f;
+                    } else {
+                        tc_store(a, 0xffffffffu, tok, row, f, row_ok && tok < a.n);
                     }
                 }
             }
@@ -354,23 +377,23 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (*flag_slot) {
                     __threadfence();
-                    if (row_ok) {
 #pragma unroll 1
-                        for (int c0 = 0; c0 < BN; c0 += 8) {
-                            float sum[8];
+                    for (int c0 = 0; c0 < BN; c0 += 8) {
+                        float sum[8];
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) sum[u] = 0.f;
+                        for (int u = 0; u < 8; ++u) sum[u] = 0.f;
+                        if (row_ok) {
                             for (int s = 0; s < a.split; ++s) {
                                 const float* ps = a.part + (static_cast<int64_t>(s) * a.n + n0 + c0) * a.N + row;
 #pragma unroll
                                 for (int u = 0; u < 8; ++u)
                                     if (n0 + c0 + u < a.n) sum[u] += __ldcg(ps + static_cast<int64_t>(u) * a.N);
                             }
+                        }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) {
-                                const int64_t tok = n0 + c0 + u;
-                                if (tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(sum[u]));
-                            }
+                        for (int u = 0; u < 8; ++u) {
+                            const int64_t tok = n0 + c0 + u;
+                            tc_store(a, 0xffffffffu, tok, row, sum[u], row_ok && tok < a.n);
                         }
                     }
                 }
@@ -401,14 +424,16 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         const uint32_t S = static_cast<uint32_t>(a.split);
         const uint32_t r = cluster_ctarank();
         constexpr uint32_t E = kTcBM * BN;
-        const uint32_t e0 = r * E / S, e1 = (r + 1) * E / S;
+        // element ranges start on even elements, so a (gate, up) row pair of the
+        // SiLU-mul epilogue stays within one CTA and one lane pair
+        const uint32_t e0 = r * (E / 2) / S * 2, e1 = (r + 1) * (E / 2) / S * 2;
         const uint32_t red_addr = smem_u32(red);
         for (uint32_t e = e0 + threadIdx.x; e < e1; e += kTcThreads) {
             float sum = 0.f;
             for (uint32_t s = 0; s < S; ++s) sum += ld_dsmem_f32(mapa_shared(red_addr + e * 4u, s));
             const int64_t tok = n0 + static_cast<int64_t>(e / kTcBM);
             const int64_t rr = m0 + static_cast<int64_t>(e % kTcBM);
-            if (tok < a.n && rr < a.N) a.y[tok * a.N + rr] = __half_as_ushort(__float2half_rn(sum));
+            tc_store(a, __activemask(), tok, rr, sum, tok < a.n && rr < a.N);
         }
         cluster_arrive_release();
         cluster_wait_acquire();
@@ -528,7 +553,7 @@ size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split) {
 
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
               const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
-              cudaStream_t stream) {
+              cudaStream_t stream, const Fusion& fu) {
     CUtensorMap mw, ms;
     int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
@@ -542,6 +567,9 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.kt = static_cast<int>((K + kTcWStageK - 1) / kTcWStageK);
     a.part = nullptr; a.cnt = nullptr;
     a.cluster = plan.cluster;
+    a.ops = fu.ops & (RELAX_OP_SILU_MUL | RELAX_OP_RESIDUAL);
+    a.res = fu.res;
+    a.Nout = (fu.ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
     static int tr = [] { const char* e = std::getenv("RELAX_Q4_TRACE"); return (e && *e == '1') ? 1 : 0; }();
     a.trace = tr;
     if (plan.split > 1 && !plan.cluster) {

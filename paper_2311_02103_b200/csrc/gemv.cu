@@ -254,7 +254,7 @@ int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32
         return launch_gemv_row(x, n, K, N, w, s, y, pdl, stream);
     if (impl == 1 && nt <= 2 && gemv_mma_ok(n >= 2 ? 2 : 1, K, N))
         return launch_gemv_mma(x, n, K, N, w, s, y, pdl, stream);
-    if (impl <= 1 && nt <= 2 && gemv_stream_ok(nt, K) && N >= 1)
+    if (impl <= 1 && nt <= 2 && gemv_stream_ok(nt, K) && N >= 1 && N < (int64_t{1} << 24))
         return launch_gemv_stream(x, n, K, N, w, s, y, pdl, stream);
     if (nt < 1 || nt > kGemvMaxNT) nt = kGemvMaxNT;
     for (int64_t t0 = 0; t0 < n; t0 += nt) {

@@ -31,6 +31,7 @@
 #include "relax_q4.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
+#include "fusion.cuh"
 
 namespace rq4 {
 
@@ -44,6 +45,12 @@ struct GsArgs {
     uint32_t stage_bytes;  // RS * (K/2 + K/16)
     int rows_cta_max;
     uint32_t trace_seq;    // 0 = no trace, else launch sequence number
+    // fused neighbours (include/relax_q4.h RELAX_OP_*)
+    uint32_t ops;
+    float eps;             // RMSNORM_X
+    const uint16_t* gamma; // RMSNORM_X: fp16 [K]
+    const uint16_t* res;   // RESIDUAL: fp16 [NT][Nout]
+    int64_t Nout;          // N/2 with SILU_MUL, else N (row stride of y and res)
 };
 
 // ---- optional per-CTA timeline (RELAX_Q4_TRACE=1; include/relax_q4_debug.h)
@@ -176,7 +183,66 @@ __device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const u
     }
 }
 
-template <int NT, int RPW, int ZPF, int FULLG, int MAXT>
+// ---- fused neighbours (RELAX_OP_*, include/relax_q4.h) -------------------
+// RMSNorm prologue on the x registers: r_t = 1/sqrt(mean x^2 + eps) over the
+// whole row (per-lane sums -> warp shuffle -> one partial per K-column warp in
+// shared memory -> every consumer sums the WK partials in fixed order), then
+// x <- fp16(fp16(x * r_t) * gamma) in place.  `scratch` is the partial-sum
+// area, free before the stage loop.
+template <int NT>
+__device__ __forceinline__ void rmsnorm_prologue(uint4 (&xr)[NT][4], const GsArgs& a, bool gv, int g, int warp,
+                                                 int lane, int kw, int h, int nwc, float* scratch) {
+    uint4 gm[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        gm[q] = gv ? reinterpret_cast<const uint4*>(a.gamma + g * 32)[q] : make_uint4(0u, 0u, 0u, 0u);
+    float ss[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t w4[4] = {xr[t][q].x, xr[t][q].y, xr[t][q].z, xr[t][q].w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f = __half22float2(u32_as_h2(w4[u]));
+                acc = fmaf(f.x, f.x, acc);
+                acc = fmaf(f.y, f.y, acc);
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        ss[t] = acc;
+    }
+    if (h == 0 && lane == 0)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) scratch[kw * NT + t] = ss[t];
+    asm volatile("bar.sync 1, %0;" :: "r"(nwc * 32) : "memory");
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        float tot = 0.f;
+        for (int c = 0; c < a.WK; ++c) tot += scratch[c * NT + t];
+        const float r = 1.0f / sqrtf(tot / static_cast<float>(a.K) + a.eps);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t w4[4] = {xr[t][q].x, xr[t][q].y, xr[t][q].z, xr[t][q].w};
+            const uint32_t g4[4] = {gm[q].x, gm[q].y, gm[q].z, gm[q].w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f = __half22float2(u32_as_h2(w4[u]));
+                const __half2 hn = __floats2half2_rn(f.x * r, f.y * r);        // cast back to fp16
+                w4[u] = h2_as_u32(__hmul2(hn, u32_as_h2(g4[u])));              // fp16 * gamma, one rounding
+            }
+            xr[t][q] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
+    }
+    // everyone has read the partials before the stage loop overwrites them
+    asm volatile("bar.sync 1, %0;" :: "r"(nwc * 32) : "memory");
+}
+
+// FU = 0: the plain matmul (the fused-neighbour code is compiled out, so the
+// decode kernel of relax_q4_matmul is exactly the unfused one); FU = 1: a.ops.
+template <int NT, int RPW, int ZPF, int FULLG, int MAXT, int FU>
 __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kernel(const __grid_constant__ GsArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
@@ -188,8 +254,14 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
     uint8_t* ring = smem + 256;
     float* part = reinterpret_cast<float*>(ring + static_cast<size_t>(a.NS) * a.stage_bytes + 1024);
 
-    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * a.N / gridDim.x;
-    const int64_t row1 = static_cast<int64_t>(blockIdx.x + 1) * a.N / gridDim.x;
+    // rows of this CTA; with SILU_MUL whole (gate, up) pairs
+    // (32-bit arithmetic: N < 2^24 is checked on the host; a 64-bit division
+    // here would delay the producer's first copy on every launch)
+    const uint32_t ops = FU ? a.ops : 0u;
+    const uint32_t pair = (ops & RELAX_OP_SILU_MUL) ? 2u : 1u;
+    const uint32_t units = static_cast<uint32_t>(a.N) / pair;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x * units / gridDim.x * pair);
+    const int64_t row1 = static_cast<int64_t>((blockIdx.x + 1) * units / gridDim.x * pair);
     const int rows = static_cast<int>(row1 - row0);
     const int nst = (rows + a.RS - 1) / a.RS;
     const uint32_t cb_row = static_cast<uint32_t>(a.K / 2);
@@ -236,11 +308,14 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         uint4 xr[NT][4];
         float m7x[NT];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
+        for (int t = 0; t < NT; ++t)
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 xr[t][q] = gv ? reinterpret_cast<const uint4*>(a.x + static_cast<int64_t>(t) * a.K + g * 32)[q]
                               : make_uint4(0u, 0u, 0u, 0u);
+        if (ops & RELAX_OP_RMSNORM_X) rmsnorm_prologue<NT>(xr, a, gv, g, warp, lane, kw, h, nwc, part);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
             float sx = 0.f;           // sum of the group's x (factored zero point)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -293,13 +368,30 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
     }
     __syncthreads();
     // fixed-order sum over the WK K-columns; fp32 -> fp16 RNE
-    for (int o = threadIdx.x; o < rows * NT; o += blockDim.x) {
-        const int rl = o / NT;
-        const int t = o - rl * NT;
-        float sum = 0.f;
-        for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
-        if (ZPF) sum *= 16777216.0f;                        // exact power-of-two rescale
-        a.y[static_cast<int64_t>(t) * a.N + row0 + rl] = __half_as_ushort(__float2half_rn(sum));
+    const float rescale = ZPF ? 16777216.0f : 1.0f;          // exact power-of-two rescale
+    if (ops & RELAX_OP_SILU_MUL) {
+        const int np = rows / 2;
+        for (int o = threadIdx.x; o < np * NT; o += blockDim.x) {
+            const int pl = o / NT;
+            const int t = o - pl * NT;
+            float sg = 0.f, su = 0.f;
+            for (int c = 0; c < a.WK; ++c) {
+                sg += part[(static_cast<size_t>(2 * pl) * a.WK + c) * NT + t];
+                su += part[(static_cast<size_t>(2 * pl + 1) * a.WK + c) * NT + t];
+            }
+            const int64_t j = row0 / 2 + pl;
+            a.y[static_cast<int64_t>(t) * a.Nout + j] = epilogue_value(silu_mul_value(sg * rescale, su * rescale),
+                                                                       ops, a.res, static_cast<int64_t>(t) * a.Nout + j);
+        }
+    } else {
+        for (int o = threadIdx.x; o < rows * NT; o += blockDim.x) {
+            const int rl = o / NT;
+            const int t = o - rl * NT;
+            float sum = 0.f;
+            for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
+            const int64_t idx = static_cast<int64_t>(t) * a.Nout + row0 + rl;
+            a.y[idx] = epilogue_value(__half_as_ushort(__float2half_rn(sum * rescale)), ops, a.res, idx);
+        }
     }
     if (a.trace_seq) {
         __syncthreads();
@@ -329,7 +421,7 @@ static int gs_zpf() {
     return v;
 }
 
-static GsConfig gs_config(int64_t K, int64_t N) {
+static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
     GsConfig c{};
     const int G = static_cast<int>(K / kGroup);
     c.WK = (G + 31) / 32;
@@ -356,7 +448,8 @@ static GsConfig gs_config(int64_t K, int64_t N) {
     int mult = 1;
     if (const char* e = std::getenv("RELAX_Q4_GS_GRID_MULT")) { const int v = std::atoi(e); if (v >= 1 && v <= 4) mult = v; }
     c.grid = static_cast<int>(N < kNumSMs * mult ? N : kNumSMs * mult);
-    c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
+    const int64_t units = N / pair;                       // rows, or (gate, up) pairs
+    c.rows_cta_max = static_cast<int>((units + c.grid - 1) / c.grid) * pair;
     c.smem = 256 + static_cast<size_t>(c.NS) * stage + 1024 +
              static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
     // At most two GEMV CTAs per SM (the running kernel and the next one under
@@ -366,13 +459,13 @@ static GsConfig gs_config(int64_t K, int64_t N) {
 }
 
 bool gemv_stream_ok(int nt, int64_t K) {
-    if (nt < 1 || nt > 2 || K % 256 != 0) return false;
+    if (nt < 1 || nt > 2 || K % 256 != 0) return false;   // (and N < 2^24: launch_gemv_stream)
     const GsConfig c = gs_config(K, kNumSMs);
     return c.threads <= 1024 && c.smem <= 200 * 1024;
 }
 
-template <int NT, int RPW, int ZPF, int FULLG>
-static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
+template <int NT, int RPW, int ZPF, int FULLG, int MAXT, int FU>
+static int launch_gs_k(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c.grid);
     cfg.blockDim = dim3(c.threads);
@@ -383,17 +476,7 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (c.threads <= 544) {
-        auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 544>;
-        static bool set = false;
-        if (!set) {
-            cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(k), 210 * 1024);
-            if (e != cudaSuccess) return static_cast<int>(e);
-            set = true;
-        }
-        return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
-    }
-    auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, 1024>;   // K > 16K: one CTA per SM
+    auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, MAXT, FU>;
     static bool set = false;
     if (!set) {
         cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(k), 210 * 1024);
@@ -401,6 +484,17 @@ static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
         set = true;
     }
     return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
+}
+
+template <int NT, int RPW, int ZPF, int FULLG>
+static int launch_gs_t(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_t stream) {
+    const bool fu = a.ops != 0;
+    if (c.threads <= 544)
+        return fu ? launch_gs_k<NT, RPW, ZPF, FULLG, 544, 1>(a, c, pdl, stream)
+                  : launch_gs_k<NT, RPW, ZPF, FULLG, 544, 0>(a, c, pdl, stream);
+    // K > 16K: one CTA per SM
+    return fu ? launch_gs_k<NT, RPW, ZPF, FULLG, 1024, 1>(a, c, pdl, stream)
+              : launch_gs_k<NT, RPW, ZPF, FULLG, 1024, 0>(a, c, pdl, stream);
 }
 
 template <int NT, int ZPF, int FULLG>
@@ -420,8 +514,10 @@ static int launch_gs_z(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
 }
 
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
-    const GsConfig c = gs_config(K, N);
+                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream, const Fusion& fu) {
+    const int64_t Nout = (fu.ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
+    if (N >= (int64_t{1} << 24)) return static_cast<int>(cudaErrorInvalidValue);   // 32-bit row partition
+    const GsConfig c = gs_config(K, N, (fu.ops & RELAX_OP_SILU_MUL) ? 2 : 1);
     if (std::getenv("RELAX_Q4_GS_PRINT"))
         fprintf(stderr, "gemv_stream K=%lld N=%lld WK=%d H=%d RPW=%d RS=%d NS=%d threads=%d grid=%d smem=%zu\n",
                 (long long)K, (long long)N, c.WK, c.H, c.RPW, c.RS, c.NS, c.threads, c.grid, c.smem);
@@ -432,11 +528,16 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.x = x + t0 * K;
         a.w = reinterpret_cast<const uint8_t*>(w);
         a.s = reinterpret_cast<const uint8_t*>(s);
-        a.y = y + t0 * N;
+        a.y = y + t0 * Nout;
         a.N = N;
         a.K = static_cast<int>(K);
         a.G = static_cast<int>(K / kGroup);
         a.WK = c.WK; a.H = c.H; a.RS = c.RS; a.NS = c.NS;
+        a.ops = fu.ops;
+        a.eps = fu.eps;
+        a.gamma = fu.gamma;
+        a.res = fu.res ? fu.res + t0 * Nout : nullptr;
+        a.Nout = Nout;
         a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
         a.rows_cta_max = c.rows_cta_max;
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;

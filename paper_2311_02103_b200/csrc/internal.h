@@ -31,6 +31,14 @@ inline cudaError_t set_kernel_smem(const void* fn, int dyn_bytes) {
                                 static_cast<int>(cudaSharedmemCarveoutMaxShared));
 }
 
+// Fused neighbours of one call (include/relax_q4.h RELAX_OP_*); ops == 0: none.
+struct Fusion {
+    uint32_t ops = 0;
+    float eps = 0.f;
+    const uint16_t* gamma = nullptr;   // RMSNORM_X, fp16 [K]
+    const uint16_t* res = nullptr;     // RESIDUAL, fp16 [n][N_out]
+};
+
 enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2 };
 
 struct Plan {
@@ -57,8 +65,13 @@ int launch_dequant(const uint32_t* w, const uint16_t* s, int64_t K, int64_t N,
 int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                 const uint16_t* s, uint16_t* y, int nt, bool pdl, cudaStream_t stream);
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
+                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream,
+                       const Fusion& fu = Fusion());
 bool gemv_stream_ok(int nt, int64_t K);
+// RMSNorm of fp16 rows into `out` (the TC path's RMSNORM_X prologue; the
+// decode GEMV normalises in registers instead).
+int launch_rmsnorm(const uint16_t* x, int64_t n, int64_t K, const uint16_t* gamma, float eps,
+                   uint16_t* out, bool pdl, cudaStream_t stream);
 int launch_gemv_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                     const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 bool gemv_mma_ok(int nt, int64_t K, int64_t N);
@@ -70,6 +83,7 @@ int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const ui
 bool gemv_row_ok(int64_t K);
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
               const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
-              cudaStream_t stream);
+              cudaStream_t stream,
+              const Fusion& fu = Fusion());
 
 }  // namespace rq4

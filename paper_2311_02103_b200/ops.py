@@ -36,7 +36,17 @@ FLAG_SPLIT_WORKSPACE = 2
 
 # every symbol include/relax_q4.h declares
 EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",
-           "relax_query_schedule", "relax_q4_dequant", "relax_status_str", "relax_version")
+           "relax_query_schedule", "relax_q4_dequant", "relax_status_str", "relax_version",
+           "relax_plan_workspace_fused", "relax_q4_matmul_fused")
+
+# fused neighbours (include/relax_q4.h RELAX_OP_*)
+OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL = 1, 2, 4
+
+
+class Fusion(ctypes.Structure):
+    """struct relax_q4_fusion."""
+    _fields_ = [("ops", ctypes.c_uint32), ("rms_eps", ctypes.c_float),
+                ("rms_weight", ctypes.c_void_p), ("residual", ctypes.c_void_p)]
 
 
 class RelaxError(RuntimeError):
@@ -79,6 +89,10 @@ def lib() -> ctypes.CDLL:
         L.relax_status_str.restype = ctypes.c_char_p
         L.relax_version.argtypes = []
         L.relax_version.restype = ctypes.c_char_p
+        L.relax_plan_workspace_fused.argtypes = [I64, I64, I64, ctypes.c_uint32, ctypes.POINTER(SZ)]
+        L.relax_plan_workspace_fused.restype = I
+        L.relax_q4_matmul_fused.argtypes = [P, I64, I64, I64, P, P, P, ctypes.POINTER(Fusion), P, SZ, P]
+        L.relax_q4_matmul_fused.restype = I
         _lib = L
         return L
 
@@ -172,6 +186,41 @@ def q4_dequant(packed_w, scales, K: int, w_out=None, stream=None):
     rc = lib().relax_q4_dequant(_ptr(packed_w), _ptr(scales), K, N, _ptr(w_out), _stream_ptr(stream))
     _check(rc, "relax_q4_dequant")
     return w_out
+
+
+def plan_workspace_fused(n_max: int, K: int, N: int, ops: int) -> int:
+    out = ctypes.c_size_t(0)
+    _check(lib().relax_plan_workspace_fused(n_max, K, N, ops, ctypes.byref(out)), "relax_plan_workspace_fused")
+    return int(out.value)
+
+
+def q4_matmul_fused(x, packed_w, scales, y=None, rms_weight=None, rms_eps: float = 1e-5, silu_mul: bool = False,
+                    residual=None, ws=None, stream=None):
+    """relax_q4_matmul_fused: optional RMSNorm prologue on x (rms_weight = gamma [K]),
+    SiLU-mul epilogue over interleaved (gate, up) rows (y has N/2 columns) and a
+    residual add; see include/relax_q4.h for the exact fp16 semantics."""
+    import torch
+    n, K, N = _shapes(x, packed_w, scales)
+    ops = (OP_RMSNORM_X if rms_weight is not None else 0) | (OP_SILU_MUL if silu_mul else 0) | \
+          (OP_RESIDUAL if residual is not None else 0)
+    n_out = N // 2 if silu_mul else N
+    if y is None:
+        y = torch.empty((n, n_out), dtype=torch.float16, device=x.device)
+    fz = Fusion(ops, float(rms_eps), _ptr(rms_weight) or None, _ptr(residual) or None)
+    nb = 0 if ws is None else ws.numel() * ws.element_size()
+    rc = lib().relax_q4_matmul_fused(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y), ctypes.byref(fz),
+                                     _ptr(ws), nb, _stream_ptr(stream))
+    _check(rc, "relax_q4_matmul_fused")
+    return y
+
+
+def interleave_rows(a, b):
+    """Weight prep for the SiLU-mul epilogue (a one-time repack): rows of a
+    (gate) and b (up) alternated, out[2j] = a[j], out[2j+1] = b[j]."""
+    import torch
+    if a.shape != b.shape:
+        raise ValueError("gate and up must have the same shape")
+    return torch.stack((a, b), dim=1).reshape((2 * a.shape[0],) + tuple(a.shape[1:])).contiguous()
 
 
 def version() -> str:

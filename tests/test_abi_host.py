@@ -27,7 +27,7 @@ def header_symbols():
 
 def test_exports_every_declared_symbol(L):
     syms = header_symbols()
-    assert len(syms) == 8
+    assert len(syms) == 10
     assert sorted(ops.EXPORTS) == syms
     for s in syms:
         assert hasattr(L, s), s
@@ -139,3 +139,45 @@ def test_dispatch_shape_specialisation():
     for n in (17, 100, 1000):
         s = ops.query_schedule(n, 4096, 11008)
         assert s["variant"] == "tc" and s["tile"] >= min(n, 16)
+
+
+# ------------------------------------------------------------- fused neighbours
+def fcall(L, ops_=0, eps=1e-5, gamma=A + 32 * MB, res=0, x=A, n=1, K=256, N=256, w=A + 8 * MB,
+          s=A + 16 * MB, y=A + 24 * MB, ws=0, wsb=0):
+    fz = ops.Fusion(ops_, eps, gamma or None, res or None)
+    return L.relax_q4_matmul_fused(x, n, K, N, w, s, y, ctypes.byref(fz), ws, wsb, None)
+
+
+def test_fused_validation_codes(L):
+    R, S, Q = ops.OP_RMSNORM_X, ops.OP_SILU_MUL, ops.OP_RESIDUAL
+    assert fcall(L, ops_=8) == 1                                  # unknown op bit
+    assert fcall(L, ops_=R, K=96) == 2                            # fused ops need K % 256 == 0
+    assert fcall(L, ops_=S, N=255) == 2                           # SiLU-mul pairs need N even
+    assert fcall(L, ops_=R, gamma=0) == 1                         # RMSNorm without gamma
+    assert fcall(L, ops_=R, eps=-1.0) == 1
+    assert fcall(L, ops_=R, eps=float("nan")) == 1
+    assert fcall(L, ops_=Q, res=0) == 1                           # residual without pointer
+    assert fcall(L, ops_=R, gamma=A + 32 * MB + 8) == 3           # misaligned gamma
+    assert fcall(L, ops_=Q, res=A + 24 * MB + 16) == 4            # residual partially overlapping y
+    assert fcall(L, ops_=R, gamma=A + 24 * MB) == 4               # y overlapping gamma
+    assert fcall(L, ops_=Q, res=A + 24 * MB) == 6                 # in-place residual (res == y) is legal
+    assert fcall(L, ops_=R | S | Q, res=A + 40 * MB) == 6         # valid: reaches the device check
+    assert fcall(L, ops_=R, n=64) == 5                            # TC path normalises into the workspace
+    assert fcall(L, ops_=R, n=0, x=0, y=0) == 0                   # n == 0: no-op
+    assert fcall(L, ops_=0, K=100) == 2                           # ops == 0: plain matmul validation
+
+
+def test_fused_workspace_plan(L):
+    R = ops.OP_RMSNORM_X
+    assert ops.plan_workspace_fused(2, 4096, 4096, R) == 0        # decode GEMV normalises in registers
+    assert ops.plan_workspace_fused(64, 4096, 4096, 0) == ops.plan_workspace(64, 4096, 4096)
+    assert ops.plan_workspace_fused(64, 4096, 4096, R) >= 64 * 4096 * 2
+    assert ops.plan_workspace_fused(100000, 4096, 4096, R) >= 100000 * 4096 * 2
+    with pytest.raises(ops.RelaxError):
+        ops.plan_workspace_fused(4, 4096, 4095 * 2 + 1, ops.OP_SILU_MUL)
+    # plan soundness: every n <= n_max fits
+    for n_max in (1, 3, 17, 300):
+        nb = ops.plan_workspace_fused(n_max, 4096, 11008, R)
+        for n in range(1, n_max + 1, max(1, n_max // 7)):
+            assert fcall(L, ops_=R, n=n, K=4096, N=11008, w=A + 64 * MB, s=A + 128 * MB, y=A + 256 * MB,
+                         gamma=A + 512 * MB, ws=A + 1024 * MB, wsb=nb) == 6
