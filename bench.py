@@ -158,6 +158,76 @@ class Clocks:
 
 
 # --------------------------------------------------------------------- ours
+def block_step(args, mats, weights, n, dev, stream):
+    """Decoder-block chain over the fused-layout linears:
+    per layer  qkv = W_qkv . RMSNorm(h);  h += W_o . a;  act = SiLU(g) * u with
+    [g; u] = W_gate_up . RMSNorm(h);  h += W_down . act;  then logits =
+    W_head . RMSNorm(h).  Attention itself is out of scope: `a` is a fixed
+    fp16 tensor standing in for its output.  --block fused runs each linear
+    with its neighbours fused (relax_q4_matmul_fused: 4 kernels per layer,
+    gate/up rows interleaved); --block unfused runs the same linears through
+    relax_q4_matmul with the element-wise ops as separate torch kernels (the
+    unfused program)."""
+    import torch
+    from paper_2311_02103_b200 import ops
+    model = args.workload.rsplit("-", 1)[0]
+    hidden = inputs.LLAMA_SETS[model]["mats"][0][1]
+    h0 = torch.from_numpy(inputs.activations(3, n, hidden).view(np.float16)).to(dev)
+    h = h0.clone()
+    attn = torch.from_numpy(inputs.activations(4, n, hidden).view(np.float16)).to(dev)
+    gamma = torch.from_numpy((np.random.default_rng(5).uniform(0.8, 1.2, hidden)).astype(np.float16)).to(dev)
+    eps = 1e-5
+    outs = {}
+    for (name, K, N) in mats:
+        kind = name.split(".")[-1]
+        if kind == "gate_up":
+            outs[name] = torch.empty((n, N // 2 if args.block == "fused" else N), dtype=torch.float16, device=dev)
+        elif kind in ("qkv", "lm_head"):
+            outs[name] = torch.empty((n, N), dtype=torch.float16, device=dev)
+    tmp = torch.empty((n, hidden), dtype=torch.float16, device=dev)
+    wss = {}
+    for (name, K, N) in mats:
+        nb = ops.plan_workspace_fused(n, K, N, ops.OP_RMSNORM_X | (ops.OP_SILU_MUL if "gate_up" in name else 0))
+        wss[name] = torch.zeros(nb, dtype=torch.uint8, device=dev) if nb else None
+
+    def rms(v):
+        vf = v.float()
+        r = torch.rsqrt(vf.pow(2).mean(-1, keepdim=True) + eps)
+        return (vf * r).half() * gamma
+
+    def step():
+        h.copy_(h0)                                      # every step decodes the same token
+        act = None
+        for (name, K, N), (pk, sc) in zip(mats, weights):
+            kind = name.split(".")[-1]
+            if args.block == "fused":
+                if kind in ("qkv", "lm_head"):
+                    ops.q4_matmul_fused(h, pk, sc, y=outs[name], rms_weight=gamma, rms_eps=eps, ws=wss[name],
+                                        stream=stream)
+                elif kind == "o":
+                    ops.q4_matmul_fused(attn, pk, sc, y=h, residual=h, stream=stream)
+                elif kind == "gate_up":
+                    act = outs[name]
+                    ops.q4_matmul_fused(h, pk, sc, y=act, rms_weight=gamma, rms_eps=eps, silu_mul=True,
+                                        ws=wss[name], stream=stream)
+                else:                                    # down
+                    ops.q4_matmul_fused(act, pk, sc, y=h, residual=h, stream=stream)
+            else:
+                if kind in ("qkv", "lm_head"):
+                    ops.q4_matmul(rms(h), pk, sc, y=outs[name], stream=stream)
+                elif kind == "o":
+                    ops.q4_matmul(attn, pk, sc, y=tmp, stream=stream)
+                    h.add_(tmp)
+                elif kind == "gate_up":
+                    gu = outs[name]
+                    ops.q4_matmul(rms(h), pk, sc, y=gu, stream=stream)
+                    act = torch.nn.functional.silu(gu[:, 0::2]) * gu[:, 1::2]
+                else:
+                    ops.q4_matmul(act.contiguous(), pk, sc, y=tmp, stream=stream)
+                    h.add_(tmp)
+    return step, (h0, outs[mats[-1][0]])
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -200,6 +270,10 @@ def run_ours(args, rank, world, local_rank):
     def step():
         for (name, K, N), (pk, sc), y in zip(mats, weights, ys):
             ops.q4_matmul_ex(xs[K], pk, sc, y=y, ws=wss[(K, N)], flags=flags, stream=stream)
+
+    block_io = None
+    if args.block != "none":
+        step, block_io = block_step(args, mats, weights, n, dev, stream)
 
     # capture the step
     torch.cuda.synchronize()
@@ -247,13 +321,13 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- end to end through the public API: pinned host x in, logits out
     x_host = torch.from_numpy(inputs.activations(99, n, mats[0][1]).view(np.float16)).pin_memory()
-    out_host = torch.empty(ys[-1].shape, dtype=torch.float16).pin_memory()
-    x_dev = xs[mats[0][1]]
+    x_dev, y_last = (xs[mats[0][1]], ys[-1]) if block_io is None else block_io
+    out_host = torch.empty(y_last.shape, dtype=torch.float16).pin_memory()
     with torch.cuda.stream(stream):
         for _ in range(2):
             x_dev.copy_(x_host, non_blocking=True)
             replay()
-            out_host.copy_(ys[-1], non_blocking=True)
+            out_host.copy_(y_last, non_blocking=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -262,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(args.steps):
             x_dev.copy_(x_host, non_blocking=True)
             replay()
-            out_host.copy_(ys[-1], non_blocking=True)
+            out_host.copy_(y_last, non_blocking=True)
         e1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
@@ -286,7 +360,8 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / peaks["hbm_gbs"], 4), "peak_src": f"{peaks['src']} hbm copy"}
     label = (args.workload + ("-fused-qkv-gateup" if args.fused else "")
-             + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else ""))
+             + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else "")
+             + (f"-block-{args.block}" if args.block != "none" else ""))
     roof["traffic"] = traffic_per_launch(label, n)
     roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
     roof["kernel"] = "gemv_stream_kernel (streamed GEMV)" if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" \
@@ -402,11 +477,16 @@ def main():
     ap.add_argument("--fused", action="store_true",
                     help="stack q/k/v and gate/up rows into one call each (same weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--block", default="none", choices=["none", "fused", "unfused"],
+                    help="decoder-block chain with RMSNorm / SiLU-mul / residual fused into the linears "
+                         "(fused) or as separate kernels (unfused); implies the fused q/k/v, gate/up layout")
     args = ap.parse_args()
     if args.n is None:
         args.n = 1 if args.workload.endswith("decode") else 512
     if args.warmup < 3:
         args.warmup = 3
+    if args.block != "none":
+        args.fused = True
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

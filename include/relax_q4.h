@@ -160,7 +160,9 @@ RELAX_API int relax_q4_matmul_ex(const void* x, int64_t n, int64_t K, int64_t N,
 typedef struct relax_q4_fusion {
     uint32_t ops;             /* RELAX_OP_* bitmask (0 = plain matmul) */
     float rms_eps;            /* RMSNORM_X: epsilon (>= 0, finite) */
-    const void* rms_weight;   /* RMSNORM_X: device fp16 [K] (gamma), 16-byte aligned */
+    const void* rms_weight;   /* RMSNORM_X: device fp16 [K] (gamma), 16-byte aligned; a model
+                                 parameter: like packed_w/scales it may be read before the
+                                 kernel waits on the previous kernel of the stream (PDL) */
     const void* residual;     /* RESIDUAL: device fp16 [n][N_out], 16-byte aligned; may be
                                  exactly y (in-place add) but not partially overlap it */
 } relax_q4_fusion;

@@ -19,11 +19,16 @@ __device__ __forceinline__ uint16_t silu_mul_value(float sg, float su) {
     return __half_as_ushort(__float2half_rn(sl * u));
 }
 
-// Residual add on the fp16 output value v: fp16(v + res[idx]).
-__device__ __forceinline__ uint16_t epilogue_value(uint16_t v, uint32_t ops, const uint16_t* res, int64_t idx) {
+// Residual add on the fp16 output value v: fp16(v + r) (r = the residual's
+// fp16 bits; ignored without RELAX_OP_RESIDUAL).
+__device__ __forceinline__ uint16_t residual_add(uint16_t v, uint32_t ops, uint16_t r) {
     if (!(ops & RELAX_OP_RESIDUAL)) return v;
-    const float f = __half2float(__ushort_as_half(v)) + __half2float(__ushort_as_half(res[idx]));
+    const float f = __half2float(__ushort_as_half(v)) + __half2float(__ushort_as_half(r));
     return __half_as_ushort(__float2half_rn(f));
+}
+
+__device__ __forceinline__ uint16_t epilogue_value(uint16_t v, uint32_t ops, const uint16_t* res, int64_t idx) {
+    return residual_add(v, ops, (ops & RELAX_OP_RESIDUAL) ? res[idx] : uint16_t(0));
 }
 
 }  // namespace rq4

@@ -187,29 +187,29 @@ __device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const u
 // RMSNorm prologue on the x registers: r_t = 1/sqrt(mean x^2 + eps) over the
 // whole row (per-lane sums -> warp shuffle -> one partial per K-column warp in
 // shared memory -> every consumer sums the WK partials in fixed order), then
-// x <- fp16(fp16(x * r_t) * gamma) in place.  `scratch` is the partial-sum
-// area, free before the stage loop.
+// x <- fp16(fp16(x * r_t) * gamma) in place.  `scratch`: WK * NT floats of
+// static shared memory (not reused, so one barrier suffices).  gamma is a
+// model parameter like the weights and is loaded before griddepcontrol.wait.
 template <int NT>
-__device__ __forceinline__ void rmsnorm_prologue(uint4 (&xr)[NT][4], const GsArgs& a, bool gv, int g, int warp,
+__device__ __forceinline__ void rmsnorm_prologue(uint4 (&xr)[NT][4], const uint4 (&gm)[4], const GsArgs& a,
                                                  int lane, int kw, int h, int nwc, float* scratch) {
-    uint4 gm[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-        gm[q] = gv ? reinterpret_cast<const uint4*>(a.gamma + g * 32)[q] : make_uint4(0u, 0u, 0u, 0u);
     float ss[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-        float acc = 0.f;
+        float pq[4];                                      // four independent chains (latency)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const uint32_t w4[4] = {xr[t][q].x, xr[t][q].y, xr[t][q].z, xr[t][q].w};
+            float acc = 0.f;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const float2 f = __half22float2(u32_as_h2(w4[u]));
                 acc = fmaf(f.x, f.x, acc);
                 acc = fmaf(f.y, f.y, acc);
             }
+            pq[q] = acc;
         }
+        float acc = (pq[0] + pq[1]) + (pq[2] + pq[3]);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         ss[t] = acc;
@@ -236,8 +236,6 @@ __device__ __forceinline__ void rmsnorm_prologue(uint4 (&xr)[NT][4], const GsArg
             xr[t][q] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
     }
-    // everyone has read the partials before the stage loop overwrites them
-    asm volatile("bar.sync 1, %0;" :: "r"(nwc * 32) : "memory");
 }
 
 // FU = 0: the plain matmul (the fused-neighbour code is compiled out, so the
@@ -270,6 +268,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
 
     const uint64_t t_start = a.trace_seq ? gtime() : 0;
     __shared__ uint64_t tr_wait, tr_first;
+    __shared__ float rms_red[(FU ? 32 : 1) * NT];        // RMSNorm partials (WK <= 32)
+    uint16_t res_pre = 0;                                 // RESIDUAL: prefetched first value
     if (threadIdx.x == 0) {
         for (int i = 0; i < a.NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], a.WK); }
         fence_mbar_init();
@@ -303,6 +303,12 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         const int kw = warp - h * a.WK;
         const int g = kw * 32 + lane;
         const bool gv = g < a.G;
+        uint4 gm[4];                                      // RMSNorm gamma of this lane's group
+        if (ops & RELAX_OP_RMSNORM_X) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                gm[q] = gv ? reinterpret_cast<const uint4*>(a.gamma + g * 32)[q] : make_uint4(0u, 0u, 0u, 0u);
+        }
         pdl_wait();
         if (a.trace_seq && warp == 0 && lane == 0) tr_wait = gtime();
         uint4 xr[NT][4];
@@ -313,20 +319,34 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
             for (int q = 0; q < 4; ++q)
                 xr[t][q] = gv ? reinterpret_cast<const uint4*>(a.x + static_cast<int64_t>(t) * a.K + g * 32)[q]
                               : make_uint4(0u, 0u, 0u, 0u);
-        if (ops & RELAX_OP_RMSNORM_X) rmsnorm_prologue<NT>(xr, a, gv, g, warp, lane, kw, h, nwc, part);
+        if (ops & RELAX_OP_RMSNORM_X) rmsnorm_prologue<NT>(xr, gm, a, lane, kw, h, nwc, rms_red);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            float sx = 0.f;           // sum of the group's x (factored zero point)
+            float pq[4];              // sum of the group's x (factored zero point), 4 chains
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t w4[4] = {xr[t][q].x, xr[t][q].y, xr[t][q].z, xr[t][q].w};
+                float a2 = 0.f;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const float2 f = __half22float2(u32_as_h2(w4[u]));
-                    sx += f.x + f.y;
+                    a2 += f.x + f.y;
                 }
+                pq[q] = a2;
             }
+            const float sx = (pq[0] + pq[1]) + (pq[2] + pq[3]);
             m7x[t] = ZPF ? -7.0f * 5.9604644775390625e-08f * sx : 0.f;   // -7 * 2^-24 * sum x
+        }
+        if (ops & RELAX_OP_RESIDUAL) {
+            // prefetch this thread's first residual value of the final loop (its
+            // latency would otherwise sit on the kernel's tail)
+            const int units_cta = (ops & RELAX_OP_SILU_MUL) ? rows / 2 : rows;
+            if (static_cast<int>(threadIdx.x) < units_cta * NT) {
+                const int o = threadIdx.x;
+                const int ul = o / NT, t = o - ul * NT;
+                const int64_t col = (ops & RELAX_OP_SILU_MUL) ? row0 / 2 + ul : row0 + ul;
+                res_pre = a.res[static_cast<int64_t>(t) * a.Nout + col];
+            }
         }
         if (a.trace_seq && warp == 0 && lane == 0) tr_first = gtime();   // x in registers
         const int rsel = reduce_row_of_lane<RPW>(lane);
@@ -379,9 +399,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
                 sg += part[(static_cast<size_t>(2 * pl) * a.WK + c) * NT + t];
                 su += part[(static_cast<size_t>(2 * pl + 1) * a.WK + c) * NT + t];
             }
-            const int64_t j = row0 / 2 + pl;
-            a.y[static_cast<int64_t>(t) * a.Nout + j] = epilogue_value(silu_mul_value(sg * rescale, su * rescale),
-                                                                       ops, a.res, static_cast<int64_t>(t) * a.Nout + j);
+            const int64_t idx = static_cast<int64_t>(t) * a.Nout + row0 / 2 + pl;
+            const bool pre = o == static_cast<int>(threadIdx.x) && warp < nwc;
+            a.y[idx] = residual_add(silu_mul_value(sg * rescale, su * rescale), ops,
+                                    (ops & RELAX_OP_RESIDUAL) ? (pre ? res_pre : a.res[idx]) : uint16_t(0));
         }
     } else {
         for (int o = threadIdx.x; o < rows * NT; o += blockDim.x) {
@@ -390,7 +411,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
             float sum = 0.f;
             for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
             const int64_t idx = static_cast<int64_t>(t) * a.Nout + row0 + rl;
-            a.y[idx] = epilogue_value(__half_as_ushort(__float2half_rn(sum * rescale)), ops, a.res, idx);
+            const bool pre = o == static_cast<int>(threadIdx.x) && warp < nwc;
+            a.y[idx] = residual_add(__half_as_ushort(__float2half_rn(sum * rescale)), ops,
+                                    (ops & RELAX_OP_RESIDUAL) ? (pre ? res_pre : a.res[idx]) : uint16_t(0));
         }
     }
     if (a.trace_seq) {
