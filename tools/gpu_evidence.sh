@@ -15,6 +15,10 @@ b 7b_decode
 b 7b_decode_fused --fused --no-cpu-baseline
 b 13b_decode --workload llama2-13b-decode --no-cpu-baseline
 b 13b_decode_fused --workload llama2-13b-decode --fused --no-cpu-baseline
+b 7b_block_fused --block fused --no-cpu-baseline
+b 7b_block_unfused --block unfused --no-cpu-baseline
+b 13b_block_fused --workload llama2-13b-decode --block fused --no-cpu-baseline
+b 13b_block_unfused --workload llama2-13b-decode --block unfused --no-cpu-baseline
 b 70b_decode --workload llama2-70b-decode --no-cpu-baseline
 b 70b_decode_fused --workload llama2-70b-decode --fused --no-cpu-baseline
 b 7b_prefill_n512 --workload llama2-7b-prefill --n 512 --no-cpu-baseline
