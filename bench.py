@@ -236,7 +236,10 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     ops.lib()
-    model, mats = layer_set(args.workload, args.fused, args.tp_shard)
+    tp_world = world if args.tp else 1
+    if args.tp and args.tp_shard > 1:
+        raise SystemExit("--tp (real tensor parallelism over the ranks) and --tp-shard are exclusive")
+    model, mats = layer_set(args.workload, args.fused, args.tp_shard if not args.tp else tp_world)
     n = args.n
     t_gen = time.time()
     # One realistic weight per distinct shape (seed 1000*config + index),
@@ -274,6 +277,16 @@ def run_ours(args, rank, world, local_rank):
     block_io = None
     if args.block != "none":
         step, block_io = block_step(args, mats, weights, n, dev, stream)
+    elif args.tp and dist.is_initialized():
+        # Megatron TP over the NCCL group: q/k/v, gate/up and
+        # lm_head column-split (no exchange), o and down row-split followed by
+        # an all_reduce of the partial y (fp16, reading 14).
+        def step():
+            for (name, K, N), (pk, sc), y in zip(mats, weights, ys):
+                ops.q4_matmul_ex(xs[K], pk, sc, y=y, ws=wss[(K, N)], flags=flags, stream=stream)
+                if name.split(".")[-1] in ("o", "down"):
+                    with torch.cuda.stream(stream):
+                        dist.all_reduce(y, op=dist.ReduceOp.SUM)
 
     # capture the step
     torch.cuda.synchronize()
@@ -282,9 +295,16 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     graph = None
     if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            step()
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                step()
+        except RuntimeError as e:                # e.g. a collective that cannot be captured
+            if not (args.tp and dist.is_initialized()):
+                raise
+            print(f"graph capture failed ({e}); timing eagerly", file=sys.stderr)
+            torch.cuda.synchronize()
+            graph = None
 
     def replay():
         if graph is not None:
@@ -347,7 +367,8 @@ def run_ours(args, rank, world, local_rank):
 
     bytes_step, flops_step = algorithmic(mats, n)
     ms_step = ms / args.steps
-    tok_s = world * n * args.steps / (ms / 1e3)
+    streams = 1 if args.tp else world            # TP: the ranks decode one stream together
+    tok_s = streams * n * args.steps / (ms / 1e3)
     gbs = bytes_step / (ms_step / 1e3) / 1e9
     tflops = flops_step / (ms_step / 1e3) / 1e12
     peaks = load_peaks()
@@ -377,20 +398,20 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.tp else "weak",
         "vs_baseline": None,
         "dtype": "q4f16 (int4 codes x fp16 -> fp32 accumulate, fp16 out)",
         "data": "synthetic (seeded realistic q4f16 weights, N(0,1) fp16 x)",
         "config": {"workload": label,
                    "model": model, "tokens_per_step": n,
                    "layers_linears": len(mats), "weight_bytes": int(sum(inputs.q4_bytes(K, N) for _, K, N in mats)),
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"tp{world}" if args.tp else f"replicas{world}") if world > 1 else "single",
                    "l2": "not flushed: per-step working set %.2f GB >> 126 MB L2" % (bytes_step / 1e9),
                    "graph": graph is not None, "pdl": not args.no_pdl, "schedule": sched},
         "hbm_gbs": round(gbs, 1),
         "tflops": round(tflops, 3),
         "roofline": roof,
-        "e2e": {"value": round(world * n * args.steps / (ms_e2e / 1e3), 2), "unit": "tok/s",
+        "e2e": {"value": round(streams * n * args.steps / (ms_e2e / 1e3), 2), "unit": "tok/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 2), "d2h_bytes_per_step": int(out_host.numel() * 2)},
         "gpu_launches": launches * args.steps,
         "clocks": ck,
@@ -477,6 +498,10 @@ def main():
     ap.add_argument("--fused", action="store_true",
                     help="stack q/k/v and gate/up rows into one call each (same weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp", action="store_true",
+                    help="with torchrun: real Megatron tensor parallelism of the layer set over the ranks "
+                         "(column/row split, NCCL all_reduce after o and down); value = tokens of the one "
+                         "stream, scaling strong")
     ap.add_argument("--block", default="none", choices=["none", "fused", "unfused"],
                     help="decoder-block chain with RMSNorm / SiLU-mul / residual fused into the linears "
                          "(fused) or as separate kernels (unfused); implies the fused q/k/v, gate/up layout")
@@ -498,7 +523,7 @@ def main():
         print(json.dumps(run_reference(args)))
         return 0
 
-    if world > 1:
+    if world > 1 or (args.tp and "MASTER_ADDR" in os.environ):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
@@ -510,8 +535,8 @@ def main():
             res["cpu_baseline"] = {"value": round(v, 6), "unit": "tok/s", "cores": info["cores"],
                                    "kind": "oracle", "sample": info["sample"]}
         print(json.dumps(res))
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
