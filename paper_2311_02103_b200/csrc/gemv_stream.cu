@@ -253,13 +253,11 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
     float* part = reinterpret_cast<float*>(ring + static_cast<size_t>(a.NS) * a.stage_bytes + 1024);
 
     // rows of this CTA; with SILU_MUL whole (gate, up) pairs
-    // (32-bit arithmetic: N < 2^24 is checked on the host; a 64-bit division
-    // here would delay the producer's first copy on every launch)
     const uint32_t ops = FU ? a.ops : 0u;
-    const uint32_t pair = (ops & RELAX_OP_SILU_MUL) ? 2u : 1u;
-    const uint32_t units = static_cast<uint32_t>(a.N) / pair;
-    const int64_t row0 = static_cast<int64_t>(blockIdx.x * units / gridDim.x * pair);
-    const int64_t row1 = static_cast<int64_t>((blockIdx.x + 1) * units / gridDim.x * pair);
+    const int psh = (ops & RELAX_OP_SILU_MUL) ? 1 : 0;       // log2 of the row unit
+    const int64_t units = a.N >> psh;
+    const int64_t row0 = (static_cast<int64_t>(blockIdx.x) * units / gridDim.x) << psh;
+    const int64_t row1 = (static_cast<int64_t>(blockIdx.x + 1) * units / gridDim.x) << psh;
     const int rows = static_cast<int>(row1 - row0);
     const int nst = (rows + a.RS - 1) / a.RS;
     const uint32_t cb_row = static_cast<uint32_t>(a.K / 2);
@@ -454,12 +452,25 @@ static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
     c.RPW = 4;
     if (const char* e = std::getenv("RELAX_Q4_GS_H")) { const int v = std::atoi(e); if (v >= 1 && v * c.WK <= 31) c.H = v; }
     if (const char* e = std::getenv("RELAX_Q4_GS_RPW")) { const int v = std::atoi(e); if (v == 1 || v == 2 || v == 4 || v == 8) c.RPW = v; }
+    int mult = 1;
+    if (const char* e = std::getenv("RELAX_Q4_GS_GRID_MULT")) { const int v = std::atoi(e); if (v >= 1 && v <= 4) mult = v; }
+    c.grid = static_cast<int>(N < kNumSMs * mult ? N : kNumSMs * mult);
+    const int64_t units = N / pair;                       // rows, or (gate, up) pairs
+    c.rows_cta_max = static_cast<int>((units + c.grid - 1) / c.grid) * pair;
+    const size_t part_bytes = static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
+    // Ring budget: the configured one, trimmed so that the whole CTA stays
+    // <= 113 KB -- two GEMV CTAs (this kernel and the next one under PDL)
+    // must fit an SM's 228 KB with 1 KB reserved each (matters for the wide
+    // lm_head, whose partial sums are large).
+    size_t budget = gs_ring_budget();
+    const size_t cap = 113 * 1024 - 256 - 1024;
+    if (part_bytes < cap && cap - part_bytes < budget) budget = cap - part_bytes;
     // at least max(H, 3) stages of RPW rows must fit the ring
     const int nsmin = c.H < 3 ? 3 : c.H;
-    while (c.RPW > 1 && static_cast<size_t>(nsmin) * c.RPW * row_bytes > gs_ring_budget()) c.RPW /= 2;
+    while (c.RPW > 1 && static_cast<size_t>(nsmin) * c.RPW * row_bytes > budget) c.RPW /= 2;
     c.RS = c.RPW;
     const size_t stage = static_cast<size_t>(c.RS) * row_bytes;
-    int ns = static_cast<int>(gs_ring_budget() / stage);
+    int ns = static_cast<int>(budget / stage);
     if (ns < nsmin) c.H = ns < 1 ? 1 : ns;          // (only for huge K with RPW = 1)
     c.NS = ns < 2 ? 2 : ns > 16 ? 16 : ns;
     if (c.NS < c.H) c.H = c.NS;
@@ -468,13 +479,7 @@ static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
     // (the classic one-consumer ring protocol per group).
     c.NS -= c.NS % c.H;
     c.threads = (c.WK * c.H + 1) * 32;
-    int mult = 1;
-    if (const char* e = std::getenv("RELAX_Q4_GS_GRID_MULT")) { const int v = std::atoi(e); if (v >= 1 && v <= 4) mult = v; }
-    c.grid = static_cast<int>(N < kNumSMs * mult ? N : kNumSMs * mult);
-    const int64_t units = N / pair;                       // rows, or (gate, up) pairs
-    c.rows_cta_max = static_cast<int>((units + c.grid - 1) / c.grid) * pair;
-    c.smem = 256 + static_cast<size_t>(c.NS) * stage + 1024 +
-             static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
+    c.smem = 256 + static_cast<size_t>(c.NS) * stage + 1024 + part_bytes;
     // At most two GEMV CTAs per SM (the running kernel and the next one under
     // PDL): a third co-resident kernel was observed to stall the chain.
     if (c.smem < 80 * 1024) c.smem = 80 * 1024;
