@@ -41,9 +41,10 @@
 
 namespace rq4 {
 
-constexpr int kTcTransformWarps = 8;   // 4 TMEM lane quarters x 2 sub-block parities (x 2 k-halves if 16)
-constexpr int kTcKHPerWarp = 16 / kTcTransformWarps;   // 32-k halves of a sub-block per warp
-constexpr int kTcThreads = (4 + kTcTransformWarps) * 32;   // 20 warps, see the role map above
+// Transform warps: 4 TMEM lane quarters x 2 sub-block parities (x 2 k-halves
+// with 16).  8 for every tile: 16 for BN >= 128 (one CTA per SM) was measured
+// 20-40% slower at n = 512..4096, so the knob stays at 8.
+template <int BN> constexpr int tc_transform_warps() { return 8; }
 constexpr int kWStages = 4;            // 256-k codes+scales stages in flight
 constexpr uint32_t kCodesStageBytes = kTcBM * (kTcWStageK / 2);     // 16 KB
 constexpr uint32_t kScalesStageBytes = kTcBM * (kTcWStageK / kGroup) * 2;  // 2 KB
@@ -106,6 +107,9 @@ struct TcCfg {
     // SW128 B layout, k permuted to match dequant_word_interleaved (no byte
     // permutes in the transform).  BN >= 128: x by TMA, natural k order.
     static constexpr bool kPermX = BN <= 64;
+    static constexpr int kTW = tc_transform_warps<BN>();            // transform warps
+    static constexpr int kKH = 16 / kTW;                             // 32-k halves per warp and sub-block
+    static constexpr int kThreads = (4 + kTW) * 32;
     static constexpr int kCtasPerSm = BN <= 64 ? 2 : 1;
     static constexpr uint32_t kTmemCols = BN <= 64 ? 256 : 512;
     static constexpr uint32_t kA0 = (BN < 32 ? 32 : BN);                 // TMEM col of A ring
@@ -124,7 +128,7 @@ struct TcCfg {
 };
 
 template <int BN>
-__global__ void __launch_bounds__(kTcThreads, TcCfg<BN>::kCtasPerSm)
+__global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kCtasPerSm)
 tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
              const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TcArgs a) {
     using Cfg = TcCfg<BN>;
@@ -165,8 +169,8 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     pdl_launch_dependents();
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], kTcTransformWarps); }
-        for (int i = 0; i < AS; ++i) { mbar_init(&a_full[i], kTcTransformWarps / 2); mbar_init(&a_empty[i], 1); }
+        for (int i = 0; i < kWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], Cfg::kTW); }
+        for (int i = 0; i < AS; ++i) { mbar_init(&a_full[i], Cfg::kTW / 2); mbar_init(&a_empty[i], 1); }
         for (int i = 0; i < XS; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); mbar_init(&x_perm[i], 1); }
         mbar_init(acc_full, 1);
         fence_mbar_init();
@@ -272,7 +276,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         const int tw = warp - 4;
         const int q = tw & 3;                 // TMEM lanes 32q..32q+31 = rows
         const int h = (tw >> 2) & 1;          // sub-block parity
-        const int kh0 = (tw >> 3) * kTcKHPerWarp;   // first k-half (32 k = 4 words) of the sub-block
+        const int kh0 = (tw >> 3) * Cfg::kKH;   // first k-half (32 k = 4 words) of the sub-block
         const int m = q * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int ws = 0, as = h;                 // this warp's sub-blocks: j = h, h+2, h+4, ...
@@ -284,9 +288,9 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 const int sub = h + 2 * u;
-                uint32_t v[kTcKHPerWarp][4][4];
+                uint32_t v[Cfg::kKH][4][4];
 #pragma unroll
-                for (int e = 0; e < kTcKHPerWarp; ++e) {
+                for (int e = 0; e < Cfg::kKH; ++e) {
                     const int kh = kh0 + e;
                     const int chunk = 2 * sub + kh;     // 16-B chunk = 32 codes = one group
                     const uint4 c = *reinterpret_cast<const uint4*>(crow + ((chunk ^ (m & 7)) << 4));
@@ -303,7 +307,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                 if (a.trace) mbar_wait_t<true>(&a_empty[as], aph ^ 1, wacc2); else mbar_wait(&a_empty[as], aph ^ 1);
                 tc_fence_after();
 #pragma unroll
-                for (int e = 0; e < kTcKHPerWarp; ++e) {
+                for (int e = 0; e < Cfg::kKH; ++e) {
                     const uint32_t acol = tmem_base + lane_base + Cfg::kA0 + as * 32 + (kh0 + e) * 16;
 #pragma unroll
                     for (int w = 0; w < 4; ++w)
@@ -428,7 +432,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         // SiLU-mul epilogue stays within one CTA and one lane pair
         const uint32_t e0 = r * (E / 2) / S * 2, e1 = (r + 1) * (E / 2) / S * 2;
         const uint32_t red_addr = smem_u32(red);
-        for (uint32_t e = e0 + threadIdx.x; e < e1; e += kTcThreads) {
+        for (uint32_t e = e0 + threadIdx.x; e < e1; e += Cfg::kThreads) {
             float sum = 0.f;
             for (uint32_t s = 0; s < S; ++s) sum += ld_dsmem_f32(mapa_shared(red_addr + e * 4u, s));
             const int64_t tok = n0 + static_cast<int64_t>(e / kTcBM);
@@ -524,7 +528,7 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>((a.N + kTcBM - 1) / kTcBM),
                        static_cast<unsigned>((a.n + BN - 1) / BN), static_cast<unsigned>(a.split));
-    cfg.blockDim = dim3(kTcThreads);
+    cfg.blockDim = dim3(Cfg::kThreads);
     cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
