@@ -87,8 +87,13 @@ struct TcArgs {
 // fused epilogue.  SILU_MUL pairs rows (2j, 2j+1), which sit in adjacent
 // lanes of the calling warp: every lane of `mask` must call this (the pair
 // exchange is a shuffle), and only the even row of a valid pair stores.
+template <int FU>
 __device__ __forceinline__ void tc_store(const TcArgs& a, unsigned mask, int64_t tok, int64_t row, float f,
                                          bool valid) {
+    if (!FU) {                          // plain matmul: the unfused store, nothing else compiled
+        if (valid) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(f));
+        return;
+    }
     if (a.ops & RELAX_OP_SILU_MUL) {
         const float fp = __shfl_xor_sync(mask, f, 1);
         if (valid && (row & 1) == 0) {
@@ -127,7 +132,9 @@ struct TcCfg {
     static_assert(128u * BN * 4u <= kOffBar, "cluster reduction buffer must fit in the rings");
 };
 
-template <int BN>
+// FU = 0: plain matmul (fused-epilogue code compiled out, so the kernel is the
+// unfused one register for register); FU = 1: a.ops (SILU_MUL / RESIDUAL).
+template <int BN, int FU>
 __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kCtasPerSm)
 tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
              const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TcArgs a) {
@@ -364,7 +371,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                     if (split) {
                         if (row_ok && tok < a.n) a.part[(static_cast<int64_t>(z) * a.n + tok) * a.N + row] = f;
                     } else {
-                        tc_store(a, 0xffffffffu, tok, row, f, row_ok && tok < a.n);
+                        tc_store<FU>(a, 0xffffffffu, tok, row, f, row_ok && tok < a.n);
                     }
                 }
             }
@@ -397,7 +404,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
 #pragma unroll
                         for (int u = 0; u < 8; ++u) {
                             const int64_t tok = n0 + c0 + u;
-                            tc_store(a, 0xffffffffu, tok, row, sum[u], row_ok && tok < a.n);
+                            tc_store<FU>(a, 0xffffffffu, tok, row, sum[u], row_ok && tok < a.n);
                         }
                     }
                 }
@@ -437,7 +444,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             for (uint32_t s = 0; s < S; ++s) sum += ld_dsmem_f32(mapa_shared(red_addr + e * 4u, s));
             const int64_t tok = n0 + static_cast<int64_t>(e / kTcBM);
             const int64_t rr = m0 + static_cast<int64_t>(e % kTcBM);
-            tc_store(a, __activemask(), tok, rr, sum, tok < a.n && rr < a.N);
+            tc_store<FU>(a, __activemask(), tok, rr, sum, tok < a.n && rr < a.N);
         }
         cluster_arrive_release();
         cluster_wait_acquire();
@@ -508,8 +515,8 @@ static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base,
     return make_tensor_map(m, dt, 2, base, dims, strides, box, sw);
 }
 
-template <int BN>
-static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint16_t* x,
+template <int BN, int FU>
+static int launch_tc_k(const CUtensorMap& mw, const CUtensorMap& ms, const uint16_t* x,
                         const TcArgs& a, bool pdl, cudaStream_t stream) {
     using Cfg = TcCfg<BN>;
     CUtensorMap mx;
@@ -518,10 +525,10 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
     if (rc) return rc;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(tc_q4_kernel<BN>),
+        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(tc_q4_kernel<BN, FU>),
                                         static_cast<int>(Cfg::kSmemBytes));
         if (e != cudaSuccess) return static_cast<int>(e);
-        e = cudaFuncSetAttribute(tc_q4_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(tc_q4_kernel<BN, FU>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return static_cast<int>(e);
         attr_set = true;
     }
@@ -543,7 +550,13 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
         attr[1].val.clusterDim.z = static_cast<unsigned>(a.split);
         cfg.numAttrs = 2;
     }
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN>, mw, ms, mx, a));
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN, FU>, mw, ms, mx, a));
+}
+
+template <int BN>
+static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint16_t* x,
+                        const TcArgs& a, bool pdl, cudaStream_t stream) {
+    return a.ops ? launch_tc_k<BN, 1>(mw, ms, x, a, pdl, stream) : launch_tc_k<BN, 0>(mw, ms, x, a, pdl, stream);
 }
 
 // Workspace layout (fixed ticket region first, so one buffer serves every n):

@@ -7,4 +7,4 @@ for i in 1 2; do
   (cd old_build && timeout 100 python bench.py --no-cpu-baseline $BENCH_ARGS > ../gpurun_out/b_old.json 2>/dev/null); echo "old: $(val gpurun_out/b_old.json)"
 done
 for sh in "4096 4096" "4096 11008" "11008 4096" "4096 32000"; do python tools/l2_rate.py $sh; done
-(cd old_build && for sh in "4096 4096" "4096 11008" "11008 4096" "4096 32000"; do python ../tools/l2_rate.py $sh; done)
+(cd old_build && for sh in "4096 4096" "4096 11008" "11008 4096" "4096 32000"; do python tools/l2_rate.py $sh; done)
