@@ -40,7 +40,7 @@ static int choose_bn(int64_t n, int64_t N) {
 // factor s <= 8 together, minimising a wave-quantised time model fitted to
 // the measured sweeps (profiles/sweep_c3_*.jsonl):
 //   waves = ceil(tiles * s / 148)           (one CTA per SM at BN >= 128)
-//   t(us) = waves * (ceil(kt / s) * step + fixed) + [s > 1] * 3
+//   t(us) = waves * (ceil(kt / s) * step + fixed) + [s > 1] * 1  (DSMEM reduce)
 //   step  = 0.92 / 1.3 us per 256-k stage, fixed = 5.7 / 8.0 us at BN = 128 / 256.
 // Split-K only within one wave: a multi-wave grid of split-K clusters was
 // measured far slower than the model (cluster placement), so s > 1 requires
@@ -58,7 +58,7 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
             if (s > 1 && (tiles > kMaxSplitTiles || tiles * s > kNumSMs)) break;
             const int64_t waves = (tiles * s + kNumSMs - 1) / kNumSMs;
             const int ks = (kt + s - 1) / s;
-            const double t = static_cast<double>(waves) * (ks * step + fixed) + (s > 1 ? 3.0 : 0.0);
+            const double t = static_cast<double>(waves) * (ks * step + fixed) + (s > 1 ? 1.0 : 0.0);
             if (t < best * 0.999) { best = t; bb = bn; bs = s; }
         }
     }

@@ -106,6 +106,35 @@ __device__ __forceinline__ void tc_store(const TcArgs& a, unsigned mask, int64_t
     }
 }
 
+// Four consecutive rows rr..rr+3 of token tok (rr % 4 == 0): the cluster
+// reduction's vector path.  SiLU-mul pairs (rr, rr+1), (rr+2, rr+3) are
+// inside the thread; rows past N are skipped (N is even with SILU_MUL).
+template <int FU>
+__device__ __forceinline__ void tc_store4(const TcArgs& a, int64_t tok, int64_t rr, const float (&f)[4]) {
+    if (tok >= a.n) return;
+    if (FU && (a.ops & RELAX_OP_SILU_MUL)) {
+#pragma unroll
+        for (int j = 0; j < 4; j += 2) {
+            if (rr + j < a.N) {
+                const int64_t idx = tok * a.Nout + (rr + j) / 2;
+                a.y[idx] = epilogue_value(silu_mul_value(f[j], f[j + 1]), a.ops, a.res, idx);
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (rr + j < a.N) {
+            if (FU) {
+                const int64_t idx = tok * a.Nout + rr + j;
+                a.y[idx] = epilogue_value(__half_as_ushort(__float2half_rn(f[j])), a.ops, a.res, idx);
+            } else {
+                a.y[tok * a.N + rr + j] = __half_as_ushort(__float2half_rn(f[j]));
+            }
+        }
+    }
+}
+
 template <int BN>
 struct TcCfg {
     // BN <= 64: x is staged by a whole warp with LDG + PRMT + STS into the
@@ -435,16 +464,19 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         const uint32_t S = static_cast<uint32_t>(a.split);
         const uint32_t r = cluster_ctarank();
         constexpr uint32_t E = kTcBM * BN;
-        // element ranges start on even elements, so a (gate, up) row pair of the
-        // SiLU-mul epilogue stays within one CTA and one lane pair
-        const uint32_t e0 = r * (E / 2) / S * 2, e1 = (r + 1) * (E / 2) / S * 2;
+        // element ranges in units of 4 (16-B DSMEM vector loads, one per rank;
+        // 4 consecutive rows of one token, so a SiLU-mul pair stays in a thread)
+        const uint32_t e0 = r * (E / 4) / S * 4, e1 = (r + 1) * (E / 4) / S * 4;
         const uint32_t red_addr = smem_u32(red);
-        for (uint32_t e = e0 + threadIdx.x; e < e1; e += Cfg::kThreads) {
-            float sum = 0.f;
-            for (uint32_t s = 0; s < S; ++s) sum += ld_dsmem_f32(mapa_shared(red_addr + e * 4u, s));
+        for (uint32_t e = e0 + 4 * threadIdx.x; e < e1; e += 4 * Cfg::kThreads) {
+            float f[4] = {0.f, 0.f, 0.f, 0.f};
+            for (uint32_t s = 0; s < S; ++s) {
+                const float4 v = ld_dsmem_v4f32(mapa_shared(red_addr + e * 4u, s));
+                f[0] += v.x; f[1] += v.y; f[2] += v.z; f[3] += v.w;
+            }
             const int64_t tok = n0 + static_cast<int64_t>(e / kTcBM);
             const int64_t rr = m0 + static_cast<int64_t>(e % kTcBM);
-            tc_store<FU>(a, __activemask(), tok, rr, sum, tok < a.n && rr < a.N);
+            tc_store4<FU>(a, tok, rr, f);
         }
         cluster_arrive_release();
         cluster_wait_acquire();

@@ -267,6 +267,13 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t cluster_addr) {
     return v;
 }
 
+__device__ __forceinline__ float4 ld_dsmem_v4f32(uint32_t cluster_addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(cluster_addr) : "memory");
+    return v;
+}
+
 // ----------------------------------------------------------------- math
 // acc += a * b with a, b binary16 and an fp32 accumulator (one FHFMA; the
 // product of two binary16 values is exact in binary32).
