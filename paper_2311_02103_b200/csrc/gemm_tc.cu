@@ -52,7 +52,8 @@ constexpr int kSubPerStage = kTcWStageK / kTcXStageK;                // 4
 
 // ---- optional per-CTA role timing (RELAX_Q4_TRACE=1): wait cycles per role
 struct TcTrace { uint32_t cta, smid, nsub, pad; uint64_t t0, t_end;
-                 uint64_t w_prod, x_prod, perm, tr_w, tr_a, mma_a, mma_x, epi; };
+                 uint64_t w_prod, x_prod, perm, tr_w, tr_a, mma_a, mma_x, epi;
+                 uint64_t t_mma0, t_acc, t_epi; };   // globaltimer: first MMA issued, accumulator ready, stores done
 constexpr int kTcTraceMax = 1 << 14;
 __device__ TcTrace g_tctrace[kTcTraceMax];
 __device__ uint32_t g_tctrace_n;
@@ -120,6 +121,14 @@ __device__ __forceinline__ void tc_store4(const TcArgs& a, int64_t tok, int64_t 
                 a.y[idx] = epilogue_value(silu_mul_value(f[j], f[j + 1]), a.ops, a.res, idx);
             }
         }
+        return;
+    }
+    if (!FU && rr + 3 < a.N && ((tok * a.N + rr) & 3) == 0) {      // one 8-B store
+        const uint32_t lo = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[0]))) |
+                            (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[1]))) << 16);
+        const uint32_t hi = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[2]))) |
+                            (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[3]))) << 16);
+        *reinterpret_cast<uint2*>(a.y + tok * a.N + rr) = make_uint2(lo, hi);
         return;
     }
 #pragma unroll
@@ -197,8 +206,8 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const int ks1 = static_cast<int>(static_cast<int64_t>(z + 1) * a.kt / a.split);
     const int nst = ks1 - ks0;              // >= 1 (split <= kt)
     const int nsub = nst * kSubPerStage;
-    __shared__ uint64_t tr_slots[8];
-    if (threadIdx.x < 8) tr_slots[threadIdx.x] = 0;
+    __shared__ uint64_t tr_slots[11];
+    if (threadIdx.x < 11) tr_slots[threadIdx.x] = 0;
     const uint64_t t_start = a.trace ? globaltimer() : 0;
     uint64_t wacc = 0, wacc2 = 0, wacc3 = 0, wacc4 = 0;
 
@@ -293,6 +302,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                     mbar_wait(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], xph);
                 }
                 tc_fence_after();
+                if (a.trace && j == 0) tr_slots[8] = globaltimer();
                 const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * Cfg::kXStageBytes));
 #pragma unroll
                 for (int kk = 0; kk < kTcXStageK / 16; ++kk) {
@@ -382,12 +392,44 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const int64_t row = m0 + m;
     const bool row_ok = row < a.N;
-    if (a.split == 1 || !a.cluster) {
+    if (a.split == 1) {
+        // Direct store: the 8 transform warps split the columns (warps w and
+        // w + 4 share TMEM lanes 32 (w % 4) ..), and the TMEM load of the next
+        // 16 columns is issued before the stores of the current ones.
+        constexpr int kCols = BN >= 32 ? BN / 2 : BN;
+        const bool mine = BN >= 32 ? (warp >= 4 && warp < 12) : epi;
+        const int cbeg = BN >= 32 ? ((warp - 4) >> 2) * kCols : 0;
+        if (mine) {
+            mbar_wait(acc_full, 0);
+            tc_fence_after();
+            if (a.trace && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
+            pdl_wait();
+            uint32_t v0[16], v1[16];
+            tmem_ld_32x32b_x16(tmem_base + lane_base + cbeg, v0);
+            tc_wait_ld();
+#pragma unroll 1
+            for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
+                if (c0 + 16 < cbeg + kCols) tmem_ld_32x32b_x16(tmem_base + lane_base + c0 + 16, v1);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    tc_store<FU>(a, 0xffffffffu, n0 + c0 + i, row, __uint_as_float(v0[i]), row_ok && n0 + c0 + i < a.n);
+                tc_wait_ld();
+                if (c0 + 16 >= cbeg + kCols) break;
+                if (c0 + 32 < cbeg + kCols) tmem_ld_32x32b_x16(tmem_base + lane_base + c0 + 32, v0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    tc_store<FU>(a, 0xffffffffu, n0 + c0 + 16 + i, row, __uint_as_float(v1[i]),
+                                 row_ok && n0 + c0 + 16 + i < a.n);
+                tc_wait_ld();
+            }
+        }
+    } else if (!a.cluster) {
         if (epi) {
             mbar_wait(acc_full, 0);
             tc_fence_after();
+            if (a.trace && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
             pdl_wait();
-            const bool split = a.split > 1;
+            const bool split = true;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 16) {
                 uint32_t v[16];
@@ -446,16 +488,29 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         // distributed shared memory in fixed rank order (deterministic, no HBM
         // workspace).
         float* red = reinterpret_cast<float*>(smem);
-        if (epi) {
+        // park the tile: 8 warps split the columns (as in the direct store),
+        // the next TMEM load issued before the current columns are written
+        constexpr int kCols = BN >= 32 ? BN / 2 : BN;
+        const bool mine = BN >= 32 ? (warp >= 4 && warp < 12) : epi;
+        const int cbeg = BN >= 32 ? ((warp - 4) >> 2) * kCols : 0;
+        if (mine) {
             mbar_wait(acc_full, 0);
             tc_fence_after();
+            if (a.trace && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
+            uint32_t v0[16], v1[16];
+            tmem_ld_32x32b_x16(tmem_base + lane_base + cbeg, v0);
+            tc_wait_ld();
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(tmem_base + lane_base + c0, v);
-                tc_wait_ld();
+            for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
+                if (c0 + 16 < cbeg + kCols) tmem_ld_32x32b_x16(tmem_base + lane_base + c0 + 16, v1);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) red[(c0 + i) * kTcBM + m] = __uint_as_float(v[i]);
+                for (int i = 0; i < 16; ++i) red[(c0 + i) * kTcBM + m] = __uint_as_float(v0[i]);
+                tc_wait_ld();
+                if (c0 + 16 >= cbeg + kCols) break;
+                if (c0 + 32 < cbeg + kCols) tmem_ld_32x32b_x16(tmem_base + lane_base + c0 + 32, v0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) red[(c0 + 16 + i) * kTcBM + m] = __uint_as_float(v1[i]);
+                tc_wait_ld();
             }
         }
         cluster_arrive_release();
@@ -485,6 +540,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (a.trace && threadIdx.x == 0) tr_slots[10] = globaltimer();
     if (warp == 3) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
     if (a.trace && threadIdx.x == 0) {
         const uint32_t i = atomicAdd(&g_tctrace_n, 1u);
@@ -495,6 +551,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             r.nsub = nsub; r.pad = 0; r.t0 = t_start; r.t_end = globaltimer();
             r.w_prod = tr_slots[0]; r.x_prod = tr_slots[1]; r.perm = tr_slots[2];
             r.tr_w = tr_slots[3]; r.tr_a = tr_slots[4]; r.mma_a = tr_slots[5]; r.mma_x = tr_slots[6]; r.epi = tr_slots[7];
+            r.t_mma0 = tr_slots[8]; r.t_acc = tr_slots[9]; r.t_epi = tr_slots[10];
             g_tctrace[i] = r;
         }
     }
