@@ -82,6 +82,7 @@ struct TcArgs {
     uint32_t ops;         // fused epilogue (RELAX_OP_SILU_MUL / RESIDUAL; RMSNORM_X runs before)
     const uint16_t* res;  // RESIDUAL: fp16 [n][Nout]
     int64_t Nout;         // N/2 with SILU_MUL, else N (row stride of y)
+    int ytma;             // 1: tm_y is valid (N % 8 == 0) and the FU = 0 epilogue stores by TMA
 };
 
 // Final store of output element (tok, row) with value f (fp32 sum) under the
@@ -175,7 +176,8 @@ struct TcCfg {
 template <int BN, int FU>
 __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kCtasPerSm)
 tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
-             const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TcArgs a) {
+             const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_y,
+             const __grid_constant__ TcArgs a) {
     using Cfg = TcCfg<BN>;
     constexpr int AS = Cfg::kAStages;
     constexpr int XS = Cfg::kXStages;
@@ -404,6 +406,10 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             tc_fence_after();
             if (a.trace && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
             pdl_wait();
+            // FU = 0: the fp16 tile is staged in the drained rings as
+            // [token][row] (rows contiguous, as in y) and written by one TMA
+            // tensor store (out-of-range rows / tokens are clipped by the TMA).
+            uint16_t* ytile = reinterpret_cast<uint16_t*>(smem);
             uint32_t v0[16], v1[16];
             tmem_ld_32x32b_x16(tmem_base + lane_base + cbeg, v0);
             tc_wait_ld();
@@ -411,16 +417,31 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
                 if (c0 + 16 < cbeg + kCols) tmem_ld_32x32b_x16(tmem_base + lane_base + c0 + 16, v1);
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    tc_store<FU>(a, 0xffffffffu, n0 + c0 + i, row, __uint_as_float(v0[i]), row_ok && n0 + c0 + i < a.n);
+                for (int i = 0; i < 16; ++i) {
+                    if (FU || !a.ytma) tc_store<FU>(a, 0xffffffffu, n0 + c0 + i, row, __uint_as_float(v0[i]),
+                                                    row_ok && n0 + c0 + i < a.n);
+                    else ytile[(c0 + i) * kTcBM + m] = __half_as_ushort(__float2half_rn(__uint_as_float(v0[i])));
+                }
                 tc_wait_ld();
                 if (c0 + 16 >= cbeg + kCols) break;
                 if (c0 + 32 < cbeg + kCols) tmem_ld_32x32b_x16(tmem_base + lane_base + c0 + 32, v0);
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    tc_store<FU>(a, 0xffffffffu, n0 + c0 + 16 + i, row, __uint_as_float(v1[i]),
-                                 row_ok && n0 + c0 + 16 + i < a.n);
+                for (int i = 0; i < 16; ++i) {
+                    if (FU || !a.ytma) tc_store<FU>(a, 0xffffffffu, n0 + c0 + 16 + i, row, __uint_as_float(v1[i]),
+                                                    row_ok && n0 + c0 + 16 + i < a.n);
+                    else ytile[(c0 + 16 + i) * kTcBM + m] = __half_as_ushort(__float2half_rn(__uint_as_float(v1[i])));
+                }
                 tc_wait_ld();
+            }
+            if (!FU && a.ytma) {
+                fence_proxy_async_smem();                     // generic STS -> async-proxy TMA read
+                constexpr int kEpiThreads = (BN >= 32 ? 8 : 4) * 32;
+                asm volatile("bar.sync 2, %0;" :: "n"(kEpiThreads) : "memory");
+                if (warp == 4 && lane == 0) {
+                    tma_store_2d(&tm_y, ytile, static_cast<int32_t>(m0), static_cast<int32_t>(n0));
+                    bulk_commit_group();
+                    bulk_wait_group_read0();                  // SMEM may be released after this
+                }
             }
         }
     } else if (!a.cluster) {
@@ -639,7 +660,15 @@ static int launch_tc_k(const CUtensorMap& mw, const CUtensorMap& ms, const uint1
         attr[1].val.clusterDim.z = static_cast<unsigned>(a.split);
         cfg.numAttrs = 2;
     }
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN, FU>, mw, ms, mx, a));
+    // y [n][N] fp16 as a 2-D tensor map {N rows, n tokens}, box {128, BN}
+    // (the FU = 0 direct epilogue stores whole tiles through it)
+    CUtensorMap my = mx;                 // placeholder when unused (ytma = 0)
+    if (a.ytma) {
+        rc = make_map_2d(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.y, a.N, a.n, a.N * 2, kTcBM, BN,
+                         CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (rc) return rc;
+    }
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN, FU>, mw, ms, mx, my, a));
 }
 
 template <int BN>
@@ -676,6 +705,7 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.ops = fu.ops & (RELAX_OP_SILU_MUL | RELAX_OP_RESIDUAL);
     a.res = fu.res;
     a.Nout = (fu.ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
+    a.ytma = (a.ops == 0 && plan.split == 1 && N % 8 == 0) ? 1 : 0;
     static int tr = [] { const char* e = std::getenv("RELAX_Q4_TRACE"); return (e && *e == '1') ? 1 : 0; }();
     a.trace = tr;
     if (plan.split > 1 && !plan.cluster) {
