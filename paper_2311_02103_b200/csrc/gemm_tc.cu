@@ -53,7 +53,8 @@ constexpr int kSubPerStage = kTcWStageK / kTcXStageK;                // 4
 // ---- optional per-CTA role timing (RELAX_Q4_TRACE=1): wait cycles per role
 struct TcTrace { uint32_t cta, smid, nsub, pad; uint64_t t0, t_end;
                  uint64_t w_prod, x_prod, perm, tr_w, tr_a, mma_a, mma_x, epi;
-                 uint64_t t_mma0, t_acc, t_epi; };   // globaltimer: first MMA issued, accumulator ready, stores done
+                 uint64_t t_mma0, t_acc, t_epi;       // globaltimer: first MMA issued, accumulator ready, stores done
+                 uint64_t t_cb1, t_cred, t_cb2; };    // cluster split: after 1st barrier, after reduce, after 2nd barrier
 constexpr int kTcTraceMax = 1 << 14;
 __device__ TcTrace g_tctrace[kTcTraceMax];
 __device__ uint32_t g_tctrace_n;
@@ -208,8 +209,8 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const int ks1 = static_cast<int>(static_cast<int64_t>(z + 1) * a.kt / a.split);
     const int nst = ks1 - ks0;              // >= 1 (split <= kt)
     const int nsub = nst * kSubPerStage;
-    __shared__ uint64_t tr_slots[11];
-    if (threadIdx.x < 11) tr_slots[threadIdx.x] = 0;
+    __shared__ uint64_t tr_slots[14];
+    if (threadIdx.x < 14) tr_slots[threadIdx.x] = 0;
     const uint64_t t_start = a.trace ? globaltimer() : 0;
     uint64_t wacc = 0, wacc2 = 0, wacc3 = 0, wacc4 = 0;
 
@@ -536,6 +537,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         }
         cluster_arrive_release();
         cluster_wait_acquire();
+        if (a.trace && threadIdx.x == 128) tr_slots[11] = globaltimer();
         pdl_wait();
         const uint32_t S = static_cast<uint32_t>(a.split);
         const uint32_t r = cluster_ctarank();
@@ -554,8 +556,10 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             const int64_t rr = m0 + static_cast<int64_t>(e % kTcBM);
             tc_store4<FU>(a, tok, rr, f);
         }
+        if (a.trace && threadIdx.x == 128) tr_slots[12] = globaltimer();
         cluster_arrive_release();
         cluster_wait_acquire();
+        if (a.trace && threadIdx.x == 128) tr_slots[13] = globaltimer();
     }
 
     tc_fence_before();
@@ -573,6 +577,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             r.w_prod = tr_slots[0]; r.x_prod = tr_slots[1]; r.perm = tr_slots[2];
             r.tr_w = tr_slots[3]; r.tr_a = tr_slots[4]; r.mma_a = tr_slots[5]; r.mma_x = tr_slots[6]; r.epi = tr_slots[7];
             r.t_mma0 = tr_slots[8]; r.t_acc = tr_slots[9]; r.t_epi = tr_slots[10];
+            r.t_cb1 = tr_slots[11]; r.t_cred = tr_slots[12]; r.t_cb2 = tr_slots[13];
             g_tctrace[i] = r;
         }
     }

@@ -18,7 +18,8 @@ from paper_2311_02103_b200 import inputs, ops  # noqa: E402
 REC = np.dtype([("cta", "<u4"), ("smid", "<u4"), ("nsub", "<u4"), ("pad", "<u4"), ("t0", "<u8"), ("te", "<u8"),
                 ("w_prod", "<u8"), ("x_prod", "<u8"), ("perm", "<u8"), ("tr_w", "<u8"), ("tr_a", "<u8"),
                 ("mma_a", "<u8"), ("mma_x", "<u8"), ("wst", "<u8"),
-                ("t_mma0", "<u8"), ("t_acc", "<u8"), ("t_epi", "<u8")])
+                ("t_mma0", "<u8"), ("t_acc", "<u8"), ("t_epi", "<u8"),
+                ("t_cb1", "<u8"), ("t_cred", "<u8"), ("t_cb2", "<u8")])
 K, N, n = map(int, sys.argv[1:4])
 split = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 bn = int(sys.argv[5]) if len(sys.argv) > 5 else 0
@@ -46,6 +47,9 @@ print(f"CTA duration us: min {dur.min():.2f} med {np.median(dur):.2f} max {dur.m
 ph = lambda a_, b_: np.median((r[b_].astype(np.int64) - r[a_].astype(np.int64)) / 1e3)  # noqa: E731
 print(f"phases (median us): start->first MMA {ph('t0', 't_mma0'):.2f}  first MMA->acc ready {ph('t_mma0', 't_acc'):.2f}  "
       f"acc ready->stores done {ph('t_acc', 't_epi'):.2f}  stores done->exit {ph('t_epi', 'te'):.2f}")
+if r["t_cb1"].max() > 0:
+    print(f"cluster split (median us): acc ready->after barrier 1 {ph('t_acc', 't_cb1'):.2f}  reduce+store {ph('t_cb1', 't_cred'):.2f}  "
+          f"barrier 2 {ph('t_cred', 't_cb2'):.2f}")
 for f in ["w_prod", "x_prod", "perm", "tr_w", "tr_a", "mma_a", "mma_x", "wst"]:
     us = r[f] / 1.9e3
     print(f"  wait {f:7s}: median {np.median(us):7.2f} us  max {us.max():7.2f} us   (cycles/1.9GHz)")
