@@ -252,3 +252,46 @@ def test_workspace_reused_across_calls():
                                        split_k=split, flags=ops.FLAG_SPLIT_WORKSPACE))
         r = oracle.matmul_cols_f64(xb, pw_np, sc_np, K, cols)
         assert_within_tol(y[:, cols], r, f"reuse n={n} split={split}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 64, 300])
+def test_dependent_pdl_chain_in_graph(n):
+    """The benchmark's launch configuration with a REAL data dependency: a
+    chain y1 = W1 x, y2 = W2 y1, y3 = W3 y2 (square shapes, K = N) launched
+    back to back with programmatic dependent launch inside one CUDA graph,
+    replayed several times.  Each kernel prefetches its weights before
+    griddepcontrol.wait; this checks that x is only read after the previous
+    kernel's y is complete: every stage matches the oracle applied to the
+    previous stage's GPU output (fp16, as the chain passes it)."""
+    K = 1024
+    mats = [inputs.weights("realistic", 7100 + i, K, K) for i in range(3)]
+    dev = [dev_weights(p, s) for p, s in mats]
+    x0 = inputs.activations(7200 + n, n, K)
+    x = dev_x(x0)
+    ys = [torch.empty((n, K), dtype=torch.float16, device="cuda") for _ in range(3)]
+    ws = ops.workspace(n, K, K)
+    st = torch.cuda.Stream()
+
+    def chain():
+        inp = x
+        for (pw, sc), y in zip(dev, ys):
+            ops.q4_matmul(inp, pw, sc, y=y, ws=ws, stream=st)
+            inp = y
+
+    with torch.cuda.stream(st):
+        chain()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        chain()
+    for y in ys:
+        y.fill_(float("nan"))
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    inp_bits = x0
+    for i, ((packed, scales), y) in enumerate(zip(mats, ys)):
+        got = host_bits(y)
+        r = oracle.matmul_f64(inp_bits, packed, scales, K, K)
+        assert_within_tol(got, r, f"chain stage {i} n={n}")
+        inp_bits = got
