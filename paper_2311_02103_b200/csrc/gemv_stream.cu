@@ -45,6 +45,7 @@ struct GsArgs {
     uint32_t stage_bytes;  // RS * (K/2 + K/16)
     int rows_cta_max;
     uint32_t trace_seq;    // 0 = no trace, else launch sequence number
+    int prefetch;          // stages the producer issues before griddepcontrol.wait
     // fused neighbours (include/relax_q4.h RELAX_OP_*)
     uint32_t ops;
     float eps;             // RMSNORM_X
@@ -283,7 +284,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
             const uint8_t* ssrc = a.s + row0 * sb_row;
             int slot = 0;
             uint32_t phase = 0;
+            int issued = 0;
             for (int r = 0; r < rows; r += a.RS) {
+                if (issued++ == a.prefetch) pdl_wait();     // stages streamed before the previous kernel ends
                 mbar_wait(&empty[slot], phase ^ 1);
                 const int nr = rows - r < a.RS ? rows - r : a.RS;
                 const uint32_t bc = static_cast<uint32_t>(nr) * cb_row;
@@ -434,6 +437,12 @@ static bool gs_trace() {
     return v;
 }
 
+static int gs_prefetch(int ns) {
+    static int v = [] { const char* e = std::getenv("RELAX_Q4_GS_PREFETCH"); return e ? std::atoi(e) : -1; }();
+    return v < 0 ? (1 << 30) : v;               // default: no limit (the whole ring)
+    (void)ns;
+}
+
 static int gs_zpf() {
     static int v = [] {
         const char* e = std::getenv("RELAX_Q4_GEMV_ZPF");
@@ -565,6 +574,7 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.Nout = Nout;
         a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
         a.rows_cta_max = c.rows_cta_max;
+        a.prefetch = gs_prefetch(c.NS);
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
         int rc;
         if (cnt == 1) rc = zpf ? launch_gs_z<1, 1>(a, c, pdl, stream) : launch_gs_z<1, 0>(a, c, pdl, stream);
