@@ -15,6 +15,9 @@ b 7b_decode
 b 7b_decode_fused --fused --no-cpu-baseline
 b 13b_decode --workload llama2-13b-decode --no-cpu-baseline
 b 13b_decode_fused --workload llama2-13b-decode --fused --no-cpu-baseline
+b 7b_decode_batch2 --n 2 --no-cpu-baseline
+b 7b_decode_batch8 --n 8 --no-cpu-baseline
+b 7b_decode_batch32 --n 32 --no-cpu-baseline
 b 7b_block_fused --block fused --no-cpu-baseline
 b 7b_block_unfused --block unfused --no-cpu-baseline
 b 13b_block_fused --workload llama2-13b-decode --block fused --no-cpu-baseline
