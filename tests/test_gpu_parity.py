@@ -295,3 +295,24 @@ def test_dependent_pdl_chain_in_graph(n):
         r = oracle.matmul_f64(inp_bits, packed, scales, K, K)
         assert_within_tol(got, r, f"chain stage {i} n={n}")
         inp_bits = got
+
+
+def test_random_shapes_every_path():
+    """Seeded random (n, K, N) over the whole dispatch range, including tiny
+    and ragged N (N < 8, N % 8 != 0: no TMA store), K at the tensor-core
+    minimum, and n just past tile sizes; the automatic schedule against the
+    oracle."""
+    rng = np.random.default_rng(20261018)
+    cases = []
+    for _ in range(24):
+        K = int(rng.choice([256, 512, 768, 1280, 2304, 4096]))
+        N = int(rng.choice([1, 2, 6, 8, 24, 130, 256, 384, 1000, 2048]))
+        n = int(rng.choice([1, 2, 3, 7, 16, 17, 33, 64, 65, 129, 200, 257]))
+        cases.append((n, K, N))
+    cases += [(300, 256, 8), (1, 256, 1), (2, 4096, 6), (129, 1280, 130)]
+    for i, (n, K, N) in enumerate(cases):
+        packed, scales = inputs.weights("realistic" if i % 2 else "stress", 8000 + i, K, N)
+        x = inputs.activations(8100 + i, n, K, "normal" if i % 2 else "uniform")
+        r = oracle.matmul_f64(x, packed, scales, K, N)
+        y = run(x, packed, scales, ws_n_max=n)
+        assert_within_tol(y, r, f"random case {i}: n={n} K={K} N={N} sched={ops.query_schedule(n, K, N)}")
