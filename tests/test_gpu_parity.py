@@ -316,3 +316,43 @@ def test_random_shapes_every_path():
         r = oracle.matmul_f64(x, packed, scales, K, N)
         y = run(x, packed, scales, ws_n_max=n)
         assert_within_tol(y, r, f"random case {i}: n={n} K={K} N={N} sched={ops.query_schedule(n, K, N)}")
+
+
+def test_bench_configuration_sampled():
+    """bench.py's launch configuration at full size: one decoder layer of the
+    7B set (q, k, v, o, gate, up, down) + lm_head, distinct weight buffers,
+    back-to-back calls with PDL captured in a CUDA graph and replayed; every
+    output checked on sampled columns against the oracle."""
+    spec = inputs.LLAMA_SETS["llama2-7b"]
+    mats = list(spec["mats"]) + [("lm_head", *spec["lm_head"])]
+    st = torch.cuda.Stream()
+    host, devw, xs, ys = [], [], {}, []
+    for i, (name, K, N) in enumerate(mats):
+        pk, sc = inputs.realistic_weights(2000 + i, K, N)
+        host.append((pk, sc))
+        devw.append(dev_weights(pk, sc))
+        if K not in xs:
+            xs[K] = inputs.activations(2100 + K, 1, K)
+        ys.append(torch.full((1, N), float("nan"), dtype=torch.float16, device="cuda"))
+    xd = {K: dev_x(v) for K, v in xs.items()}
+
+    def step():
+        for (name, K, N), (pw, sc), y in zip(mats, devw, ys):
+            ops.q4_matmul_ex(xd[K], pw, sc, y=y, stream=st)
+
+    with torch.cuda.stream(st):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        step()
+    for y in ys:
+        y.fill_(float("nan"))
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    for (name, K, N), (pk, sc), y in zip(mats, host, ys):
+        cols = np.sort(rng.choice(N, 96, replace=False))
+        r = oracle.matmul_cols_f64(xs[K], pk, sc, K, cols)
+        assert_within_tol(host_bits(y)[:, cols], r, f"bench config {name} {K}x{N}")
