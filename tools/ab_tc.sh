@@ -1,4 +1,6 @@
 #!/bin/bash
+# A/B of tensor-core sweeps: this tree vs old_build/ (a snapshot of an earlier commit: copy the
+# package, include/, oracle/, bench.py and tools/sweep.py, summarize_sweep.py into old_build/ first).
 python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
 (cd old_build && python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1)
 A="--shapes 4096x4096,11008x4096 --ns 128,512,2048 --variants auto --reps 10"

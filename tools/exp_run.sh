@@ -1,4 +1,6 @@
 #!/bin/bash
+# Fixed-latency breakdown of the decode GEMV (profiles/gemv_latency_r01.txt): needs exp_build/, a copy of
+# the package whose gemv_stream.cu honours -DEXP_NO_X / -DEXP_NO_WAIT and whose build.py passes $EXP_DEFS.
 cd exp_build
 for v in "" "-DEXP_NO_X" "-DEXP_NO_WAIT" "-DEXP_NO_X -DEXP_NO_WAIT"; do
   rm -rf build paper_2311_02103_b200/librelax_q4.so

@@ -1,4 +1,5 @@
 #!/bin/bash
+# Decoder-block benches (bench.py --block fused|unfused) for 7B and 13B.
 python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
 val() { python -c "import json;d=json.load(open('$1'));print(d['value'], d['ms_per_step'], d['e2e']['value'], d['gpu_launches'], d['config']['workload'])"; }
 for b in "--fused" "--block fused" "--block unfused"; do

@@ -1,4 +1,5 @@
 #!/bin/bash
+# Decode bench under GEMV knob settings (used for the prefetch-depth experiment).
 python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
 val() { python -c "import json;d=json.load(open('$1'));print(d['value'])"; }
 for v in "X=1" "RELAX_Q4_GS_L2PF=0" "X=1" "RELAX_Q4_GS_L2PF=0"; do
