@@ -242,14 +242,18 @@ int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32
     // Decode kernels: the streamed CUDA-core GEMV (gemv_stream.cu, default),
     // the warp-MMA GEMV (gemv_mma.cu, measured slower so far: DESIGN.md §5.2),
     // the lane-per-row GEMV (gemv_row.cu), then the generic one below.
-    // RELAX_Q4_GEMV_IMPL=stream|mma|row|v1 pins one (tests and measurements).
+    // RELAX_Q4_GEMV_IMPL=stream|mma|bdmma|row|v1 pins one (tests and measurements;
+    // bdmma = the block-diagonal warp-MMA variant, n = 1 only).
     static int impl = [] {
         const char* e = std::getenv("RELAX_Q4_GEMV_IMPL");
         if (e && std::strcmp(e, "mma") == 0) return 1;
         if (e && std::strcmp(e, "row") == 0) return 2;
         if (e && std::strcmp(e, "v1") == 0) return 3;
+        if (e && std::strcmp(e, "bdmma") == 0) return 4;
         return 0;
     }();
+    if (impl == 4 && n == 1 && gemv_bdmma_ok(K, N))
+        return launch_gemv_mma(x, n, K, N, w, s, y, pdl, stream, true);
     if (n == 1 && impl == 2 && gemv_row_ok(K))
         return launch_gemv_row(x, n, K, N, w, s, y, pdl, stream);
     if (impl == 1 && nt <= 2 && gemv_mma_ok(n >= 2 ? 2 : 1, K, N))

@@ -171,8 +171,59 @@ __device__ __forceinline__ void gm_groups(float (&acc)[4], const uint8_t* stage,
     }
 }
 
+// Block-diagonal variant (BD = 1, n = 1): the MMA's 8
+// columns are this warp's GPW groups of the chunk instead of tokens.  Lane
+// (g, t) supplies B only for the MMAs of its own group column g (zero
+// otherwise), so the 2 * GPW MMAs of a stage leave in column c the per-group
+// dot product of group c for rows g and g + 8; 4 independent accumulator
+// chains; the zero point enters once as the C operand of chain 0; the scales
+// are applied once per stage (4 FFMA) instead of once per group.
+template <int GPW>
+__device__ __forceinline__ void gm_groups_bd(float (&acc)[2], const uint8_t* stage, int g, int t, int jj0,
+                                             const uint32_t (&xb)[4], float m0, float m1) {
+    float dd[4][4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dd[c][q] = 0.f;
+    dd[0][0] = m0; dd[0][1] = m1; dd[0][2] = m0; dd[0][3] = m1;
+    const uint8_t* crow = stage + g * 128 + 4 * t;
+#pragma unroll
+    for (int i = 0; i < GPW; ++i) {
+        const int jj = jj0 + i;
+        const uint8_t* p = crow + (jj >> 3) * 2048 + (((jj & 7) ^ g) << 4);
+        const uint32_t wa = *reinterpret_cast<const uint32_t*>(p);
+        const uint32_t wb = *reinterpret_cast<const uint32_t*>(p + 1024);
+        const uint32_t wa8 = wa >> 8, wb8 = wb >> 8;
+        const uint32_t a1[4] = {wa & 0x000F000Fu, wb & 0x000F000Fu, wa8 & 0x000F000Fu, wb8 & 0x000F000Fu};
+        const uint32_t a2[4] = {wa & 0x00F000F0u, wb & 0x00F000F0u, wa8 & 0x00F000F0u, wb8 & 0x00F000F0u};
+        const bool mine = g == i;
+        float d1[4], d2[4];
+        mma16816(d1, a1, mine ? xb[0] : 0u, mine ? xb[1] : 0u, dd[(2 * i) & 3][0], dd[(2 * i) & 3][1],
+                 dd[(2 * i) & 3][2], dd[(2 * i) & 3][3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dd[(2 * i) & 3][q] = d1[q];
+        mma16816(d2, a2, mine ? xb[2] : 0u, mine ? xb[3] : 0u, dd[(2 * i + 1) & 3][0], dd[(2 * i + 1) & 3][1],
+                 dd[(2 * i + 1) & 3][2], dd[(2 * i + 1) & 3][3]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dd[(2 * i + 1) & 3][q] = d2[q];
+    }
+    float d[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = (dd[0][q] + dd[1][q]) + (dd[2][q] + dd[3][q]);
+    // scales of groups jj0 + 2t, jj0 + 2t + 1 for rows g, g + 8 (one 4-B load each)
+    const int c0 = 2 * t;
+    const uint8_t* sp = stage + kGmCodeBytes + g * 128 + ((((jj0 + c0) >> 3) ^ g) << 4) + ((jj0 + c0) & 7) * 2;
+    const uint32_t sa = c0 < GPW ? *reinterpret_cast<const uint32_t*>(sp) : 0u;
+    const uint32_t sb = c0 < GPW ? *reinterpret_cast<const uint32_t*>(sp + 1024) : 0u;
+    const float2 fa = __half22float2(u32_as_h2(sa));
+    const float2 fb = __half22float2(u32_as_h2(sb));
+    acc[0] = fmaf(fa.x, d[0], fmaf(fa.y, d[1], acc[0]));
+    acc[1] = fmaf(fb.x, d[2], fmaf(fb.y, d[3], acc[1]));
+}
+
 // W consumer warps + 1 producer warp; GPW = 64 / W groups per warp per chunk.
-template <int NT, int GPW>
+template <int NT, int GPW, int BD>
 __global__ void __launch_bounds__((64 / GPW + 1) * 32, 2)
 gemv_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap ms,
                 const __grid_constant__ GmArgs a) {
@@ -223,6 +274,75 @@ gemv_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ 
     } else {
         // ------------------------------------------------ consumers
         pdl_wait();
+        if constexpr (BD) {
+            // x straight from global: lane (g, t) needs, per chunk, the 8 x of
+            // its own group column (kw * GPW + g) at slots 8t..8t+7, and the
+            // zero-point terms of columns 2t, 2t + 1 (quad sums, shuffled).
+            const int g = lane >> 2, t = lane & 3;
+            const int kw = warp;
+            auto xload = [&](int kc) -> uint4 {
+                const int j = kc * kGmChunkG + kw * GPW + g;
+                return (g < GPW && kc < a.nkc && j < a.G)
+                       ? *reinterpret_cast<const uint4*>(a.x + static_cast<int64_t>(j) * 32 + t * 8)
+                       : make_uint4(0u, 0u, 0u, 0u);
+            };
+            uint4 vn = xload(0), vn2 = xload(1);
+            uint32_t xb[4];
+            float m0 = 0.f, m1 = 0.f;
+            const __half2 sixteenth = __float2half2_rn(0.0625f);
+            int slot = 0, rb = 0, kc = 0;
+            uint32_t phase = 0;
+            for (int st = 0; st < nst; ++st) {
+                if (rb == 0) {
+                    const uint4 v = vn;
+                    vn = vn2;
+                    vn2 = xload(kc + 2);
+                    xb[0] = prmt(v.x, v.z, 0x5410u);
+                    xb[1] = prmt(v.y, v.w, 0x5410u);
+                    xb[2] = h2_as_u32(__hmul2(u32_as_h2(prmt(v.x, v.z, 0x7632u)), sixteenth));
+                    xb[3] = h2_as_u32(__hmul2(u32_as_h2(prmt(v.y, v.w, 0x7632u)), sixteenth));
+                    const uint32_t ws[4] = {v.x, v.y, v.z, v.w};
+                    float p2[2] = {0.f, 0.f};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float2 f = __half22float2(u32_as_h2(ws[u]));
+                        p2[u & 1] += f.x + f.y;
+                    }
+                    float sum = p2[0] + p2[1];
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                    sum += __shfl_xor_sync(0xffffffffu, sum, 2);      // group of column g, at lanes 4g..4g+3
+                    const float mc0 = __shfl_sync(0xffffffffu, sum, (2 * t) * 4);
+                    const float mc1 = __shfl_sync(0xffffffffu, sum, (2 * t + 1) * 4);
+                    m0 = -7.0f * 5.9604644775390625e-08f * mc0;
+                    m1 = -7.0f * 5.9604644775390625e-08f * mc1;
+                }
+                mbar_wait(&full[slot], phase);
+                const uint8_t* stage = ring + static_cast<size_t>(slot) * kGmStageBytes;
+                float acc[2] = {0.f, 0.f};
+                gm_groups_bd<GPW>(acc, stage, g, t, kw * GPW, xb, m0, m1);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                // row sums over the quad (columns 2t, 2t + 1 -> all of the warp's groups)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 1);
+                    acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 2);
+                }
+                if (t == 0) {
+                    const int ra = rb * kGmRows + g, rbb = ra + 8;
+                    if (ra < rows) {
+                        float* p = &part[static_cast<size_t>(ra) * W + kw];
+                        *p = kc == 0 ? acc[0] : *p + acc[0];
+                    }
+                    if (rbb < rows) {
+                        float* p = &part[static_cast<size_t>(rbb) * W + kw];
+                        *p = kc == 0 ? acc[1] : *p + acc[1];
+                    }
+                }
+                if (++slot == a.NS) { slot = 0; phase ^= 1; }
+                if (++rb == nrb) { rb = 0; ++kc; }
+            }
+        } else {
         // x in fragment order: xtab[(j*NT + tok)*4 + t] = {(x0,x4), (x2,x6), (x1,x5)/16, (x3,x7)/16}
         // with xi = x[tok][32 j + 8 t + i]; mtab[j] = -7 * 2^-24 * (sum of group j)
         // as {tok0, tok1, tok0, tok1} (the MMA C operand).  G*NT*4 is a multiple of
@@ -288,6 +408,7 @@ gemv_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ 
             if (++slot == a.NS) { slot = 0; phase ^= 1; }
             if (++rb == nrb) { rb = 0; ++kc; }
         }
+        }
     }
     __syncthreads();
     // fixed-order sum over the W warps; y = 2^24 * acc -> fp16 RNE
@@ -313,15 +434,15 @@ static int gm_warps() {
     return v;
 }
 
-static GmConfig gm_config(int nt, int64_t K, int64_t N) {
+static GmConfig gm_config(int nt, int64_t K, int64_t N, bool bd = false) {
     GmConfig c{};
     c.ok = false;
     if (K % 256 != 0 || K <= 0 || N <= 0 || nt < 1 || nt > 2) return c;
     c.W = gm_warps();
     c.threads = (c.W + 1) * 32;
     const int64_t G = K / kGroup;
-    c.xtab_bytes = static_cast<uint32_t>(G * nt * 64);
-    c.mtab_bytes = static_cast<uint32_t>(((G * 16) + 127) / 128 * 128);
+    c.xtab_bytes = bd ? 0u : static_cast<uint32_t>(G * nt * 64);
+    c.mtab_bytes = bd ? 0u : static_cast<uint32_t>(((G * 16) + 127) / 128 * 128);
     c.grid = static_cast<int>(N < kNumSMs ? N : kNumSMs);
     c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
     const size_t fixed = 1024 + 256 + c.xtab_bytes + c.mtab_bytes + static_cast<size_t>(c.rows_cta_max) * c.W * nt * 4;
@@ -334,11 +455,12 @@ static GmConfig gm_config(int nt, int64_t K, int64_t N) {
 }
 
 bool gemv_mma_ok(int nt, int64_t K, int64_t N) { return gm_config(nt, K, N).ok; }
+bool gemv_bdmma_ok(int64_t K, int64_t N) { return gm_config(1, K, N, true).ok; }
 
-template <int NT, int GPW>
+template <int NT, int GPW, int BD>
 static int launch_gm_t(const CUtensorMap& mw, const CUtensorMap& ms, const GmArgs& a, const GmConfig& c,
                        bool pdl, cudaStream_t stream) {
-    auto k = gemv_mma_kernel<NT, GPW>;
+    auto k = gemv_mma_kernel<NT, GPW, BD>;
     static bool set = false;
     if (!set) {
         cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(k), static_cast<int>(kGmSmemCap));
@@ -359,7 +481,7 @@ static int launch_gm_t(const CUtensorMap& mw, const CUtensorMap& ms, const GmArg
 }
 
 int launch_gemv_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                    const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
+                    const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream, bool bd) {
     // codes: {32 words, N rows, K/256 chunks of 128 B}; scales: {K/32, N}
     CUtensorMap mw, ms;
     {
@@ -378,7 +500,7 @@ int launch_gemv_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const ui
     }
     for (int64_t t0 = 0; t0 < n; t0 += 2) {
         const int cnt = (n - t0) >= 2 ? 2 : 1;
-        const GmConfig c = gm_config(cnt, K, N);
+        const GmConfig c = gm_config(cnt, K, N, bd && cnt == 1);
         if (!c.ok) return static_cast<int>(cudaErrorInvalidConfiguration);
         if (std::getenv("RELAX_Q4_GS_PRINT"))
             fprintf(stderr, "gemv_mma K=%lld N=%lld NT=%d W=%d NS=%d grid=%d smem=%zu\n", (long long)K,
@@ -394,8 +516,10 @@ int launch_gemv_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const ui
         a.xtab_bytes = c.xtab_bytes;
         a.mtab_bytes = c.mtab_bytes;
         int rc;
-        if (c.W == 16) rc = cnt == 1 ? launch_gm_t<1, 4>(mw, ms, a, c, pdl, stream) : launch_gm_t<2, 4>(mw, ms, a, c, pdl, stream);
-        else rc = cnt == 1 ? launch_gm_t<1, 8>(mw, ms, a, c, pdl, stream) : launch_gm_t<2, 8>(mw, ms, a, c, pdl, stream);
+        if (bd && cnt == 1) rc = c.W == 16 ? launch_gm_t<1, 4, 1>(mw, ms, a, c, pdl, stream)
+                                           : launch_gm_t<1, 8, 1>(mw, ms, a, c, pdl, stream);
+        else if (c.W == 16) rc = cnt == 1 ? launch_gm_t<1, 4, 0>(mw, ms, a, c, pdl, stream) : launch_gm_t<2, 4, 0>(mw, ms, a, c, pdl, stream);
+        else rc = cnt == 1 ? launch_gm_t<1, 8, 0>(mw, ms, a, c, pdl, stream) : launch_gm_t<2, 8, 0>(mw, ms, a, c, pdl, stream);
         if (rc != 0) return rc;
     }
     return 0;

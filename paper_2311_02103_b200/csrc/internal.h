@@ -73,8 +73,9 @@ bool gemv_stream_ok(int nt, int64_t K);
 int launch_rmsnorm(const uint16_t* x, int64_t n, int64_t K, const uint16_t* gamma, float eps,
                    uint16_t* out, bool pdl, cudaStream_t stream);
 int launch_gemv_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                    const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
+                    const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream, bool bd = false);
 bool gemv_mma_ok(int nt, int64_t K, int64_t N);
+bool gemv_bdmma_ok(int64_t K, int64_t N);
 int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                     const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
                     CUtensorMapSwizzle sw);

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("impl", ["mma", "row", "v1"])
+@pytest.mark.parametrize("impl", ["mma", "bdmma", "row", "v1"])
 def test_gemv_impl_parity(impl):
     env = dict(os.environ, RELAX_Q4_GEMV_IMPL=impl)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_gemv_impl_check.py")],

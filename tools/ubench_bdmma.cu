@@ -19,7 +19,10 @@
 #include <cuda_runtime.h>
 
 constexpr int STEPS = 2048;
-constexpr int WARPS = 16;
+#ifndef WARPS_N
+#define WARPS_N 16
+#endif
+constexpr int WARPS = WARPS_N;
 
 __device__ __forceinline__ float fhfma(uint16_t a, uint16_t b, float c) {
     float d;
