@@ -78,9 +78,19 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_fhfma(float* out, long long* 
 }
 
 // Block-diagonal MMA loop: 16 rows x 8 groups (4096 weights) per warp per step.
+// V adds the real kernel's per-step overheads one at a time:
+//   V >= 1: the 128-B-swizzled stage addressing of gemv_mma.cu (jj ^ g)
+//   V >= 2: quad-shuffle row reduction + partial-sum read-modify-write in SMEM
+//   V >= 3: an mbarrier try_wait (already complete) + arrive per step
+template <int V>
 __global__ void __launch_bounds__(WARPS * 32, 2) k_bdmma(float* out, long long* cyc, uint32_t seed) {
     // 16 rows x 8 groups x 16 B codes, padded row stride 144 B (conflict-free), + scales
     __shared__ __align__(16) uint8_t sm[16 * 144 + 16 * 16 + 128];
+    __shared__ float part[16 * WARPS];
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(&bar)), "r"((1 << 20) - 1));
+    }
     for (int i = threadIdx.x; i < (int)sizeof(sm) / 4; i += blockDim.x)
         reinterpret_cast<uint32_t*>(sm)[i] = seed * 2654435761u + i;
     __syncthreads();
@@ -94,8 +104,9 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_bdmma(float* out, long long* 
         const int jit = (st & 7) * 16;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const uint32_t wa = *reinterpret_cast<const uint32_t*>(sm + jit + g * 144 + i * 16 + t * 4);
-            const uint32_t wb = *reinterpret_cast<const uint32_t*>(sm + jit + (g + 8) * 144 + i * 16 + t * 4);
+            const int off = V >= 1 ? (((i ^ g) & 7) * 16) : i * 16;
+            const uint32_t wa = *reinterpret_cast<const uint32_t*>(sm + jit + g * 144 + off + t * 4);
+            const uint32_t wb = *reinterpret_cast<const uint32_t*>(sm + jit + (g + 8) * 144 + off + t * 4);
             const uint32_t wa8 = wa >> 8, wb8 = wb >> 8;
             const uint32_t a1[4] = {wa & 0x000F000Fu, wb & 0x000F000Fu, wa8 & 0x000F000Fu, wb8 & 0x000F000Fu};
             const uint32_t a2[4] = {wa & 0x00F000F0u, wb & 0x00F000F0u, wa8 & 0x00F000F0u, wb8 & 0x00F000F0u};
@@ -110,8 +121,27 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_bdmma(float* out, long long* 
         const uint32_t sb = *reinterpret_cast<const uint32_t*>(sm + jit + 16 * 144 + (g + 8) * 16 + t * 4);
         const float2 fa = __half22float2(*reinterpret_cast<const __half2*>(&sa));
         const float2 fb = __half22float2(*reinterpret_cast<const __half2*>(&sb));
-        y0 = fmaf(fa.x, d[0], fmaf(fa.y, d[1], y0));
-        y1 = fmaf(fb.x, d[2], fmaf(fb.y, d[3], y1));
+        float r0 = fa.x * d[0] + fa.y * d[1], r1 = fb.x * d[2] + fb.y * d[3];
+        if (V >= 2) {
+            r0 += __shfl_xor_sync(0xffffffffu, r0, 1); r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
+            r1 += __shfl_xor_sync(0xffffffffu, r1, 1); r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+            if (t == 0) {
+                float* p = &part[(threadIdx.x >> 5) * 16 + g];
+                *p = (st & 1) ? *p + r0 : r0;
+                p[8] = (st & 1) ? p[8] + r1 : r1;
+            }
+        }
+        if (V >= 3) {
+            const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&bar);
+            uint32_t ok;
+            asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                         : "=r"(ok) : "r"(ba), "r"(1u) : "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" :: "r"(ba) : "memory");
+            y0 += (float)ok;
+        }
+        y0 += r0;
+        y1 += r1;
     }
     y0 += __shfl_xor_sync(0xffffffffu, y0, 1);
     y0 += __shfl_xor_sync(0xffffffffu, y0, 2);
@@ -126,10 +156,15 @@ int main() {
     cudaMalloc(&out, 148 * 1024 * 4);
     cudaMalloc(&cyc, 148 * 8);
     long long c[148];
-    for (int v = 0; v < 2; ++v) {
+    const char* names[] = {"fhfma (gemv_stream loop)", "bdmma", "bdmma + swizzled addressing",
+                           "bdmma + swizzle + quad reduce + partial RMW", "bdmma + all + mbarrier wait/arrive"};
+    for (int v = 0; v < 5; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             if (v == 0) k_fhfma<<<148, WARPS * 32>>>(out, cyc, 7);
-            else k_bdmma<<<148, WARPS * 32>>>(out, cyc, 7);
+            else if (v == 1) k_bdmma<0><<<148, WARPS * 32>>>(out, cyc, 7);
+            else if (v == 2) k_bdmma<1><<<148, WARPS * 32>>>(out, cyc, 7);
+            else if (v == 3) k_bdmma<2><<<148, WARPS * 32>>>(out, cyc, 7);
+            else k_bdmma<3><<<148, WARPS * 32>>>(out, cyc, 7);
             cudaDeviceSynchronize();
         }
         cudaMemcpy(c, cyc, sizeof c, cudaMemcpyDeviceToHost);
@@ -137,7 +172,7 @@ int main() {
         for (int i = 0; i < 148; ++i) mx = c[i] > mx ? c[i] : mx;
         const double w = v == 0 ? (double)STEPS * 4 * 32 * 32 * WARPS      // 4 rows x 32 codes x 32 lanes per warp-step
                                 : (double)STEPS * 16 * 256 * WARPS;         // 16 rows x 256 codes per warp-step
-        printf("%s: %.1f weights/clk/SM (%s)\n", v == 0 ? "fhfma (gemv_stream loop)" : "bdmma (block-diagonal mma.sync)",
+        printf("%s: %.1f weights/clk/SM (%s)\n", names[v],
                w / mx, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
