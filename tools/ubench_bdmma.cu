@@ -150,6 +150,75 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_bdmma(float* out, long long* 
     if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// All overheads, but two 8-group windows (8192 weights) per warp step and
+// precomputed stage offsets: the amortised design.
+__global__ void __launch_bounds__(WARPS * 32, 2) k_bdmma2(float* out, long long* cyc, uint32_t seed) {
+    __shared__ __align__(16) uint8_t sm[16 * 272 + 16 * 32 + 128];
+    __shared__ float part[16 * WARPS];
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(&bar)), "r"((1 << 20) - 1));
+    }
+    for (int i = threadIdx.x; i < (int)sizeof(sm) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(sm)[i] = seed * 2654435761u + i;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t xa = 0x3c003c00u ^ seed, xb = 0x3c003c00u ^ (seed * 3);
+    int offs[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) offs[i] = g * 272 + (((i & 7) ^ g) + (i >> 3) * 8) * 16 + t * 4;   // precomputed
+    float y0 = 0.f, y1 = 0.f;
+    long long t0 = clock64();
+    for (int st = 0; st < STEPS; ++st) {
+        const int jit = (st & 7) * 16;
+        float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            float dd[4][4] = {};
+#pragma unroll
+            for (int ii = 0; ii < 8; ++ii) {
+                const int i = w * 8 + ii;
+                const uint32_t wa = *reinterpret_cast<const uint32_t*>(sm + jit + offs[i]);
+                const uint32_t wb = *reinterpret_cast<const uint32_t*>(sm + jit + offs[i] + 8 * 272);
+                const uint32_t wa8 = wa >> 8, wb8 = wb >> 8;
+                const uint32_t a1[4] = {wa & 0x000F000Fu, wb & 0x000F000Fu, wa8 & 0x000F000Fu, wb8 & 0x000F000Fu};
+                const uint32_t a2[4] = {wa & 0x00F000F0u, wb & 0x00F000F0u, wa8 & 0x00F000F0u, wb8 & 0x00F000F0u};
+                const bool mine = g == ii;
+                mma16816(dd[(2 * ii) & 3], a1, mine ? xa : 0u, mine ? xb : 0u);
+                mma16816(dd[(2 * ii + 1) & 3], a2, mine ? xb : 0u, mine ? xa : 0u);
+            }
+            float d[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[q] = (dd[0][q] + dd[1][q]) + (dd[2][q] + dd[3][q]);
+            const uint32_t sa = *reinterpret_cast<const uint32_t*>(sm + jit + 16 * 272 + g * 32 + w * 16 + t * 4);
+            const uint32_t sb = *reinterpret_cast<const uint32_t*>(sm + jit + 16 * 272 + (g + 8) * 32 + w * 16 + t * 4);
+            const float2 fa = __half22float2(*reinterpret_cast<const __half2*>(&sa));
+            const float2 fb = __half22float2(*reinterpret_cast<const __half2*>(&sb));
+            r0 = fmaf(fa.x, d[0], fmaf(fa.y, d[1], r0));
+            r1 = fmaf(fb.x, d[2], fmaf(fb.y, d[3], r1));
+        }
+        r0 += __shfl_xor_sync(0xffffffffu, r0, 1); r0 += __shfl_xor_sync(0xffffffffu, r0, 2);
+        r1 += __shfl_xor_sync(0xffffffffu, r1, 1); r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+        if (t == 0) {
+            float* p = &part[(threadIdx.x >> 5) * 16 + g];
+            *p = (st & 1) ? *p + r0 : r0;
+            p[8] = (st & 1) ? p[8] + r1 : r1;
+        }
+        const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&bar);
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(ba), "r"(1u) : "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" :: "r"(ba) : "memory");
+        y0 += r0 + (float)ok;
+        y1 += r1;
+    }
+    long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = y0 + y1;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 int main() {
     float* out;
     long long* cyc;
@@ -157,21 +226,23 @@ int main() {
     cudaMalloc(&cyc, 148 * 8);
     long long c[148];
     const char* names[] = {"fhfma (gemv_stream loop)", "bdmma", "bdmma + swizzled addressing",
-                           "bdmma + swizzle + quad reduce + partial RMW", "bdmma + all + mbarrier wait/arrive"};
-    for (int v = 0; v < 5; ++v) {
+                           "bdmma + swizzle + quad reduce + partial RMW", "bdmma + all + mbarrier wait/arrive", "bdmma, all overheads, 2 windows/step + precomputed offsets"};
+    for (int v = 0; v < 6; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             if (v == 0) k_fhfma<<<148, WARPS * 32>>>(out, cyc, 7);
             else if (v == 1) k_bdmma<0><<<148, WARPS * 32>>>(out, cyc, 7);
             else if (v == 2) k_bdmma<1><<<148, WARPS * 32>>>(out, cyc, 7);
             else if (v == 3) k_bdmma<2><<<148, WARPS * 32>>>(out, cyc, 7);
-            else k_bdmma<3><<<148, WARPS * 32>>>(out, cyc, 7);
+            else if (v == 4) k_bdmma<3><<<148, WARPS * 32>>>(out, cyc, 7);
+            else k_bdmma2<<<148, WARPS * 32>>>(out, cyc, 7);
             cudaDeviceSynchronize();
         }
         cudaMemcpy(c, cyc, sizeof c, cudaMemcpyDeviceToHost);
         long long mx = 0;
         for (int i = 0; i < 148; ++i) mx = c[i] > mx ? c[i] : mx;
         const double w = v == 0 ? (double)STEPS * 4 * 32 * 32 * WARPS      // 4 rows x 32 codes x 32 lanes per warp-step
-                                : (double)STEPS * 16 * 256 * WARPS;         // 16 rows x 256 codes per warp-step
+                        : v == 5 ? (double)STEPS * 16 * 512 * WARPS         // 16 rows x 512 codes per warp-step
+                                 : (double)STEPS * 16 * 256 * WARPS;        // 16 rows x 256 codes per warp-step
         printf("%s: %.1f weights/clk/SM (%s)\n", names[v],
                w / mx, cudaGetErrorString(cudaGetLastError()));
     }
