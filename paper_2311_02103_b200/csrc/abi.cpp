@@ -28,6 +28,19 @@ int gemv_max_n() {
 
 static int ctas_per_sm_tc(int bn) { return bn <= 64 ? 2 : 1; }
 
+// Split-K clusters of s CTAs that all start in the first wave on a B200
+// (148 SMs), measured per resident-CTA count by tools/tc_waves.py
+// (profiles/tc_waves_r01.txt): the GPC placement of clusters holds fewer than
+// slots / s of them (two CTAs per SM: 93 clusters of 3, not 98).  More tiles
+// than this at split s run a second wave of clusters (4096 x 12288 at n = 8:
+// 96 clusters of 3 took 22.6 us vs 17.1 us at s = 2).  Index s = 1..8.
+static int64_t cluster_capacity(int bn, int s) {
+    static const int64_t two[9] = {0, 296, 148, 93, 71, 56, 45, 37, 33};
+    static const int64_t one[9] = {0, 148, 74, 45, 33, 26, 22, 15, 15};
+    if (s < 1 || s > 8) return 0;
+    return ctas_per_sm_tc(bn) == 2 ? two[s] : one[s];
+}
+
 static int choose_bn(int64_t n, int64_t N) {
     (void)N;
     if (n <= 16) return 16;
@@ -56,6 +69,7 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
         const double fixed = bn == 256 ? 8.0 : 5.7;
         for (int s = 1; s <= 8 && s <= kt; ++s) {
             if (s > 1 && (tiles > kMaxSplitTiles || tiles * s > kNumSMs)) break;
+            if (s > 1 && tiles > cluster_capacity(bn, s)) continue;   // clusters would not all be resident
             const int64_t waves = (tiles * s + kNumSMs - 1) / kNumSMs;
             const int ks = (kt + s - 1) / s;
             const double t = static_cast<double>(waves) * (ks * step + fixed) + (s > 1 ? 1.0 : 0.0);
@@ -71,7 +85,6 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
 // pipelines (RELAX_Q4_TC_CTAS_PER_SM scales the target; measured 1.0 vs 2.0
 // in DESIGN.md §6: 2.0 is 3-20% faster on every 7B shape at n = 3..64).
 static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
-    (void)bn;
     (void)n;
     static double f = [] {
         const char* e = std::getenv("RELAX_Q4_TC_CTAS_PER_SM");
@@ -83,6 +96,8 @@ static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
     if (s < 1) s = 1;
     if (s > 8) s = 8;            // portable cluster: DSMEM reduction, no workspace
     if (s > kt) s = kt;
+    // one wave of clusters (cluster_capacity)
+    while (s > 1 && tiles > cluster_capacity(bn, s)) --s;
     return s;
 }
 

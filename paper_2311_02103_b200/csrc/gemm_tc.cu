@@ -33,6 +33,7 @@
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include "internal.h"
 #include "relax_q4.h"
 #include "ptx.cuh"
@@ -682,6 +683,65 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
     return a.ops ? launch_tc_k<BN, 1>(mw, ms, x, a, pdl, stream) : launch_tc_k<BN, 0>(mw, ms, x, a, pdl, stream);
 }
 
+// How many thread-block clusters of `s` CTAs of the BN kernel can be resident
+// at once (cudaOccupancyMaxActiveClusters: GPC placement, not just SM slots --
+// with two CTAs per SM, 96 clusters of 3 do not fit in 296 slots).  Cached;
+// -1 without a device.  DESIGN.md §6.
+template <int BN>
+static int max_clusters_bn(int s) {
+    using Cfg = TcCfg<BN>;
+    if (set_kernel_smem(reinterpret_cast<const void*>(tc_q4_kernel<BN, 0>), static_cast<int>(Cfg::kSmemBytes)) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(tc_q4_kernel<BN, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, 1, static_cast<unsigned>(s));
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = static_cast<unsigned>(s);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int m = 0;
+    if (cudaOccupancyMaxActiveClusters(&m, tc_q4_kernel<BN, 0>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    return m;
+}
+
+int tc_max_active_clusters(int bn, int s) {
+    if (s < 1 || s > 8) return -1;
+    static std::mutex mu;
+    static int cache[5][9];
+    static bool init = false;
+    const int bi = bn == 16 ? 0 : bn == 32 ? 1 : bn == 64 ? 2 : bn == 128 ? 3 : bn == 256 ? 4 : -1;
+    if (bi < 0) return -1;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!init) {
+        for (auto& r : cache) for (int& v : r) v = -2;
+        init = true;
+    }
+    int& v = cache[bi][s];
+    if (v == -2) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); v = -1; return v; }
+        switch (bn) {
+            case 16: v = max_clusters_bn<16>(s); break;
+            case 32: v = max_clusters_bn<32>(s); break;
+            case 64: v = max_clusters_bn<64>(s); break;
+            case 128: v = max_clusters_bn<128>(s); break;
+            default: v = max_clusters_bn<256>(s); break;
+        }
+    }
+    return v;
+}
+
 // Workspace layout (fixed ticket region first, so one buffer serves every n):
 //   [0, kTicketBytes)            uint32 tickets, one per output tile (<= 1024)
 //   [kTicketBytes, +split*n*N*4) fp32 split-K partials [split][n][N]
@@ -728,6 +788,8 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
 }
 
 }  // namespace rq4
+
+extern "C" RELAX_API int relax_debug_tc_max_clusters(int bn, int s) { return rq4::tc_max_active_clusters(bn, s); }
 
 extern "C" RELAX_API int relax_debug_tctrace_read(void* host, size_t max_records, size_t* n_records, int reset) {
     uint32_t n = 0;

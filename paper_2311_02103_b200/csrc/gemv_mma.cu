@@ -434,6 +434,15 @@ static int gm_warps() {
     return v;
 }
 
+// CTAs per SM of one launch (RELAX_Q4_GM_CTAS = 1 | 2).
+static int gm_ctas() {
+    static int v = [] {
+        const char* e = std::getenv("RELAX_Q4_GM_CTAS");
+        return (e && std::atoi(e) == 2) ? 2 : 1;
+    }();
+    return v;
+}
+
 static GmConfig gm_config(int nt, int64_t K, int64_t N, bool bd = false) {
     GmConfig c{};
     c.ok = false;
@@ -443,7 +452,8 @@ static GmConfig gm_config(int nt, int64_t K, int64_t N, bool bd = false) {
     const int64_t G = K / kGroup;
     c.xtab_bytes = bd ? 0u : static_cast<uint32_t>(G * nt * 64);
     c.mtab_bytes = bd ? 0u : static_cast<uint32_t>(((G * 16) + 127) / 128 * 128);
-    c.grid = static_cast<int>(N < kNumSMs ? N : kNumSMs);
+    const int64_t gmax = static_cast<int64_t>(kNumSMs) * gm_ctas();
+    c.grid = static_cast<int>(N < gmax ? N : gmax);
     c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
     const size_t fixed = 1024 + 256 + c.xtab_bytes + c.mtab_bytes + static_cast<size_t>(c.rows_cta_max) * c.W * nt * 4;
     if (fixed + 2 * static_cast<size_t>(kGmStageBytes) > kGmSmemCap) return c;

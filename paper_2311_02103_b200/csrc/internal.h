@@ -55,6 +55,7 @@ struct Plan {
 // `force_variant` / `force_split` / `force_bn` override (0 = choose).
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split,
               int force_bn, Plan* out, bool force_ws);
+int tc_max_active_clusters(int bn, int s);   // -1 without a device
 size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split);
 int gemv_max_n();                   // GEMV/TC threshold (env RELAX_Q4_GEMV_MAX_N)
 bool gemv_fits(int nt, int64_t K);

@@ -181,3 +181,22 @@ def test_fused_workspace_plan(L):
         for n in range(1, n_max + 1, max(1, n_max // 7)):
             assert fcall(L, ops_=R, n=n, K=4096, N=11008, w=A + 64 * MB, s=A + 128 * MB, y=A + 256 * MB,
                          gamma=A + 512 * MB, ws=A + 1024 * MB, wsb=nb) == 6
+
+
+@pytest.mark.parametrize("n", [3, 8, 16, 32, 64, 128, 512])
+@pytest.mark.parametrize("K,N", [(4096, 4096), (4096, 11008), (11008, 4096), (4096, 12288), (4096, 22016),
+                                 (8192, 1024), (8192, 28672)])
+def test_split_clusters_fit_one_wave(n, K, N):
+    """Automatic split-K never asks for more clusters than one wave holds on a
+    B200 (profiles/tc_waves_r01.txt): 4096 x 12288 at n = 8 takes
+    s = 2, not the 3 that two CTAs per SM alone would suggest."""
+    cap2 = {1: 296, 2: 148, 3: 93, 4: 71, 5: 56, 6: 45, 7: 37, 8: 33}
+    cap1 = {1: 148, 2: 74, 3: 45, 4: 33, 5: 26, 6: 22, 7: 15, 8: 15}
+    s = ops.query_schedule(n, K, N)
+    if s["variant"] != "tc" or s["split_k"] == 1:
+        return
+    tiles = -(-N // 128) * -(-n // s["tile"])
+    cap = (cap2 if s["tile"] <= 64 else cap1)[s["split_k"]]
+    assert tiles <= cap, (s, tiles, cap)
+    if (n, K, N) == (8, 4096, 12288):
+        assert s["split_k"] == 2

@@ -44,6 +44,9 @@ dur = (r["te"] - r["t0"]) / 1e3
 print(f"K={K} N={N} n={n} sched={ops.query_schedule(n, K, N)} ctas={len(r)} nsub={r['nsub'][0]}")
 print(f"CTA duration us: min {dur.min():.2f} med {np.median(dur):.2f} max {dur.max():.2f}; "
       f"kernel span {(r['te'].max() - r['t0'].min()) / 1e3:.2f} us")
+st = (r["t0"] - r["t0"].min()) / 1e3
+print(f"CTA start offset us: p10 {np.percentile(st, 10):.2f} p50 {np.median(st):.2f} p90 {np.percentile(st, 90):.2f} "
+      f"max {st.max():.2f}; CTAs per SM histogram {np.bincount(np.bincount(r['smid'].astype(np.int64)))}")
 ph = lambda a_, b_: np.median((r[b_].astype(np.int64) - r[a_].astype(np.int64)) / 1e3)  # noqa: E731
 print(f"phases (median us): start->first MMA {ph('t0', 't_mma0'):.2f}  first MMA->acc ready {ph('t_mma0', 't_acc'):.2f}  "
       f"acc ready->stores done {ph('t_acc', 't_epi'):.2f}  stores done->exit {ph('t_epi', 'te'):.2f}")
