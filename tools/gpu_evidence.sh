@@ -18,6 +18,8 @@ b 13b_decode_fused --workload llama2-13b-decode --fused --no-cpu-baseline
 b 7b_decode_batch2 --n 2 --no-cpu-baseline
 b 7b_decode_batch8 --n 8 --no-cpu-baseline
 b 7b_decode_batch32 --n 32 --no-cpu-baseline
+b 7b_decode_fused_batch8 --fused --n 8 --no-cpu-baseline
+b 7b_decode_fused_batch32 --fused --n 32 --no-cpu-baseline
 b 7b_block_fused --block fused --no-cpu-baseline
 b 7b_block_unfused --block unfused --no-cpu-baseline
 b 13b_block_fused --workload llama2-13b-decode --block fused --no-cpu-baseline
