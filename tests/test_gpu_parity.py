@@ -318,13 +318,24 @@ def test_random_shapes_every_path():
         assert_within_tol(y, r, f"random case {i}: n={n} K={K} N={N} sched={ops.query_schedule(n, K, N)}")
 
 
-def test_bench_configuration_sampled():
+@pytest.mark.parametrize("layout", ["plain", "fused"])
+@pytest.mark.parametrize("n", [1, 8, 32])
+def test_bench_configuration_sampled(layout, n):
     """bench.py's launch configuration at full size: one decoder layer of the
-    7B set (q, k, v, o, gate, up, down) + lm_head, distinct weight buffers,
-    back-to-back calls with PDL captured in a CUDA graph and replayed; every
-    output checked on sampled columns against the oracle."""
+    7B set (q, k, v, o, gate, up, down -- or, in the fused layout bench.py
+    --fused times, qkv 4096x12288, o, gate_up 4096x22016, down) + lm_head,
+    distinct weight buffers, n tokens (1 = decode, 8/32 = the batched-decode
+    lines: small-n tensor path with cluster split-K), back-to-back calls with
+    PDL captured in a CUDA graph and replayed; every output checked on sampled
+    columns (all n rows) against the oracle."""
     spec = inputs.LLAMA_SETS["llama2-7b"]
-    mats = list(spec["mats"]) + [("lm_head", *spec["lm_head"])]
+    if layout == "fused":
+        d = {name: (K, N) for name, K, N in spec["mats"]}
+        mats = [("qkv", 4096, d["q"][1] + d["k"][1] + d["v"][1]), ("o", *d["o"]),
+                ("gate_up", 4096, d["gate"][1] + d["up"][1]), ("down", *d["down"])]
+    else:
+        mats = list(spec["mats"])
+    mats.append(("lm_head", *spec["lm_head"]))
     st = torch.cuda.Stream()
     host, devw, xs, ys = [], [], {}, []
     for i, (name, K, N) in enumerate(mats):
@@ -332,8 +343,8 @@ def test_bench_configuration_sampled():
         host.append((pk, sc))
         devw.append(dev_weights(pk, sc))
         if K not in xs:
-            xs[K] = inputs.activations(2100 + K, 1, K)
-        ys.append(torch.full((1, N), float("nan"), dtype=torch.float16, device="cuda"))
+            xs[K] = inputs.activations(2100 + K + n, n, K)
+        ys.append(torch.full((n, N), float("nan"), dtype=torch.float16, device="cuda"))
     xd = {K: dev_x(v) for K, v in xs.items()}
 
     def step():
@@ -355,4 +366,5 @@ def test_bench_configuration_sampled():
     for (name, K, N), (pk, sc), y in zip(mats, host, ys):
         cols = np.sort(rng.choice(N, 96, replace=False))
         r = oracle.matmul_cols_f64(xs[K], pk, sc, K, cols)
-        assert_within_tol(host_bits(y)[:, cols], r, f"bench config {name} {K}x{N}")
+        assert_within_tol(host_bits(y)[:, cols], r,
+                          f"bench config {layout} n={n} {name} {K}x{N} sched={ops.query_schedule(n, K, N)}")
