@@ -4,7 +4,7 @@ variant) as back-to-back calls in a CUDA graph that rotates over R distinct
 weight copies totalling >= 4x the L2 (so weights stream from HBM), report
 GB/s of algorithmic bytes and TFLOPS.  One JSON object per line.
 
-    python tools/sweep.py [--shapes 4096x4096,...] [--ns 1,2,4,...] [--variants auto,gemv,tc]
+    python tools/sweep.py [--shapes 4096x4096,...] [--ns 1,2,4,...] [--variants auto,gemv,tc,tc:4]
                           [--reps 20] [--out gpurun_out/sweep.jsonl] [--no-pdl]
 """
 import argparse
@@ -72,17 +72,19 @@ def main():
             for var in a.variants.split(","):
                 if var == "gemv" and n > 8:
                     continue
-                v = {"auto": ops.VARIANT_AUTO, "gemv": ops.VARIANT_GEMV, "tc": ops.VARIANT_TC}[var]
+                base, _, sp = var.partition(":")        # "tc:S" forces split-K S (cluster reduction)
+                split = int(sp) if sp else 0
+                v = {"auto": ops.VARIANT_AUTO, "gemv": ops.VARIANT_GEMV, "tc": ops.VARIANT_TC}[base]
                 # a rotation long enough to stream >= 4 L2 of weights per replay
                 fns = [lambda p=p, s=s: ops.q4_matmul_ex(x, p, s, y=y, ws=ws, variant=v, flags=flags,
-                                                         stream=stream) for p, s in copies]
+                                                         split_k=split, stream=stream) for p, s in copies]
                 try:
                     ms = time_calls(fns, a.reps, stream)
                 except Exception as e:  # noqa: BLE001
                     print(json.dumps({"K": K, "N": N, "n": n, "variant": var, "error": str(e)}), flush=True)
                     continue
                 by = wb + 2 * n * K + 2 * n * N
-                rec = {"K": K, "N": N, "n": n, "variant": var, "sched": ops.query_schedule(n, K, N),
+                rec = {"K": K, "N": N, "n": n, "variant": var, "split": split, "sched": ops.query_schedule(n, K, N),
                        "us": round(ms * 1e3, 3), "GBps": round(by / (ms * 1e-3) / 1e9, 1),
                        "TFLOPS": round(2 * n * K * N / (ms * 1e-3) / 1e12, 2), "R": R, "pdl": not a.no_pdl}
                 print(json.dumps(rec), flush=True)
