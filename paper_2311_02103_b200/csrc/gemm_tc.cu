@@ -201,7 +201,9 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + Cfg::kNumBars);
     uint32_t* flag_slot = tmem_slot + 1;
 
-    const int warp = threadIdx.x >> 5;
+    // warp index through a shuffle: provably warp-uniform, so the per-warp
+    // TMEM addresses of the transform stay in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kTcBM;
     const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BN;
