@@ -4,7 +4,7 @@ python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
 (cd old_build && python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1)
 val() { python -c "import json;d=json.load(open('$1'));print(d['value'])"; }
 for i in 1 2; do
-  for f in "" "--fused"; do
+  for f in "" "--fused" "--n 2"; do
     timeout 100 python bench.py --no-cpu-baseline $f > gpurun_out/b_new.json 2>/dev/null
     (cd old_build && timeout 100 python bench.py --no-cpu-baseline $f > ../gpurun_out/b_old.json 2>/dev/null)
     echo "[$f] new: $(val gpurun_out/b_new.json)  old: $(val gpurun_out/b_old.json)"
