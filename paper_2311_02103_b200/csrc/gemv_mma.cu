@@ -229,7 +229,7 @@ gemv_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ 
                 const __grid_constant__ GmArgs a) {
     constexpr int W = kGmChunkG / GPW;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);   // provably warp-uniform
     const int lane = threadIdx.x & 31;
     // [pad to 1 KB][ring NS x 18 KB][barriers 256 B][xtab][mtab][part]
     uint8_t* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
