@@ -452,7 +452,7 @@ static GmConfig gm_config(int nt, int64_t K, int64_t N, bool bd = false) {
     const int64_t G = K / kGroup;
     c.xtab_bytes = bd ? 0u : static_cast<uint32_t>(G * nt * 64);
     c.mtab_bytes = bd ? 0u : static_cast<uint32_t>(((G * 16) + 127) / 128 * 128);
-    const int64_t gmax = static_cast<int64_t>(kNumSMs) * gm_ctas();
+    const int64_t gmax = static_cast<int64_t>(num_sms()) * gm_ctas();
     c.grid = static_cast<int>(N < gmax ? N : gmax);
     c.rows_cta_max = static_cast<int>((N + c.grid - 1) / c.grid);
     const size_t fixed = 1024 + 256 + c.xtab_bytes + c.mtab_bytes + static_cast<size_t>(c.rows_cta_max) * c.W * nt * 4;

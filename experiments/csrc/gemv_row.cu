@@ -199,7 +199,7 @@ bool gemv_row_ok(int64_t K) {
 
 int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                     const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
-    const int grid = static_cast<int>(N < kNumSMs ? N : kNumSMs);
+    const int grid = static_cast<int>(N < num_sms() ? N : num_sms());
     const int rows_max = static_cast<int>((N + grid - 1) / grid);
     const int G = static_cast<int>(K / kGroup);
     int NS = 2;

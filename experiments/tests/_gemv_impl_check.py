@@ -1,4 +1,4 @@
-"""Subprocess body for tests/test_gpu_gemv_impls.py (needs a GPU).
+"""Subprocess body for experiments/tests/test_gpu_gemv_impls.py (needs a GPU).
 
 Runs the decode path (n = 1, 2, forced GEMV variant) under whatever
 RELAX_Q4_GEMV_IMPL the parent set and checks it against the oracle.
@@ -9,7 +9,7 @@ import sys
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import oracle  # noqa: E402
 from paper_2311_02103_b200 import inputs, ops  # noqa: E402
@@ -42,7 +42,7 @@ def main():
             torch.cuda.synchronize()
             got = host_bits(y)[0]
             want = w[:, k]
-            assert np.array_equal(got & 0x7FFF, want & 0x7FFF) or np.array_equal(got, want), \
+            assert np.array_equal(got, want), \
                 f"one-hot K={K} N={N} k={k}"
     print("ALL OK")
 

@@ -39,8 +39,18 @@
  *     error nothing is launched and y is untouched ("never a wrong answer",
  *     S:629).
  *   - Kernels are compiled for sm_100a (B200) only.
- *   - Reentrant; the only global state is lazily initialised per-process
- *     kernel attributes and the cuTensorMapEncodeTiled entry point.
+ *   - Reentrant and thread-safe.  The only global state is per device and
+ *     initialised once, under std::call_once / a mutex: the SM count every
+ *     schedule is planned with, and the kernels' function attributes (set on
+ *     each device the process uses).  Tensor maps of the operands are cached
+ *     per host thread (keyed by everything they encode), so steady-state
+ *     host dispatch is a few hash probes, not a driver encode.
+ *   - "Host only" planning calls (relax_plan_workspace*, relax_query_schedule)
+ *     launch nothing; they read the current device's SM count when a device
+ *     is visible (the plan then matches what a call on that device does) and
+ *     assume a B200's 148 SMs otherwise.
+ *   - The library reads no environment variable (experiment knobs exist only
+ *     in the separate experiments build).
  */
 #ifndef RELAX_Q4_H
 #define RELAX_Q4_H
@@ -82,7 +92,7 @@ enum relax_variant {
 #define RELAX_FLAG_SPLIT_WORKSPACE 2u   /* TC split-K through the workspace, not a cluster */
 
 /* Upper-bound workspace plan (lifted workspace P:438-441).
- * Host only, pure: no CUDA call, no allocation.
+ * Host only, pure: no launch, no allocation.
  *   n_max     largest token count the caller will pass (>= 0)
  *   K, N      static shape of the weight
  *   ws_bytes  out: max over n in [1, n_max] of the bytes the automatic
@@ -170,7 +180,11 @@ typedef struct relax_q4_fusion {
 /* Workspace plan of relax_q4_matmul_fused for n <= n_max: the plain plan plus
  * n_max*K*2 bytes for the normalised x when RMSNORM_X is requested and some
  * n <= n_max takes the tensor-core path (the decode GEMV normalises in
- * registers).  Same guarantee and zero-fill contract as relax_plan_workspace.
+ * registers).  The normalised x is written at an offset past the split-K
+ * ticket region (>= 4096 B), so a fused workspace may also serve
+ * relax_q4_matmul_ex calls with RELAX_FLAG_SPLIT_WORKSPACE.  Same guarantee
+ * and zero-fill contract as relax_plan_workspace (the ticket region is left
+ * zero; the normalised-x region is scratch).
  * Errors: as relax_plan_workspace, plus RELAX_ERR_INVALID_ARG for unknown ops
  * bits and RELAX_ERR_UNSUPPORTED_SHAPE when ops != 0 and K % 256 != 0 or
  * (SILU_MUL) N is odd. */

@@ -1,4 +1,7 @@
 /* relax_q4_debug.h -- diagnostics, not part of the operator boundary.
+ * Exported only by the experiments build (build_exp/librelax_q4_exp.so,
+ * `python -m paper_2311_02103_b200.build --experiments`), never by the
+ * product library.
  *
  * With RELAX_Q4_TRACE=1 in the environment, every streamed-GEMV CTA records
  * {launch seq, cta, smid, t_start, t_after_griddepcontrol_wait,

@@ -1,6 +1,12 @@
 """Build librelax_q4.so in-tree with nvcc for sm_100a (B200 only).
 
-    python -m paper_2311_02103_b200.build [--force] [--verbose]
+    python -m paper_2311_02103_b200.build [--force] [--verbose] [--experiments]
+
+--experiments builds a separate library, build_exp/librelax_q4_exp.so, with
+RQ4_EXPERIMENTS defined (csrc/knobs.h): RELAX_Q4_* environment overrides,
+per-CTA timelines, and the measured-slower decode variants of
+experiments/csrc.  Tools load it through RELAX_Q4_LIB; the product library
+reads no environment variable.
 
 Objects go to build/ (git-ignored); the shared library lands next to this
 file so it travels with the repo snapshot to the GPU box.  The CUDA runtime
@@ -24,8 +30,12 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "librelax_q4.so")
 
-SOURCES = ["abi.cpp", "gemv.cu", "gemv_stream.cu", "gemv_mma.cu", "gemv_row.cu", "gemm_tc.cu", "fused.cu"]
-HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh", "fusion.cuh"]
+SOURCES = ["abi.cpp", "device.cpp", "gemv.cu", "gemv_stream.cu", "gemm_tc.cu", "fused.cu"]
+HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh", "fusion.cuh", "knobs.h"]
+EXP_DIR = os.path.join(ROOT, "experiments", "csrc")
+EXP_SOURCES = ["gemv_mma.cu", "gemv_row.cu"]
+BUILD_EXP = os.path.join(ROOT, "build_exp")
+LIB_EXP = os.path.join(BUILD_EXP, "librelax_q4_exp.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -59,16 +69,23 @@ def _flag_changed(obj) -> bool:
     return ("-DRQ4_DEBUG_HANG" in first) != want
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, experiments: bool = False) -> str:
+    bdir = BUILD_EXP if experiments else BUILD
+    lib = LIB_EXP if experiments else LIB
+    os.makedirs(bdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "relax_q4.h")]
+    srcs = [os.path.join(CSRC, f) for f in SOURCES]
+    if experiments:
+        srcs += [os.path.join(EXP_DIR, f) for f in EXP_SOURCES]
     objs, jobs = [], []
-    for src in SOURCES:
-        sp = os.path.join(CSRC, src)
-        op = os.path.join(BUILD, src + ".o")
+    for sp in srcs:
+        src = os.path.basename(sp)
+        op = os.path.join(bdir, src + ".o")
         objs.append(op)
         if force or _stale(op, [sp, *hdrs, __file__]) or _flag_changed(op):
             extra = ["-Xptxas", "-v"] if src.endswith(".cu") else []
+            if experiments:
+                extra += ["-DRQ4_EXPERIMENTS"]
             lang = ["-x", "cu"] if src.endswith(".cu") else ["-x", "c++"]
             jobs.append([nvcc(), *_flags(extra), *lang, "-c", sp, "-o", op])
 
@@ -78,7 +95,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         for cmd, r in ex.map(run, jobs):
-            log = os.path.join(BUILD, os.path.basename(cmd[-1]) + ".log")
+            log = os.path.join(bdir, os.path.basename(cmd[-1]) + ".log")
             with open(log, "w") as f:
                 f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
             if r.returncode != 0:
@@ -86,21 +103,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
             if verbose:
                 sys.stderr.write(r.stderr)
-    if force or jobs or _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+    if force or jobs or _stale(lib, objs):
+        tmp = lib + f".tmp{os.getpid()}"
         cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
                "-Xcompiler", "-fvisibility=hidden"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--experiments", action="store_true")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, experiments=a.experiments))

@@ -11,18 +11,13 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "knobs.h"
 
 namespace rq4 {
 
 int gemv_max_n() {
-    static int v = [] {
-        const char* e = std::getenv("RELAX_Q4_GEMV_MAX_N");
-        if (e && *e) {
-            const int x = std::atoi(e);
-            if (x >= 0) return x;
-        }
-        return 2;   // measured crossover (profiles/sweep_cross_r01.jsonl): DESIGN.md §6
-    }();
+    // measured crossover (profiles/sweep_cross_r01.jsonl): DESIGN.md §6
+    static const int v = [] { const int x = knob_int("RELAX_Q4_GEMV_MAX_N", 2); return x >= 0 ? x : 2; }();
     return v;
 }
 
@@ -34,11 +29,15 @@ static int ctas_per_sm_tc(int bn) { return bn <= 64 ? 2 : 1; }
 // slots / s of them (two CTAs per SM: 93 clusters of 3, not 98).  More tiles
 // than this at split s run a second wave of clusters (4096 x 12288 at n = 8:
 // 96 clusters of 3 took 22.6 us vs 17.1 us at s = 2).  Index s = 1..8.
+// On a device with another SM count the B200 table is scaled by the SM ratio
+// (rounded down), a conservative estimate: GPC placement is not measured there.
 static int64_t cluster_capacity(int bn, int s) {
     static const int64_t two[9] = {0, 296, 148, 93, 71, 56, 45, 37, 33};
     static const int64_t one[9] = {0, 148, 74, 45, 33, 26, 22, 15, 15};
     if (s < 1 || s > 8) return 0;
-    return ctas_per_sm_tc(bn) == 2 ? two[s] : one[s];
+    const int64_t v = ctas_per_sm_tc(bn) == 2 ? two[s] : one[s];
+    const int sms = num_sms();
+    return sms == kB200SMs ? v : v * sms / kB200SMs;
 }
 
 static int choose_bn(int64_t n, int64_t N) {
@@ -61,6 +60,7 @@ static int choose_bn(int64_t n, int64_t N) {
 // it (every BN/split meets the same tolerance).
 static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out) {
     const int64_t tm = (N + kTcBM - 1) / kTcBM;
+    const int64_t sms = num_sms();
     double best = 1e300;
     int bb = 128, bs = 1;
     for (int bn : {128, 256}) {
@@ -68,9 +68,9 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
         const double step = bn == 256 ? 1.3 : 0.92;
         const double fixed = bn == 256 ? 8.0 : 5.7;
         for (int s = 1; s <= 8 && s <= kt; ++s) {
-            if (s > 1 && (tiles > kMaxSplitTiles || tiles * s > kNumSMs)) break;
+            if (s > 1 && (tiles > kMaxSplitTiles || tiles * s > sms)) break;
             if (s > 1 && tiles > cluster_capacity(bn, s)) continue;   // clusters would not all be resident
-            const int64_t waves = (tiles * s + kNumSMs - 1) / kNumSMs;
+            const int64_t waves = (tiles * s + sms - 1) / sms;
             const int ks = (kt + s - 1) / s;
             const double t = static_cast<double>(waves) * (ks * step + fixed) + (s > 1 ? 1.0 : 0.0);
             if (t < best * 0.999) { best = t; bb = bn; bs = s; }
@@ -86,12 +86,11 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
 // in DESIGN.md §6: 2.0 is 3-20% faster on every 7B shape at n = 3..64).
 static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
     (void)n;
-    static double f = [] {
-        const char* e = std::getenv("RELAX_Q4_TC_CTAS_PER_SM");
-        const double v = e ? std::atof(e) : 0.0;
+    static const double f = [] {
+        const double v = knob_double("RELAX_Q4_TC_CTAS_PER_SM", 2.0);
         return v > 0.1 && v <= 4.0 ? v : 2.0;
     }();
-    const double target = f * kNumSMs;
+    const double target = f * num_sms();
     int s = static_cast<int>(target / static_cast<double>(tiles) + 0.5);
     if (s < 1) s = 1;
     if (s > 8) s = 8;            // portable cluster: DSMEM reduction, no workspace
@@ -110,15 +109,16 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
     int v = force_variant;
     if (v == kVariantAuto) {
         const int nt = static_cast<int>(n < kGemvMaxNT ? n : kGemvMaxNT);
-        if (n <= gemv_max_n() && gemv_fits(nt < 1 ? 1 : nt, K)) v = kVariantGemv;
+        const int nt1 = nt < 1 ? 1 : nt;
+        if (n <= gemv_max_n() && (gemv_stream_ok(nt1, K, N) || gemv_fits(nt1, K))) v = kVariantGemv;
         else if (tc_ok) v = kVariantTc;
         else v = kVariantGemv;
     }
     if (v == kVariantGemv) {
         int nt = static_cast<int>(n < kGemvMaxNT ? n : kGemvMaxNT);
         if (nt < 1) nt = 1;
-        while (nt > 1 && !gemv_fits(nt, K)) --nt;
-        if (!gemv_fits(nt, K)) return RELAX_ERR_UNSUPPORTED_SHAPE;
+        while (nt > 1 && !gemv_fits(nt, K) && !(nt <= 2 && gemv_stream_ok(nt, K, N))) --nt;
+        if (!gemv_fits(nt, K) && !gemv_stream_ok(nt, K, N)) return RELAX_ERR_UNSUPPORTED_SHAPE;
         p.variant = kVariantGemv;
         p.nt = nt;
         p.ws_bytes = 0;
@@ -250,6 +250,12 @@ static constexpr uint32_t kOpsAll = RELAX_OP_RMSNORM_X | RELAX_OP_SILU_MUL | REL
 
 static size_t align16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
 
+// Where the tensor path's RMSNORM_X prologue puts the normalised x in a fused
+// call's workspace: after the plan's own bytes and never inside the split-K
+// ticket region [0, kTicketBytes), so a workspace shared with
+// RELAX_FLAG_SPLIT_WORKSPACE calls still finds its tickets zero.
+static size_t fused_xn_offset(size_t plan_bytes) { return align16(plan_bytes > kTicketBytes ? plan_bytes : kTicketBytes); }
+
 static int fused_shape_check(int64_t K, int64_t N, uint32_t ops) {
     if (ops & ~kOpsAll) return RELAX_ERR_INVALID_ARG;
     if (ops != 0 && K % kTcWStageK != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
@@ -294,12 +300,16 @@ static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint
         rc = make_plan(n, K, N, kVariantAuto, sp, 0, &plan, false);
     }
     if (rc != RELAX_OK) return rc;
+    if (plan.variant == kVariantGemv && !gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1)) {
+        // the fused neighbours live in the streamed decode kernel and the
+        // tensor-core kernel only: a shape the former cannot hold takes the latter
+        rc = make_plan(n, K, N, kVariantTc, 0, 0, &plan, false);
+        if (rc != RELAX_OK) return rc;
+    }
     const bool tc_norm = plan.variant == kVariantTc && (ops & RELAX_OP_RMSNORM_X);
-    const size_t xn_off = align16(plan.ws_bytes);
+    const size_t xn_off = fused_xn_offset(plan.ws_bytes);
     const size_t need = tc_norm ? xn_off + xb : plan.ws_bytes;
     if (need > ws_bytes) return RELAX_ERR_WORKSPACE;
-    if (plan.variant == kVariantGemv && !gemv_stream_ok(plan.nt < 2 ? plan.nt : 2, K))
-        return RELAX_ERR_UNSUPPORTED_SHAPE;
     rc = check_device();
     if (rc != RELAX_OK) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -340,7 +350,7 @@ int relax_plan_workspace_fused(int64_t n_max, int64_t K, int64_t N, uint32_t ops
     if (K % rq4::kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
     int rc = rq4::fused_shape_check(K, N, ops);
     if (rc != RELAX_OK) return rc;
-    const int64_t n_cap = static_cast<int64_t>(rq4::kNumSMs) * 256;
+    const int64_t n_cap = static_cast<int64_t>(rq4::num_sms()) * 256;
     const int64_t hi = n_max < n_cap ? n_max : n_cap;
     const bool norm = (ops & RELAX_OP_RMSNORM_X) != 0;
     size_t best = 0;
@@ -348,13 +358,19 @@ int relax_plan_workspace_fused(int64_t n_max, int64_t K, int64_t N, uint32_t ops
         rq4::Plan p;
         rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
         if (rc != RELAX_OK) return rc;
+        // a GEMV plan the streamed decode kernel cannot hold runs on the TC path (fused_impl)
+        if (p.variant == rq4::kVariantGemv &&
+            !rq4::gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1)) {
+            rc = rq4::make_plan(n, K, N, rq4::kVariantTc, 0, 0, &p, false);
+            if (rc != RELAX_OK) return rc;
+        }
         size_t need = p.ws_bytes;
-        if (norm && p.variant == rq4::kVariantTc) need = rq4::align16(p.ws_bytes) + static_cast<size_t>(n) * K * 2;
+        if (norm && p.variant == rq4::kVariantTc) need = rq4::fused_xn_offset(p.ws_bytes) + static_cast<size_t>(n) * K * 2;
         if (need > best) best = need;
     }
     if (norm && n_max > hi) {
         // beyond n_cap every schedule is split-free (no plan bytes) and takes the TC path
-        const size_t need = static_cast<size_t>(n_max) * K * 2;
+        const size_t need = rq4::fused_xn_offset(0) + static_cast<size_t>(n_max) * K * 2;
         if (need > best) best = need;
     }
     *ws_bytes = best;
@@ -372,7 +388,7 @@ int relax_plan_workspace(int64_t n_max, int64_t K, int64_t N, size_t* ws_bytes) 
     if (K % rq4::kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
     // Beyond this n every schedule has >= one full wave of tiles, so split-K
     // (the only workspace user) is 1: the maximum is reached below it.
-    const int64_t n_cap = static_cast<int64_t>(rq4::kNumSMs) * 256;
+    const int64_t n_cap = static_cast<int64_t>(rq4::num_sms()) * 256;
     const int64_t hi = n_max < n_cap ? n_max : n_cap;
     size_t best = 0;
     for (int64_t n = 1; n <= hi; ++n) {

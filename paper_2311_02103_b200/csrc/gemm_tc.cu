@@ -39,6 +39,7 @@
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
 #include "fusion.cuh"
+#include "knobs.h"
 
 namespace rq4 {
 
@@ -56,9 +57,11 @@ struct TcTrace { uint32_t cta, smid, nsub, pad; uint64_t t0, t_end;
                  uint64_t w_prod, x_prod, perm, tr_w, tr_a, mma_a, mma_x, epi;
                  uint64_t t_mma0, t_acc, t_epi;       // globaltimer: first MMA issued, accumulator ready, stores done
                  uint64_t t_cb1, t_cred, t_cb2; };    // cluster split: after 1st barrier, after reduce, after 2nd barrier
+#if RQ4_TRACE
 constexpr int kTcTraceMax = 1 << 14;
 __device__ TcTrace g_tctrace[kTcTraceMax];
 __device__ uint32_t g_tctrace_n;
+#endif
 
 template <bool T>
 __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, uint64_t& acc) {
@@ -214,7 +217,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
     const int nsub = nst * kSubPerStage;
     __shared__ uint64_t tr_slots[14];
     if (threadIdx.x < 14) tr_slots[threadIdx.x] = 0;
-    const uint64_t t_start = a.trace ? globaltimer() : 0;
+    const uint64_t t_start = (RQ4_TRACE && a.trace) ? globaltimer() : 0;
     uint64_t wacc = 0, wacc2 = 0, wacc3 = 0, wacc4 = 0;
 
     pdl_launch_dependents();
@@ -247,7 +250,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             int slot = 0;
             uint32_t ph = 0;
             for (int i = 0; i < nst; ++i, slot = (slot + 1 == kWStages) ? 0 : slot + 1, ph ^= (slot == 0)) {
-                if (a.trace) mbar_wait_t<true>(&w_empty[slot], ph ^ 1, wacc); else mbar_wait(&w_empty[slot], ph ^ 1);
+                if ((RQ4_TRACE && a.trace)) mbar_wait_t<true>(&w_empty[slot], ph ^ 1, wacc); else mbar_wait(&w_empty[slot], ph ^ 1);
                 mbar_arrive_expect_tx(&w_full[slot], kCodesStageBytes + kScalesStageBytes);
                 const int kb = ks0 + i;
                 tma_load_2d(codes_sm + slot * kCodesStageBytes, &tm_w, &w_full[slot],
@@ -264,7 +267,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             int slot = 0;
             uint32_t ph = 0;
             for (int j = 0; j < nsub; ++j, slot = (slot + 1 == XS) ? 0 : slot + 1, ph ^= (slot == 0)) {
-                if (a.trace) mbar_wait_t<true>(&x_empty[slot], ph ^ 1, wacc); else mbar_wait(&x_empty[slot], ph ^ 1);
+                if ((RQ4_TRACE && a.trace)) mbar_wait_t<true>(&x_empty[slot], ph ^ 1, wacc); else mbar_wait(&x_empty[slot], ph ^ 1);
                 mbar_arrive_expect_tx(&x_full[slot], Cfg::kXStageBytes);
                 const int32_t k = (ks0 * kSubPerStage + j) * kTcXStageK;
                 tma_load_2d(x_sm + slot * Cfg::kXStageBytes, &tm_x, &x_full[slot], k,
@@ -280,7 +283,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             int slot = 0;
             uint32_t ph = 0;
             for (int j = 0; j < nsub; ++j, slot = (slot + 1 == XS) ? 0 : slot + 1, ph ^= (slot == 0)) {
-                if (a.trace) mbar_wait_t<true>(&x_full[slot], ph, wacc); else mbar_wait(&x_full[slot], ph);
+                if ((RQ4_TRACE && a.trace)) mbar_wait_t<true>(&x_full[slot], ph, wacc); else mbar_wait(&x_full[slot], ph);
                 uint4* xt = reinterpret_cast<uint4*>(x_sm + slot * Cfg::kXStageBytes);
 #pragma unroll
                 for (int it = 0; it < (BN * 8) / 32; ++it) {
@@ -300,7 +303,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             uint32_t aph = 0, xph = 0;
             for (int j = 0; j < nsub; ++j, as = (as + 1 == AS) ? 0 : as + 1, aph ^= (as == 0),
                                            xs = (xs + 1 == XS) ? 0 : xs + 1, xph ^= (xs == 0)) {
-                if (a.trace) {
+                if ((RQ4_TRACE && a.trace)) {
                     mbar_wait_t<true>(&a_full[as], aph, wacc);
                     mbar_wait_t<true>(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], xph, wacc2);
                 } else {
@@ -308,7 +311,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                     mbar_wait(Cfg::kPermX ? &x_perm[xs] : &x_full[xs], xph);
                 }
                 tc_fence_after();
-                if (a.trace && j == 0) tr_slots[8] = globaltimer();
+                if ((RQ4_TRACE && a.trace) && j == 0) tr_slots[8] = globaltimer();
                 const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * Cfg::kXStageBytes));
 #pragma unroll
                 for (int kk = 0; kk < kTcXStageK / 16; ++kk) {
@@ -334,7 +337,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         int ws = 0, as = h;                 // this warp's sub-blocks: j = h, h+2, h+4, ...
         uint32_t wph = 0, aph = 0;
         for (int i = 0; i < nst; ++i) {
-            if (a.trace) mbar_wait_t<true>(&w_full[ws], wph, wacc); else mbar_wait(&w_full[ws], wph);
+            if ((RQ4_TRACE && a.trace)) mbar_wait_t<true>(&w_full[ws], wph, wacc); else mbar_wait(&w_full[ws], wph);
             const uint8_t* crow = codes_sm + ws * kCodesStageBytes + m * 128;
             const uint32_t* srow = reinterpret_cast<const uint32_t*>(scales_sm + ws * kScalesStageBytes + m * 16);
 #pragma unroll
@@ -356,7 +359,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                         else dequant_word_natural(words[w], s2, v[e][w]);
                     }
                 }
-                if (a.trace) mbar_wait_t<true>(&a_empty[as], aph ^ 1, wacc2); else mbar_wait(&a_empty[as], aph ^ 1);
+                if ((RQ4_TRACE && a.trace)) mbar_wait_t<true>(&a_empty[as], aph ^ 1, wacc2); else mbar_wait(&a_empty[as], aph ^ 1);
                 tc_fence_after();
 #pragma unroll
                 for (int e = 0; e < Cfg::kKH; ++e) {
@@ -365,7 +368,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
                     for (int w = 0; w < 4; ++w)
                         tmem_st_32x32b_x4(acol + 4 * w, v[e][w][0], v[e][w][1], v[e][w][2], v[e][w][3]);
                 }
-                if (a.trace) {
+                if ((RQ4_TRACE && a.trace)) {
                     const uint64_t c0 = clock64();
                     tc_wait_st();
                     wacc3 += clock64() - c0;
@@ -384,7 +387,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         }
     }
 
-    if (a.trace && lane == 0) {
+    if ((RQ4_TRACE && a.trace) && lane == 0) {
         if (warp == 0) tr_slots[0] = wacc;                    // W producer: waits for free W slots
         if (warp == 3) tr_slots[1] = wacc;                    // x producer: waits for free x slots
         if (warp == 2) tr_slots[2] = wacc;                    // permuter: waits for x data
@@ -408,7 +411,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (mine) {
             mbar_wait(acc_full, 0);
             tc_fence_after();
-            if (a.trace && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
+            if ((RQ4_TRACE && a.trace) && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
             pdl_wait();
             // FU = 0: the fp16 tile is staged in the drained rings as
             // [token][row] (rows contiguous, as in y) and written by one TMA
@@ -452,7 +455,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (epi) {
             mbar_wait(acc_full, 0);
             tc_fence_after();
-            if (a.trace && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
+            if ((RQ4_TRACE && a.trace) && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
             pdl_wait();
             const bool split = true;
 #pragma unroll 1
@@ -521,7 +524,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         if (mine) {
             mbar_wait(acc_full, 0);
             tc_fence_after();
-            if (a.trace && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
+            if ((RQ4_TRACE && a.trace) && warp == 4 && lane == 0) tr_slots[9] = globaltimer();
             uint32_t v0[16], v1[16];
             tmem_ld_32x32b_x16(tmem_base + lane_base + cbeg, v0);
             tc_wait_ld();
@@ -540,7 +543,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
         }
         cluster_arrive_release();
         cluster_wait_acquire();
-        if (a.trace && threadIdx.x == 128) tr_slots[11] = globaltimer();
+        if ((RQ4_TRACE && a.trace) && threadIdx.x == 128) tr_slots[11] = globaltimer();
         pdl_wait();
         const uint32_t S = static_cast<uint32_t>(a.split);
         const uint32_t r = cluster_ctarank();
@@ -559,18 +562,19 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             const int64_t rr = m0 + static_cast<int64_t>(e % kTcBM);
             tc_store4<FU>(a, tok, rr, f);
         }
-        if (a.trace && threadIdx.x == 128) tr_slots[12] = globaltimer();
+        if ((RQ4_TRACE && a.trace) && threadIdx.x == 128) tr_slots[12] = globaltimer();
         cluster_arrive_release();
         cluster_wait_acquire();
-        if (a.trace && threadIdx.x == 128) tr_slots[13] = globaltimer();
+        if ((RQ4_TRACE && a.trace) && threadIdx.x == 128) tr_slots[13] = globaltimer();
     }
 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (a.trace && threadIdx.x == 0) tr_slots[10] = globaltimer();
+    if ((RQ4_TRACE && a.trace) && threadIdx.x == 0) tr_slots[10] = globaltimer();
     if (warp == 3) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
-    if (a.trace && threadIdx.x == 0) {
+#if RQ4_TRACE
+    if ((RQ4_TRACE && a.trace) && threadIdx.x == 0) {
         const uint32_t i = atomicAdd(&g_tctrace_n, 1u);
         if (i < kTcTraceMax) {
             TcTrace r;
@@ -584,6 +588,7 @@ tc_q4_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ C
             g_tctrace[i] = r;
         }
     }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -595,14 +600,15 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static EncodeTiledFn get_encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
+    static const EncodeTiledFn fn = []() -> EncodeTiledFn {     // thread-safe one-time lookup
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
+            return reinterpret_cast<EncodeTiledFn>(p);
+        cudaGetLastError();
+        return nullptr;
+    }();
     return fn;
 }
 
@@ -624,13 +630,53 @@ int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void
     return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
 }
 
+// 2-D maps are cached per host thread (direct-mapped, keyed by everything the
+// map encodes: a hit is exactly the map cuTensorMapEncodeTiled would return),
+// so the steady-state dispatch of a call costs a hash probe per operand, not
+// an encode (~0.5 us each).  No locking: thread_local.
+struct MapKey {
+    const void* base;
+    uint64_t inner, outer, row_bytes;
+    uint32_t box_inner, box_outer;
+    int dt, sw;
+    bool operator==(const MapKey& o) const {
+        return base == o.base && inner == o.inner && outer == o.outer && row_bytes == o.row_bytes &&
+               box_inner == o.box_inner && box_outer == o.box_outer && dt == o.dt && sw == o.sw;
+    }
+};
+struct MapEntry { MapKey key; CUtensorMap map; bool valid; };
+constexpr int kMapCacheSlots = 1024;
+
+static size_t map_hash(const MapKey& k) {
+    uint64_t h = reinterpret_cast<uintptr_t>(k.base) * 0x9E3779B97F4A7C15ull;
+    h ^= (k.inner + 0x632BE59BD9B4E019ull + (h << 6) + (h >> 2));
+    h ^= (k.outer * 0xD6E8FEB86659FD93ull + (h << 6) + (h >> 2));
+    h ^= (k.row_bytes + (static_cast<uint64_t>(k.box_inner) << 20) + (static_cast<uint64_t>(k.box_outer) << 40) +
+          (static_cast<uint64_t>(k.dt) << 8) + static_cast<uint64_t>(k.sw) + (h << 6) + (h >> 2));
+    return static_cast<size_t>(h ^ (h >> 29));
+}
+
 static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
                        uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
                        CUtensorMapSwizzle sw) {
+    thread_local MapEntry* cache = nullptr;
+    if (!cache) cache = new MapEntry[kMapCacheSlots]();       // per thread, lives as long as the thread
+    const MapKey key{base, inner, outer, row_bytes, box_inner, box_outer, static_cast<int>(dt), static_cast<int>(sw)};
+    MapEntry& e = cache[map_hash(key) % kMapCacheSlots];
+    if (e.valid && e.key == key) {
+        *m = e.map;
+        return 0;
+    }
     const uint64_t dims[2] = {inner, outer};
     const uint64_t strides[1] = {row_bytes};
     const uint32_t box[2] = {box_inner, box_outer};
-    return make_tensor_map(m, dt, 2, base, dims, strides, box, sw);
+    const int rc = make_tensor_map(m, dt, 2, base, dims, strides, box, sw);
+    if (rc == 0) {
+        e.key = key;
+        e.map = *m;
+        e.valid = true;
+    }
+    return rc;
 }
 
 template <int BN, int FU>
@@ -641,15 +687,9 @@ static int launch_tc_k(const CUtensorMap& mw, const CUtensorMap& ms, const uint1
     int rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, a.K, a.n, a.K * 2, kTcXStageK, BN,
                          CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(tc_q4_kernel<BN, FU>),
-                                        static_cast<int>(Cfg::kSmemBytes));
-        if (e != cudaSuccess) return static_cast<int>(e);
-        e = cudaFuncSetAttribute(tc_q4_kernel<BN, FU>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return static_cast<int>(e);
-        attr_set = true;
-    }
+    const cudaError_t ae = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_kernel<BN, FU>),
+                                               static_cast<int>(Cfg::kSmemBytes), true);
+    if (ae != cudaSuccess) return static_cast<int>(ae);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>((a.N + kTcBM - 1) / kTcBM),
                        static_cast<unsigned>((a.n + BN - 1) / BN), static_cast<unsigned>(a.split));
@@ -685,6 +725,7 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
     return a.ops ? launch_tc_k<BN, 1>(mw, ms, x, a, pdl, stream) : launch_tc_k<BN, 0>(mw, ms, x, a, pdl, stream);
 }
 
+#ifdef RQ4_EXPERIMENTS
 // How many thread-block clusters of `s` CTAs of the BN kernel can be resident
 // at once (cudaOccupancyMaxActiveClusters: GPC placement, not just SM slots --
 // with two CTAs per SM, 96 clusters of 3 do not fit in 296 slots).  Cached;
@@ -692,9 +733,8 @@ static int launch_tc_bn(const CUtensorMap& mw, const CUtensorMap& ms, const uint
 template <int BN>
 static int max_clusters_bn(int s) {
     using Cfg = TcCfg<BN>;
-    if (set_kernel_smem(reinterpret_cast<const void*>(tc_q4_kernel<BN, 0>), static_cast<int>(Cfg::kSmemBytes)) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(tc_q4_kernel<BN, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    if (ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_kernel<BN, 0>), static_cast<int>(Cfg::kSmemBytes),
+                            true) != cudaSuccess) {
         cudaGetLastError();
         return -1;
     }
@@ -744,6 +784,8 @@ int tc_max_active_clusters(int bn, int s) {
     return v;
 }
 
+#endif
+
 // Workspace layout (fixed ticket region first, so one buffer serves every n):
 //   [0, kTicketBytes)            uint32 tickets, one per output tile (<= 1024)
 //   [kTicketBytes, +split*n*N*4) fp32 split-K partials [split][n][N]
@@ -773,7 +815,7 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.res = fu.res;
     a.Nout = (fu.ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
     a.ytma = (a.ops == 0 && plan.split == 1 && N % 8 == 0) ? 1 : 0;
-    static int tr = [] { const char* e = std::getenv("RELAX_Q4_TRACE"); return (e && *e == '1') ? 1 : 0; }();
+    static const int tr = RQ4_TRACE ? knob_int("RELAX_Q4_TRACE", 0) : 0;
     a.trace = tr;
     if (plan.split > 1 && !plan.cluster) {
         a.cnt = static_cast<uint32_t*>(ws);
@@ -791,8 +833,11 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
 
 }  // namespace rq4
 
+#ifdef RQ4_EXPERIMENTS
 extern "C" RELAX_API int relax_debug_tc_max_clusters(int bn, int s) { return rq4::tc_max_active_clusters(bn, s); }
+#endif
 
+#if RQ4_TRACE
 extern "C" RELAX_API int relax_debug_tctrace_read(void* host, size_t max_records, size_t* n_records, int reset) {
     uint32_t n = 0;
     if (cudaMemcpyFromSymbol(&n, rq4::g_tctrace_n, sizeof n) != cudaSuccess) return RELAX_ERR_CUDA;
@@ -806,3 +851,4 @@ extern "C" RELAX_API int relax_debug_tctrace_read(void* host, size_t max_records
     }
     return RELAX_OK;
 }
+#endif

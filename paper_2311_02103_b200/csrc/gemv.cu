@@ -27,6 +27,7 @@
 #include "internal.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
+#include "knobs.h"
 
 namespace rq4 {
 
@@ -50,7 +51,7 @@ __device__ __forceinline__ int xs_slot(int g, int q) { return g * 4 + (q ^ ((g >
 
 template <int NT>
 __global__ void __launch_bounds__(kGemvThreads, kGemvCtasPerSM)
-gemv_q4_kernel(const __grid_constant__ GemvArgs a) {
+q4_decode_generic_kernel(const __grid_constant__ GemvArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint4* xs = reinterpret_cast<uint4*>(smem);
     const int64_t K = a.K, N = a.N;
@@ -204,7 +205,8 @@ static size_t gemv_smem_bytes(int nt, int64_t K, int64_t N, int grid) {
 
 static int gemv_grid(int64_t N) {
     const int64_t RB = (N + kGemvRows - 1) / kGemvRows;
-    return static_cast<int>(RB < kGemvCtasPerSM * kNumSMs ? RB : kGemvCtasPerSM * kNumSMs);
+    const int64_t gmax = static_cast<int64_t>(kGemvCtasPerSM) * num_sms();
+    return static_cast<int>(RB < gmax ? RB : gmax);
 }
 
 bool gemv_fits(int nt, int64_t K) {
@@ -218,12 +220,8 @@ static int launch_gemv_nt(const GemvArgs& a, bool pdl, cudaStream_t stream) {
     const int grid = gemv_grid(a.N);
     const size_t smem = gemv_smem_bytes(NT, a.K, a.N, grid);
     if (smem > 227 * 1024) return static_cast<int>(cudaErrorInvalidConfiguration);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(gemv_q4_kernel<NT>), 227 * 1024);
-        if (e != cudaSuccess) return static_cast<int>(e);
-        attr_set = true;
-    }
+    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(q4_decode_generic_kernel<NT>), 227 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kGemvThreads);
@@ -234,31 +232,29 @@ static int launch_gemv_nt(const GemvArgs& a, bool pdl, cudaStream_t stream) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, gemv_q4_kernel<NT>, a));
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, q4_decode_generic_kernel<NT>, a));
 }
 
 int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                 const uint16_t* s, uint16_t* y, int nt, bool pdl, cudaStream_t stream) {
-    // Decode kernels: the streamed CUDA-core GEMV (gemv_stream.cu, default),
-    // the warp-MMA GEMV (gemv_mma.cu, measured slower so far: DESIGN.md §5.2),
-    // the lane-per-row GEMV (gemv_row.cu), then the generic one below.
-    // RELAX_Q4_GEMV_IMPL=stream|mma|bdmma|row|v1 pins one (tests and measurements;
-    // bdmma = the block-diagonal warp-MMA variant, n = 1 only).
-    static int impl = [] {
-        const char* e = std::getenv("RELAX_Q4_GEMV_IMPL");
-        if (e && std::strcmp(e, "mma") == 0) return 1;
-        if (e && std::strcmp(e, "row") == 0) return 2;
-        if (e && std::strcmp(e, "v1") == 0) return 3;
-        if (e && std::strcmp(e, "bdmma") == 0) return 4;
-        return 0;
-    }();
+    // Decode kernels: the streamed CUDA-core kernel (gemv_stream.cu) for
+    // n <= 2 when the shape fits it, else the generic one below (any K % 32 == 0,
+    // up to 8 tokens per launch).  The experiments build can pin one of the
+    // measured-slower variants kept in experiments/csrc (RELAX_Q4_GEMV_IMPL =
+    // mma | bdmma | row | v1).
+    int impl = 0;
+#ifdef RQ4_EXPERIMENTS
+    static const int impl_env = knob_is("RELAX_Q4_GEMV_IMPL", "mma") ? 1 : knob_is("RELAX_Q4_GEMV_IMPL", "row") ? 2
+                              : knob_is("RELAX_Q4_GEMV_IMPL", "v1") ? 3 : knob_is("RELAX_Q4_GEMV_IMPL", "bdmma") ? 4 : 0;
+    impl = impl_env;
     if (impl == 4 && n == 1 && gemv_bdmma_ok(K, N))
         return launch_gemv_mma(x, n, K, N, w, s, y, pdl, stream, true);
     if (n == 1 && impl == 2 && gemv_row_ok(K))
         return launch_gemv_row(x, n, K, N, w, s, y, pdl, stream);
     if (impl == 1 && nt <= 2 && gemv_mma_ok(n >= 2 ? 2 : 1, K, N))
         return launch_gemv_mma(x, n, K, N, w, s, y, pdl, stream);
-    if (impl <= 1 && nt <= 2 && gemv_stream_ok(nt, K) && N >= 1 && N < (int64_t{1} << 24))
+#endif
+    if (impl <= 1 && nt <= 2 && gemv_stream_ok(nt, K, N))
         return launch_gemv_stream(x, n, K, N, w, s, y, pdl, stream);
     if (nt < 1 || nt > kGemvMaxNT) nt = kGemvMaxNT;
     for (int64_t t0 = 0; t0 < n; t0 += nt) {
@@ -311,7 +307,8 @@ int launch_dequant(const uint32_t* w, const uint16_t* s, int64_t K, int64_t N,
     const int64_t total = N * (K / kGroup);
     if (total == 0) return 0;
     int64_t blocks = (total + 255) / 256;
-    if (blocks > 8 * kNumSMs) blocks = 8 * kNumSMs;
+    const int64_t bmax = 8 * static_cast<int64_t>(num_sms());
+    if (blocks > bmax) blocks = bmax;
     dequant_q4_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(w, s, K, N, out);
     return static_cast<int>(cudaGetLastError());
 }

@@ -32,6 +32,7 @@
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
 #include "fusion.cuh"
+#include "knobs.h"
 
 namespace rq4 {
 
@@ -46,6 +47,7 @@ struct GsArgs {
     int rows_cta_max;
     uint32_t trace_seq;    // 0 = no trace, else launch sequence number
     int prefetch;          // stages the producer issues before griddepcontrol.wait
+    int trigger;           // where the CTA signals launch_dependents (0 start, 1 after x, 2 after stage 0)
     // fused neighbours (include/relax_q4.h RELAX_OP_*)
     uint32_t ops;
     float eps;             // RMSNORM_X
@@ -54,11 +56,14 @@ struct GsArgs {
     int64_t Nout;          // N/2 with SILU_MUL, else N (row stride of y and res)
 };
 
-// ---- optional per-CTA timeline (RELAX_Q4_TRACE=1; include/relax_q4_debug.h)
+// ---- optional per-CTA timeline (experiments build only, RELAX_Q4_TRACE=1;
+// include/relax_q4_debug.h)
+#if RQ4_TRACE
 constexpr int kTraceMax = 1 << 16;                // records
 struct TraceRec { uint32_t seq, cta, smid, pad; uint64_t t0, t_wait, t_first, t_end; };
 __device__ TraceRec g_trace[kTraceMax];
 __device__ uint32_t g_trace_n;
+#endif
 
 __device__ __forceinline__ uint64_t gtime() {
     uint64_t t;
@@ -82,8 +87,7 @@ constexpr int kGsMaxConsumerWarps = 16;   // consumer warps per CTA (one CTA per
 // share of weights while this kernel finishes.
 static size_t gs_ring_budget() {
     static size_t v = [] {
-        const char* e = std::getenv("RELAX_Q4_GS_RING_KB");
-        const int kb = e ? std::atoi(e) : 0;
+        const int kb = knob_int("RELAX_Q4_GS_RING_KB", 112);
         return static_cast<size_t>(kb >= 72 && kb <= 190 ? kb : 112) * 1024;
     }();
     return v;
@@ -133,54 +137,65 @@ __device__ __forceinline__ int reduce_row_of_lane(int lane) {
 //   ZPF = 0: exact centering -- (q - 7) as fp16 via the magic-number unpack
 //            (1 SHF + 4 LOP3 + 4 HFMA2 per 8 codes), then 8 FHFMA;
 //   ZPF = 1: factored zero point -- codes as fp16 subnormals q * 2^-24 (pure
-//            masks, 1 SHF + 4 LOP3 per 8 codes), 8 FHFMA, and per group
-//            2^-24 sum (q - 7) x = acc_e + acc_o / 16, with acc_e started at
-//            m7x = -7 * 2^-24 * sum x; the 2^24 is applied once per output.
+//            masks, 1 SHF + 4 LOP3 per 8 codes), 8 FHFMA into an even-code and an
+//            odd-code chain, and per group 2^-24 sum (q - 7) x =
+//            (acc_e - z_e) + (acc_o - z_o) / 16, where (z_e, z_o) are the SAME two
+//            FHFMA chains run once per kernel with every code = 7.  For an all-7
+//            group the chains repeat z's operations bit for bit, so the group
+//            contributes exactly 0 (r == 0 => y == +-0, reading 10);
+//            the 2^24 is applied once per output.
+template <int ZPF>
+__device__ __forceinline__ void unpack_word(uint32_t word, uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3) {
+    if (ZPF) {
+        const uint32_t v8 = word >> 8;
+        c0 = word & 0x000F000Fu;      // (q0, q4)   * 2^-24
+        c1 = word & 0x00F000F0u;      // (q1, q5)   * 2^-20
+        c2 = v8 & 0x000F000Fu;        // (q2, q6)   * 2^-24
+        c3 = v8 & 0x00F000F0u;        // (q3, q7)   * 2^-20
+    } else {
+        __half2 cc[4];
+        unpack_centered_interleaved(word, cc);
+        c0 = h2_as_u32(cc[0]); c1 = h2_as_u32(cc[1]); c2 = h2_as_u32(cc[2]); c3 = h2_as_u32(cc[3]);
+    }
+}
+
+// The even/odd FHFMA chains of one 32-code group (4 words), NT tokens; the
+// codes are unpacked once and shared by the tokens.
 template <int NT, int ZPF>
-__device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const uint4 (&xr)[NT][4],
-                                        const float (&m7x)[NT], float (&out)[NT]) {
-    const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
-    float ge[NT], go[NT];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) { ge[t] = ZPF ? m7x[t] : 0.f; go[t] = 0.f; }
+__device__ __forceinline__ void group_chains(const uint32_t (&words)[4], const uint4 (&xr)[NT][4],
+                                             float (&e)[NT], float (&o)[NT]) {
 #pragma unroll
     for (int wi = 0; wi < 4; ++wi) {
         uint32_t c0, c1, c2, c3;
-        if (ZPF) {
-            const uint32_t v8 = words[wi] >> 8;
-            c0 = words[wi] & 0x000F000Fu;      // (q0, q4)   * 2^-24
-            c1 = words[wi] & 0x00F000F0u;      // (q1, q5)   * 2^-20
-            c2 = v8 & 0x000F000Fu;             // (q2, q6)   * 2^-24
-            c3 = v8 & 0x00F000F0u;             // (q3, q7)   * 2^-20
-        } else {
-            __half2 cc[4];
-            unpack_centered_interleaved(words[wi], cc);
-            c0 = h2_as_u32(cc[0]); c1 = h2_as_u32(cc[1]); c2 = h2_as_u32(cc[2]); c3 = h2_as_u32(cc[3]);
-        }
+        unpack_word<ZPF>(words[wi], c0, c1, c2, c3);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-            const uint4 X = xr[t][wi];         // (k0,k1) (k2,k3) (k4,k5) (k6,k7)
-            float e = ge[t], o = go[t];
-            e = fhfma(lo16(c0), lo16(X.x), e);   // k0
-            o = fhfma(lo16(c1), hi16(X.x), o);   // k1
-            e = fhfma(lo16(c2), lo16(X.y), e);   // k2
-            o = fhfma(lo16(c3), hi16(X.y), o);   // k3
-            e = fhfma(hi16(c0), lo16(X.z), e);   // k4
-            o = fhfma(hi16(c1), hi16(X.z), o);   // k5
-            e = fhfma(hi16(c2), lo16(X.w), e);   // k6
-            o = fhfma(hi16(c3), hi16(X.w), o);   // k7
-            ge[t] = e;
-            go[t] = o;
+            const uint4 x = xr[t][wi];            // (k0,k1) (k2,k3) (k4,k5) (k6,k7)
+            e[t] = fhfma(lo16(c0), lo16(x.x), e[t]);   // k0
+            o[t] = fhfma(lo16(c1), hi16(x.x), o[t]);   // k1
+            e[t] = fhfma(lo16(c2), lo16(x.y), e[t]);   // k2
+            o[t] = fhfma(lo16(c3), hi16(x.y), o[t]);   // k3
+            e[t] = fhfma(hi16(c0), lo16(x.z), e[t]);   // k4
+            o[t] = fhfma(hi16(c1), hi16(x.z), o[t]);   // k5
+            e[t] = fhfma(hi16(c2), lo16(x.w), e[t]);   // k6
+            o[t] = fhfma(hi16(c3), hi16(x.w), o[t]);   // k7
         }
     }
+}
+
+template <int NT, int ZPF>
+__device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const uint4 (&xr)[NT][4],
+                                        const float (&ze)[NT], const float (&zo)[NT], float (&out)[NT]) {
+    const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+    float e[NT], o[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) { e[t] = 0.f; o[t] = 0.f; }
+    group_chains<NT, ZPF>(words, xr, e, o);
     const float sc = __half2float(__ushort_as_half(sbits));
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-        if (ZPF) {
-            out[t] = sc * fmaf(go[t], 0.0625f, ge[t]);          // units of 2^-24
-        } else {
-            out[t] = sc * (ge[t] + go[t]);
-        }
+        if (ZPF) out[t] = sc * fmaf(o[t] - zo[t], 0.0625f, e[t] - ze[t]);   // units of 2^-24
+        else out[t] = sc * (e[t] + o[t]);
     }
 }
 
@@ -242,7 +257,7 @@ __device__ __forceinline__ void rmsnorm_prologue(uint4 (&xr)[NT][4], const uint4
 // FU = 0: the plain matmul (the fused-neighbour code is compiled out, so the
 // decode kernel of relax_q4_matmul is exactly the unfused one); FU = 1: a.ops.
 template <int NT, int RPW, int ZPF, int FULLG, int MAXT, int FU>
-__global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kernel(const __grid_constant__ GsArgs a) {
+__global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_kernel(const __grid_constant__ GsArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     // NT = 2: the warp index through a shuffle (provably warp-uniform, so the
     // per-warp ring addressing moves to uniform registers): n = 2 decode
@@ -269,7 +284,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
     const uint32_t sb_row = static_cast<uint32_t>(a.K / 16);
     const uint32_t codes_stage = static_cast<uint32_t>(a.RS) * cb_row;
 
-    const uint64_t t_start = a.trace_seq ? gtime() : 0;
+    const uint64_t t_start = (RQ4_TRACE && a.trace_seq) ? gtime() : 0;
     __shared__ uint64_t tr_wait, tr_first;
     __shared__ float rms_red[(FU ? 32 : 1) * NT];        // RMSNorm partials (WK <= 32)
     uint16_t res_pre = 0;                                 // RESIDUAL: prefetched first value
@@ -278,7 +293,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_launch_dependents();
+    if (a.trigger == 0) pdl_launch_dependents();
 
     if (warp == nwc) {
         // ------------------------------------------------ producer (one thread)
@@ -315,9 +330,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
                 gm[q] = gv ? reinterpret_cast<const uint4*>(a.gamma + g * 32)[q] : make_uint4(0u, 0u, 0u, 0u);
         }
         pdl_wait();
-        if (a.trace_seq && warp == 0 && lane == 0) tr_wait = gtime();
+        if (RQ4_TRACE && a.trace_seq && warp == 0 && lane == 0) tr_wait = gtime();
         uint4 xr[NT][4];
-        float m7x[NT];
+        float ze[NT], zo[NT];
 #pragma unroll
         for (int t = 0; t < NT; ++t)
 #pragma unroll
@@ -325,22 +340,13 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
                 xr[t][q] = gv ? reinterpret_cast<const uint4*>(a.x + static_cast<int64_t>(t) * a.K + g * 32)[q]
                               : make_uint4(0u, 0u, 0u, 0u);
         if (ops & RELAX_OP_RMSNORM_X) rmsnorm_prologue<NT>(xr, gm, a, lane, kw, h, nwc, rms_red);
+        // zero-point chains: the per-group FHFMA chains with every code = 7
+        // (exactly what row_dot computes for an all-7 group)
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            float pq[4];              // sum of the group's x (factored zero point), 4 chains
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t w4[4] = {xr[t][q].x, xr[t][q].y, xr[t][q].z, xr[t][q].w};
-                float a2 = 0.f;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float2 f = __half22float2(u32_as_h2(w4[u]));
-                    a2 += f.x + f.y;
-                }
-                pq[q] = a2;
-            }
-            const float sx = (pq[0] + pq[1]) + (pq[2] + pq[3]);
-            m7x[t] = ZPF ? -7.0f * 5.9604644775390625e-08f * sx : 0.f;   // -7 * 2^-24 * sum x
+        for (int t = 0; t < NT; ++t) { ze[t] = 0.f; zo[t] = 0.f; }
+        if (ZPF) {
+            const uint32_t sevens[4] = {0x77777777u, 0x77777777u, 0x77777777u, 0x77777777u};
+            group_chains<NT, 1>(sevens, xr, ze, zo);
         }
         if (ops & RELAX_OP_RESIDUAL) {
             // prefetch this thread's first residual value of the final loop (its
@@ -353,7 +359,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
                 res_pre = a.res[static_cast<int64_t>(t) * a.Nout + col];
             }
         }
-        if (a.trace_seq && warp == 0 && lane == 0) tr_first = gtime();   // x in registers
+        if (RQ4_TRACE && a.trace_seq && warp == 0 && lane == 0) tr_first = gtime();   // x in registers
+        if (a.trigger == 1) pdl_launch_dependents();
         const int rsel = reduce_row_of_lane<RPW>(lane);
         const bool writer = (lane & (32 / RPW - 1)) == 0;
         // Stages (RPW rows each) go round-robin to the H row groups: warp (h, kw)
@@ -375,12 +382,13 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
                 uint16_t sbits = *reinterpret_cast<const uint16_t*>(stage + soff + i * sb_row);
                 if (!FULLG && !gv) sbits = 0;                 // lanes past K: x = 0 and s = 0
                 float o[NT];
-                row_dot<NT, ZPF>(cw, sbits, xr, m7x, o);
+                row_dot<NT, ZPF>(cw, sbits, xr, ze, zo, o);
 #pragma unroll
                 for (int t = 0; t < NT; ++t) acc[t][i] = o[t];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);      // stage bytes fully consumed
+            if (a.trigger == 2) pdl_launch_dependents();
             slot += a.H;
             if (slot >= a.NS) { slot -= a.NS; phase ^= 1; }
 #pragma unroll
@@ -421,6 +429,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
                                     (ops & RELAX_OP_RESIDUAL) ? (pre ? res_pre : a.res[idx]) : uint16_t(0));
         }
     }
+#if RQ4_TRACE
     if (a.trace_seq) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -433,27 +442,19 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) gemv_stream_kerne
             }
         }
     }
+#else
+    (void)t_start;
+#endif
 }
 
 static uint32_t g_launch_seq = 0;
-static bool gs_trace() {
-    static bool v = [] { const char* e = std::getenv("RELAX_Q4_TRACE"); return e && *e == '1'; }();
-    return v;
-}
-
-static int gs_prefetch(int ns) {
-    static int v = [] { const char* e = std::getenv("RELAX_Q4_GS_PREFETCH"); return e ? std::atoi(e) : -1; }();
-    return v < 0 ? (1 << 30) : v;               // default: no limit (the whole ring)
-    (void)ns;
-}
-
-static int gs_zpf() {
-    static int v = [] {
-        const char* e = std::getenv("RELAX_Q4_GEMV_ZPF");
-        return (e && *e == '0') ? 0 : 1;   // factored zero point by default
-    }();
-    return v;
-}
+static bool gs_trace() { return RQ4_TRACE && knob_int("RELAX_Q4_TRACE", 0) == 1; }
+// stages the producer issues before griddepcontrol.wait (default: the whole ring)
+static int gs_prefetch() { static const int v = knob_int("RELAX_Q4_GS_PREFETCH", -1); return v < 0 ? (1 << 30) : v; }
+// where each CTA signals griddepcontrol.launch_dependents (0: at its start)
+static int gs_trigger() { static const int v = knob_int("RELAX_Q4_GS_TRIGGER", 0); return v; }
+// factored zero point (default); 0 = exact centering (experiments build)
+static int gs_zpf() { static const int v = knob_int("RELAX_Q4_GEMV_ZPF", 1); return v; }
 
 static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
     GsConfig c{};
@@ -463,11 +464,12 @@ static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
     if (c.H < 1) c.H = 1;
     const size_t row_bytes = static_cast<size_t>(K / 2 + K / 16);
     c.RPW = 4;
-    if (const char* e = std::getenv("RELAX_Q4_GS_H")) { const int v = std::atoi(e); if (v >= 1 && v * c.WK <= 31) c.H = v; }
-    if (const char* e = std::getenv("RELAX_Q4_GS_RPW")) { const int v = std::atoi(e); if (v == 1 || v == 2 || v == 4 || v == 8) c.RPW = v; }
+    { const int v = knob_int("RELAX_Q4_GS_H", 0); if (v >= 1 && v * c.WK <= 31) c.H = v; }
+    { const int v = knob_int("RELAX_Q4_GS_RPW", 0); if (v == 1 || v == 2 || v == 4 || v == 8) c.RPW = v; }
     int mult = 1;
-    if (const char* e = std::getenv("RELAX_Q4_GS_GRID_MULT")) { const int v = std::atoi(e); if (v >= 1 && v <= 4) mult = v; }
-    c.grid = static_cast<int>(N < kNumSMs * mult ? N : kNumSMs * mult);
+    { const int v = knob_int("RELAX_Q4_GS_GRID_MULT", 1); if (v >= 1 && v <= 4) mult = v; }
+    const int64_t gmax = static_cast<int64_t>(num_sms()) * mult;
+    c.grid = static_cast<int>(N < gmax ? N : gmax);
     const int64_t units = N / pair;                       // rows, or (gate, up) pairs
     c.rows_cta_max = static_cast<int>((units + c.grid - 1) / c.grid) * pair;
     const size_t part_bytes = static_cast<size_t>(c.rows_cta_max) * c.WK * 2 * 4;
@@ -496,10 +498,15 @@ static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
     return c;
 }
 
-bool gemv_stream_ok(int nt, int64_t K) {
-    if (nt < 1 || nt > 2 || K % 256 != 0) return false;   // (and N < 2^24: launch_gemv_stream)
-    const GsConfig c = gs_config(K, kNumSMs);
-    return c.threads <= 1024 && c.smem <= 200 * 1024;
+// Largest dynamic shared memory any decode-stream launch may request (the
+// attribute set once per device and kernel).
+constexpr int kGsSmemMax = 210 * 1024;
+
+bool gemv_stream_ok(int nt, int64_t K, int64_t N, int pair) {
+    if (nt < 1 || nt > 2 || K % 256 != 0 || N < 1 || N >= (int64_t{1} << 24)) return false;
+    if (pair != 1 && (pair != 2 || N % 2 != 0)) return false;
+    const GsConfig c = gs_config(K, N, pair);
+    return c.threads <= 1024 && c.smem <= static_cast<size_t>(kGsSmemMax);
 }
 
 template <int NT, int RPW, int ZPF, int FULLG, int MAXT, int FU>
@@ -514,13 +521,9 @@ static int launch_gs_k(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    auto k = gemv_stream_kernel<NT, RPW, ZPF, FULLG, MAXT, FU>;
-    static bool set = false;
-    if (!set) {
-        cudaError_t e = set_kernel_smem(reinterpret_cast<const void*>(k), 210 * 1024);
-        if (e != cudaSuccess) return static_cast<int>(e);
-        set = true;
-    }
+    auto k = q4_decode_stream_kernel<NT, RPW, ZPF, FULLG, MAXT, FU>;
+    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(k), kGsSmemMax);
+    if (e != cudaSuccess) return static_cast<int>(e);
     return static_cast<int>(cudaLaunchKernelEx(&cfg, k, a));
 }
 
@@ -554,9 +557,10 @@ static int launch_gs_z(const GsArgs& a, const GsConfig& c, bool pdl, cudaStream_
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                        const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream, const Fusion& fu) {
     const int64_t Nout = (fu.ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
-    if (N >= (int64_t{1} << 24)) return static_cast<int>(cudaErrorInvalidValue);   // 32-bit row partition
-    const GsConfig c = gs_config(K, N, (fu.ops & RELAX_OP_SILU_MUL) ? 2 : 1);
-    if (std::getenv("RELAX_Q4_GS_PRINT"))
+    const int pair = (fu.ops & RELAX_OP_SILU_MUL) ? 2 : 1;
+    if (!gemv_stream_ok(n >= 2 ? 2 : 1, K, N, pair)) return static_cast<int>(cudaErrorInvalidValue);
+    const GsConfig c = gs_config(K, N, pair);
+    if (knob_int("RELAX_Q4_GS_PRINT", 0))
         fprintf(stderr, "gemv_stream K=%lld N=%lld WK=%d H=%d RPW=%d RS=%d NS=%d threads=%d grid=%d smem=%zu\n",
                 (long long)K, (long long)N, c.WK, c.H, c.RPW, c.RS, c.NS, c.threads, c.grid, c.smem);
     const int zpf = gs_zpf();
@@ -578,11 +582,17 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.Nout = Nout;
         a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
         a.rows_cta_max = c.rows_cta_max;
-        a.prefetch = gs_prefetch(c.NS);
+        a.prefetch = gs_prefetch();
+        a.trigger = gs_trigger();
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
         int rc;
-        if (cnt == 1) rc = zpf ? launch_gs_z<1, 1>(a, c, pdl, stream) : launch_gs_z<1, 0>(a, c, pdl, stream);
-        else rc = zpf ? launch_gs_z<2, 1>(a, c, pdl, stream) : launch_gs_z<2, 0>(a, c, pdl, stream);
+#ifdef RQ4_EXPERIMENTS
+        if (!zpf) rc = cnt == 1 ? launch_gs_z<1, 0>(a, c, pdl, stream) : launch_gs_z<2, 0>(a, c, pdl, stream);
+        else
+#else
+        (void)zpf;
+#endif
+        rc = cnt == 1 ? launch_gs_z<1, 1>(a, c, pdl, stream) : launch_gs_z<2, 1>(a, c, pdl, stream);
         if (rc != 0) return rc;
     }
     return 0;
@@ -590,6 +600,7 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
 
 }  // namespace rq4
 
+#if RQ4_TRACE
 extern "C" RELAX_API int relax_debug_trace_read(void* host, size_t max_records, size_t* n_records, int reset) {
     uint32_t n = 0;
     if (cudaMemcpyFromSymbol(&n, rq4::g_trace_n, sizeof n) != cudaSuccess) return RELAX_ERR_CUDA;
@@ -603,3 +614,4 @@ extern "C" RELAX_API int relax_debug_trace_read(void* host, size_t max_records, 
     }
     return RELAX_OK;
 }
+#endif

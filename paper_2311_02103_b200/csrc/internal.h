@@ -9,7 +9,14 @@
 namespace rq4 {
 
 constexpr int kGroup = 32;          // codes per fp16 scale (reading 2)
-constexpr int kNumSMs = 148;        // B200; dispatch is planned for this count
+constexpr int kB200SMs = 148;       // B200: the SM count the measured tables were taken on
+
+// SM count of the current device, read once per device (std::call_once) and
+// cached; kB200SMs when no device is visible (host-only planning).  Every
+// schedule decision (grids, split-K, cluster waves) is planned with it.
+int num_sms();
+// cudaGetDevice, or -1 without a device.
+int current_device();
 constexpr int kGemvMaxNT = 8;       // tokens per GEMV launch
 constexpr int kTcBM = 128;          // tcgen05 tile: weight rows (MMA M)
 constexpr int kTcWStageK = 256;     // k per weight (codes+scales) TMA stage
@@ -30,6 +37,11 @@ inline cudaError_t set_kernel_smem(const void* fn, int dyn_bytes) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 static_cast<int>(cudaSharedmemCarveoutMaxShared));
 }
+// set_kernel_smem (plus, with `cluster`, the non-portable cluster-size
+// attribute) once per (device, kernel): function attributes are per device,
+// so a process driving several GPUs sets them on each.  Thread-safe; the
+// steady-state cost is one uncontended lock and a hash lookup.
+cudaError_t ensure_kernel_attrs(const void* fn, int dyn_bytes, bool cluster = false);
 
 // Fused neighbours of one call (include/relax_q4.h RELAX_OP_*); ops == 0: none.
 struct Fusion {
@@ -55,7 +67,6 @@ struct Plan {
 // `force_variant` / `force_split` / `force_bn` override (0 = choose).
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split,
               int force_bn, Plan* out, bool force_ws);
-int tc_max_active_clusters(int bn, int s);   // -1 without a device
 size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split);
 int gemv_max_n();                   // GEMV/TC threshold (env RELAX_Q4_GEMV_MAX_N)
 bool gemv_fits(int nt, int64_t K);
@@ -68,21 +79,27 @@ int launch_gemv(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32
 int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                        const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream,
                        const Fusion& fu = Fusion());
-bool gemv_stream_ok(int nt, int64_t K);
+// Whether the streamed decode kernel can run nt (1, 2) tokens of this shape
+// (K % 256 == 0, N < 2^24, its shared-memory footprint within the attribute);
+// pair = 2 with the SiLU-mul epilogue (CTAs own whole (gate, up) row pairs).
+bool gemv_stream_ok(int nt, int64_t K, int64_t N, int pair = 1);
 // RMSNorm of fp16 rows into `out` (the TC path's RMSNORM_X prologue; the
 // decode GEMV normalises in registers instead).
 int launch_rmsnorm(const uint16_t* x, int64_t n, int64_t K, const uint16_t* gamma, float eps,
                    uint16_t* out, bool pdl, cudaStream_t stream);
+#ifdef RQ4_EXPERIMENTS
+// measured-slower decode variants (experiments/csrc/, experiments build only)
 int launch_gemv_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                     const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream, bool bd = false);
 bool gemv_mma_ok(int nt, int64_t K, int64_t N);
 bool gemv_bdmma_ok(int64_t K, int64_t N);
-int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
-                    const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
-                    CUtensorMapSwizzle sw);
 int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                     const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 bool gemv_row_ok(int64_t K);
+#endif
+int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
+                    const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
+                    CUtensorMapSwizzle sw);
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
               const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
               cudaStream_t stream,

@@ -22,7 +22,9 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "librelax_q4.so")
+# RELAX_Q4_LIB points the binding at another build of the same ABI (the
+# experiments library of `build --experiments`, used by tools/ only).
+LIB_PATH = os.environ.get("RELAX_Q4_LIB") or os.path.join(PKG, "librelax_q4.so")
 
 RELAX_OK = 0
 STATUS = {
@@ -129,13 +131,58 @@ def query_schedule(n: int, K: int, N: int) -> dict:
     return {"variant": name, "tile": t.value, "split_k": s.value, "ws_bytes": int(ws.value)}
 
 
+def _device_of_call():
+    import torch
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _check_tensor(t, name, dtype, shape=None, dev=None):
+    """Every tensor crossing the boundary: CUDA, on the current device, dense
+    row-major, of the ABI's dtype and (where given) shape.  The C-ABI only sees
+    pointers, so a mismatch here would otherwise read or write out of bounds."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if t.dtype not in (dtype if isinstance(dtype, tuple) else (dtype,)):
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_cuda or (dev is not None and t.device != dev):
+        raise ValueError(f"{name}: on {t.device}, expected the current CUDA device {dev}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous (dense row-major)")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
 def _shapes(x, packed_w, scales):
+    import torch
+    dev = _device_of_call()
+    if x.dim() != 2 or packed_w.dim() != 2 or scales.dim() != 2:
+        raise ValueError("x, packed_w and scales must be 2-D")
     n, K = x.shape
     N = packed_w.shape[0]
     if packed_w.shape[1] * 8 != K or scales.shape != (N, K // 32):
         raise ValueError(f"shape mismatch: x {tuple(x.shape)} packed_w {tuple(packed_w.shape)} "
                          f"scales {tuple(scales.shape)}")
+    _check_tensor(x, "x", torch.float16, dev=dev)
+    _check_tensor(packed_w, "packed_w", (torch.int32, torch.uint32), dev=dev)
+    _check_tensor(scales, "scales", torch.float16, dev=dev)
     return n, K, N
+
+
+def _out(y, n, N, x):
+    import torch
+    if y is None:
+        return torch.empty((n, N), dtype=torch.float16, device=x.device)
+    _check_tensor(y, "y", torch.float16, (n, N), dev=x.device)
+    return y
+
+
+def _ws_bytes(ws, dev):
+    if ws is None:
+        return 0
+    import torch
+    _check_tensor(ws, "ws", (torch.uint8, torch.int8, torch.int32, torch.float32), dev=dev)
+    return ws.numel() * ws.element_size()
 
 
 def workspace(n_max: int, K: int, N: int, device=None):
@@ -149,28 +196,25 @@ def workspace(n_max: int, K: int, N: int, device=None):
 
 def q4_matmul(x, packed_w, scales, y=None, ws=None, stream=None):
     """y[n, N] = x[n, K] . dequant(packed_w, scales) via relax_q4_matmul(_ws)."""
-    import torch
     n, K, N = _shapes(x, packed_w, scales)
-    if y is None:
-        y = torch.empty((n, N), dtype=torch.float16, device=x.device)
+    y = _out(y, n, N, x)
+    nb = _ws_bytes(ws, x.device)
     st = _stream_ptr(stream)
     if ws is None:
         rc = lib().relax_q4_matmul(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y), st)
         _check(rc, "relax_q4_matmul")
     else:
         rc = lib().relax_q4_matmul_ws(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y),
-                                      _ptr(ws), ws.numel() * ws.element_size(), st)
+                                      _ptr(ws), nb, st)
         _check(rc, "relax_q4_matmul_ws")
     return y
 
 
 def q4_matmul_ex(x, packed_w, scales, y=None, ws=None, variant=VARIANT_AUTO, split_k=0, bn=0,
                  flags=0, stream=None):
-    import torch
     n, K, N = _shapes(x, packed_w, scales)
-    if y is None:
-        y = torch.empty((n, N), dtype=torch.float16, device=x.device)
-    nb = 0 if ws is None else ws.numel() * ws.element_size()
+    y = _out(y, n, N, x)
+    nb = _ws_bytes(ws, x.device)
     rc = lib().relax_q4_matmul_ex(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y),
                                   _ptr(ws), nb, variant, split_k, bn, flags, _stream_ptr(stream))
     _check(rc, "relax_q4_matmul_ex")
@@ -180,9 +224,16 @@ def q4_matmul_ex(x, packed_w, scales, y=None, ws=None, variant=VARIANT_AUTO, spl
 def q4_dequant(packed_w, scales, K: int, w_out=None, stream=None):
     """w_out[N, K] fp16 = fp16_RNE((q - 7) * s), bit-exact."""
     import torch
+    dev = _device_of_call()
+    if packed_w.dim() != 2 or packed_w.shape[1] * 8 != K:
+        raise ValueError(f"packed_w {tuple(packed_w.shape)} does not hold K = {K} codes per row")
     N = packed_w.shape[0]
+    _check_tensor(packed_w, "packed_w", (torch.int32, torch.uint32), dev=dev)
+    _check_tensor(scales, "scales", torch.float16, (N, K // 32), dev=dev)
     if w_out is None:
         w_out = torch.empty((N, K), dtype=torch.float16, device=packed_w.device)
+    else:
+        _check_tensor(w_out, "w_out", torch.float16, (N, K), dev=dev)
     rc = lib().relax_q4_dequant(_ptr(packed_w), _ptr(scales), K, N, _ptr(w_out), _stream_ptr(stream))
     _check(rc, "relax_q4_dequant")
     return w_out
@@ -204,10 +255,13 @@ def q4_matmul_fused(x, packed_w, scales, y=None, rms_weight=None, rms_eps: float
     ops = (OP_RMSNORM_X if rms_weight is not None else 0) | (OP_SILU_MUL if silu_mul else 0) | \
           (OP_RESIDUAL if residual is not None else 0)
     n_out = N // 2 if silu_mul else N
-    if y is None:
-        y = torch.empty((n, n_out), dtype=torch.float16, device=x.device)
+    y = _out(y, n, n_out, x)
+    if rms_weight is not None:
+        _check_tensor(rms_weight, "rms_weight", torch.float16, (K,), dev=x.device)
+    if residual is not None:
+        _check_tensor(residual, "residual", torch.float16, (n, n_out), dev=x.device)
     fz = Fusion(ops, float(rms_eps), _ptr(rms_weight) or None, _ptr(residual) or None)
-    nb = 0 if ws is None else ws.numel() * ws.element_size()
+    nb = _ws_bytes(ws, x.device)
     rc = lib().relax_q4_matmul_fused(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y), ctypes.byref(fz),
                                      _ptr(ws), nb, _stream_ptr(stream))
     _check(rc, "relax_q4_matmul_fused")

@@ -29,7 +29,11 @@ def host_bits(t):
 
 
 def tol_stats(y_bits, r):
-    y = np.asarray(y_bits, dtype=np.uint16).view(np.float16).astype(np.float64)
+    return tol_stats_f(np.asarray(y_bits, dtype=np.uint16).view(np.float16).astype(np.float64), r)
+
+
+def tol_stats_f(y, r):
+    y = np.asarray(y, dtype=np.float64)
     r = np.asarray(r, dtype=np.float64)
     diff = y - r
     nr = np.linalg.norm(r)
@@ -48,6 +52,18 @@ def assert_within_tol(y_bits, r, what=""):
     if np.all(np.asarray(r) == 0):
         y = np.asarray(y_bits, dtype=np.uint16)
         assert np.all((y & 0x7FFF) == 0), f"{what}: r == 0 but y != 0"
+        return st
+    assert st["rel_f"] <= REL_F, f"{what}: rel_F {st['rel_f']:.3e} > {REL_F}"
+    assert st["max_rel"] <= MAX_REL, f"{what}: max_rel {st['max_rel']:.3e} > {MAX_REL}"
+    return st
+
+
+def assert_within_tol_f(y, r, what=""):
+    """assert_within_tol for outputs already decoded to float64 (y != 0 where r == 0 fails)."""
+    st = tol_stats_f(y, r)
+    assert st["finite"], f"{what}: non-finite output"
+    if np.all(np.asarray(r) == 0):
+        assert np.all(np.asarray(y) == 0), f"{what}: r == 0 but y != 0"
         return st
     assert st["rel_f"] <= REL_F, f"{what}: rel_F {st['rel_f']:.3e} > {REL_F}"
     assert st["max_rel"] <= MAX_REL, f"{what}: max_rel {st['max_rel']:.3e} > {MAX_REL}"

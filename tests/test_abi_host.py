@@ -6,6 +6,9 @@ import ctypes
 import os
 import random
 import re
+import subprocess
+import sys
+import threading
 
 import pytest
 
@@ -40,61 +43,19 @@ def test_status_strings(L):
     assert L.relax_status_str(99).decode() == "RELAX_ERR_UNKNOWN"
 
 
-A = 0x10000          # fake, 16-byte aligned, never dereferenced: validation
-MB = 1 << 20         # precedes every CUDA call
+def run_fake_pointer_checks():
+    """The fake-pointer validation checks (tests/_abi_fake_ptr.py) run in a
+    subprocess with CUDA_VISIBLE_DEVICES="": valid arguments then stop at the
+    device check (RELAX_ERR_DEVICE), so no kernel is ever launched on an
+    unmapped address, even when the suite runs on a GPU box."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_abi_fake_ptr.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
 
 
-def call(L, x=A, n=1, K=256, N=256, w=A + 8 * MB, s=A + 16 * MB, y=A + 24 * MB, ws=0, wsb=0):
-    return L.relax_q4_matmul_ws(x, n, K, N, w, s, y, ws, wsb, None)
-
-
-def test_validation_codes(L):
-    assert call(L, n=-1) == 1
-    assert call(L, K=0) == 1
-    assert call(L, N=0) == 1
-    assert call(L, x=0) == 1
-    assert call(L, y=0) == 1
-    assert call(L, w=0) == 1
-    assert call(L, ws=0, wsb=64) == 1
-    assert call(L, K=100) == 2                       # K % 32 != 0
-    assert call(L, n=0, x=0, y=0) == 0               # n == 0: no-op
-    assert call(L, x=A + 2) == 3                     # misaligned
-    assert call(L, y=A + 8 * MB + 8) == 3
-    assert call(L, y=A + 8 * MB) == 4                # y overlaps packed_w
-    assert call(L, y=A + 100) in (3, 4)
-    assert call(L, y=A + 112) == 4                   # y overlaps x (aligned)
-    assert call(L, ws=A + 24 * MB, wsb=1024) == 4    # workspace overlaps y
-    # valid arguments reach the device check: there is no GPU here
-    assert call(L) == 6
-    assert L.relax_q4_matmul(A, 4, 256, 256, A + 8 * MB, A + 16 * MB, A + 24 * MB, None) == 6
-    assert L.relax_q4_dequant(A, A + MB, 256, 256, A + 8 * MB, None) == 6
-    assert L.relax_q4_dequant(A, A + MB, 256, 256, A, None) == 4
-    assert L.relax_q4_dequant(A, A + MB, 250, 256, A + 8 * MB, None) == 2
-    assert L.relax_q4_dequant(A, A + MB, 256, 0, 0, None) == 0
-
-
-def test_workspace_too_small_is_reported(L):
-    # a forced split-K through the workspace (RELAX_FLAG_SPLIT_WORKSPACE) needs
-    # split * n * N * 4 B + tickets: a 16-byte workspace is too small
-    assert L.relax_q4_matmul_ex(A, 16, 8192, 1024, A + 8 * MB, A + 16 * MB, A + 64 * MB,
-                                A + 128 * MB, 16, 2, 8, 16, 2, None) == 5
-    # the automatic schedule splits K inside a thread-block cluster (DSMEM
-    # reduction): no workspace at all, so a workspace-free call proceeds
-    sched = ops.query_schedule(16, 8192, 1024)
-    assert sched["variant"] == "tc" and sched["split_k"] > 1 and sched["ws_bytes"] == 0
-    assert call(L, n=16, K=8192, N=1024, y=A + 64 * MB) == 6
-    assert ops.query_schedule(16, 4096, 4096)["ws_bytes"] == 0
-    # forced TC on a K that is not a multiple of 256
-    assert L.relax_q4_matmul_ex(A, 16, 4128, 256, A + 8 * MB, A + 16 * MB, A + 64 * MB, 0, 0,
-                                2, 0, 0, 0, None) == 2
-
-
-def test_plan_invalid(L):
-    out = ctypes.c_size_t()
-    assert L.relax_plan_workspace(-1, 256, 256, ctypes.byref(out)) == 1
-    assert L.relax_plan_workspace(8, 0, 256, ctypes.byref(out)) == 1
-    assert L.relax_plan_workspace(8, 256, 256, None) == 1
-    assert L.relax_plan_workspace(8, 100, 256, ctypes.byref(out)) == 2
+def test_validation_and_plans_without_device(L):
+    run_fake_pointer_checks()
 
 
 SHAPES = [(256, 256), (4096, 4096), (4096, 11008), (11008, 4096), (4096, 32000),
@@ -141,46 +102,53 @@ def test_dispatch_shape_specialisation():
         assert s["variant"] == "tc" and s["tile"] >= min(n, 16)
 
 
-# ------------------------------------------------------------- fused neighbours
-def fcall(L, ops_=0, eps=1e-5, gamma=A + 32 * MB, res=0, x=A, n=1, K=256, N=256, w=A + 8 * MB,
-          s=A + 16 * MB, y=A + 24 * MB, ws=0, wsb=0):
-    fz = ops.Fusion(ops_, eps, gamma or None, res or None)
-    return L.relax_q4_matmul_fused(x, n, K, N, w, s, y, ctypes.byref(fz), ws, wsb, None)
-
-
-def test_fused_validation_codes(L):
-    R, S, Q = ops.OP_RMSNORM_X, ops.OP_SILU_MUL, ops.OP_RESIDUAL
-    assert fcall(L, ops_=8) == 1                                  # unknown op bit
-    assert fcall(L, ops_=R, K=96) == 2                            # fused ops need K % 256 == 0
-    assert fcall(L, ops_=S, N=255) == 2                           # SiLU-mul pairs need N even
-    assert fcall(L, ops_=R, gamma=0) == 1                         # RMSNorm without gamma
-    assert fcall(L, ops_=R, eps=-1.0) == 1
-    assert fcall(L, ops_=R, eps=float("nan")) == 1
-    assert fcall(L, ops_=Q, res=0) == 1                           # residual without pointer
-    assert fcall(L, ops_=R, gamma=A + 32 * MB + 8) == 3           # misaligned gamma
-    assert fcall(L, ops_=Q, res=A + 24 * MB + 16) == 4            # residual partially overlapping y
-    assert fcall(L, ops_=R, gamma=A + 24 * MB) == 4               # y overlapping gamma
-    assert fcall(L, ops_=Q, res=A + 24 * MB) == 6                 # in-place residual (res == y) is legal
-    assert fcall(L, ops_=R | S | Q, res=A + 40 * MB) == 6         # valid: reaches the device check
-    assert fcall(L, ops_=R, n=64) == 5                            # TC path normalises into the workspace
-    assert fcall(L, ops_=R, n=0, x=0, y=0) == 0                   # n == 0: no-op
-    assert fcall(L, ops_=0, K=100) == 2                           # ops == 0: plain matmul validation
-
-
-def test_fused_workspace_plan(L):
+def test_fused_workspace_plan_host(L):
     R = ops.OP_RMSNORM_X
     assert ops.plan_workspace_fused(2, 4096, 4096, R) == 0        # decode GEMV normalises in registers
     assert ops.plan_workspace_fused(64, 4096, 4096, 0) == ops.plan_workspace(64, 4096, 4096)
-    assert ops.plan_workspace_fused(64, 4096, 4096, R) >= 64 * 4096 * 2
+    assert ops.plan_workspace_fused(64, 4096, 4096, R) >= 64 * 4096 * 2 + 4096
     assert ops.plan_workspace_fused(100000, 4096, 4096, R) >= 100000 * 4096 * 2
     with pytest.raises(ops.RelaxError):
         ops.plan_workspace_fused(4, 4096, 4095 * 2 + 1, ops.OP_SILU_MUL)
-    # plan soundness: every n <= n_max fits
-    for n_max in (1, 3, 17, 300):
-        nb = ops.plan_workspace_fused(n_max, 4096, 11008, R)
-        for n in range(1, n_max + 1, max(1, n_max // 7)):
-            assert fcall(L, ops_=R, n=n, K=4096, N=11008, w=A + 64 * MB, s=A + 128 * MB, y=A + 256 * MB,
-                         gamma=A + 512 * MB, ws=A + 1024 * MB, wsb=nb) == 6
+
+
+def test_large_n_plans():
+    """Very wide outputs (a 405B-class lm_head, 256 k vocabularies) plan a
+    schedule whose decode kernel fits its shared memory: the
+    streamed kernel when it fits, else the generic GEMV."""
+    for K, N in ((16384, 128256), (8192, 256000), (4096, 32000), (28672, 8192)):
+        for n in (1, 2):
+            s = ops.query_schedule(n, K, N)
+            assert s["variant"] == "gemv" and s["ws_bytes"] == 0, (K, N, s)
+
+
+def test_host_calls_thread_safe(L):
+    """Reentrancy of the host side: several threads plan, query and validate
+    concurrently (ctypes drops the GIL) and agree with a serial run."""
+    shapes = [(4096, 4096), (4096, 11008), (8192, 1024), (5120, 13824)]
+    want = {(n, K, N): (ops.query_schedule(n, K, N), ops.plan_workspace(n, K, N))
+            for K, N in shapes for n in (1, 3, 17, 64, 200, 1000)}
+    errors = []
+
+    def worker(seed):
+        rng = random.Random(seed)
+        try:
+            for _ in range(300):
+                key = rng.choice(list(want))
+                got = (ops.query_schedule(*key), ops.plan_workspace(*key))
+                if got != want[key]:
+                    errors.append((key, got))
+                if L.relax_q4_matmul(0x10002, 1, 256, 256, 0x900000, 0x1100000, 0x1900000, None) != 3:
+                    errors.append("misaligned not reported")
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors[:3]
 
 
 @pytest.mark.parametrize("n", [3, 8, 16, 32, 64, 128, 512])

@@ -87,3 +87,19 @@ def test_interleave_rows():
     b = -np.arange(6).reshape(3, 2)
     out = fo.interleave_rows(a, b)
     assert out.tolist() == [[0, 1], [0, -1], [2, 3], [-2, -3], [4, 5], [-4, -5]]
+
+
+def test_residual_rounds_v_to_fp16_first():
+    """Reading 18: the residual adds the fp16 OUTPUT of the matmul (the
+    unfused chain stores it): r = 1 + 2^-12 is below half an fp16 ulp of 1
+    (2^-11), so it contributes exactly 1.0; r = 1 + 3 * 2^-12 rounds up to
+    1 + 2^-10; ties go to even (1 + 2^-11 -> 1.0, 1 + 3 * 2^-11 -> 1 + 2^-9)."""
+    res = f16bits(np.array([[0.5, 0.5, 0.5, 0.5]]))
+    r = np.array([[1.0 + 2.0 ** -12, 1.0 + 3 * 2.0 ** -12, 1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11]])
+    y = fo.residual(r, res)
+    assert y.tolist() == [[1.5, 1.5 + 2.0 ** -10, 1.5, 1.5 + 2.0 ** -9]]
+    # the fp16 bits path gives the same value as the float path
+    vb = f16bits(np.array([[1.0, 1.0 + 2.0 ** -10]]))
+    assert fo.residual(vb, res[:, :2], v_is_bits=True).tolist() == [[1.5, 1.5 + 2.0 ** -10]]
+    # overflow of v itself: fp16(70000) = inf, not 70000
+    assert np.isinf(fo.residual(np.array([[70000.0]]), f16bits(np.array([[-1.0]])))[0, 0])

@@ -5,6 +5,7 @@ cudaOccupancyMaxActiveClusters through relax_debug_tc_max_clusters.
     python tools/tc_clusters.py
 """
 import os
+os.environ.setdefault("RELAX_Q4_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build_exp", "librelax_q4_exp.so"))  # traces: experiments build
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

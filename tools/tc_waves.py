@@ -17,6 +17,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("RELAX_Q4_TRACE", "1")
+os.environ.setdefault("RELAX_Q4_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build_exp", "librelax_q4_exp.so"))  # traces: experiments build
 from paper_2311_02103_b200 import inputs, ops  # noqa: E402
 
 REC = np.dtype([("cta", "<u4"), ("smid", "<u4"), ("nsub", "<u4"), ("pad", "<u4"), ("t0", "<u8"), ("te", "<u8")]
