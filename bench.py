@@ -2,8 +2,8 @@
 """bench.py -- Llama-2 layer-set throughput of the fused q4f16 dequant-matmul.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload llama2-7b-decode|llama2-13b-decode|llama2-7b-prefill|...]
-                    [--n TOKENS]
+                    [--workload llama2-7b-decode|llama2-13b-decode|llama2-70b-decode|llama2-7b-prefill|...]
+                    [--n TOKENS] [--fused] [--replicas] [--tp-shard P] [--block fused|unfused]
 
 A step = one pass of the whole hot path over one batch: every linear layer of
 the model (32 x {q,k,v,o,gate,up,down} + lm_head for 7B) applied to n tokens,
@@ -13,14 +13,22 @@ layer, so the 3.7 GB working set streams from HBM -- far larger than the
 (programmatic dependent launch between consecutive kernels) and replayed.
 
 Default workload = BASELINE.json config 2, "Llama-2-7B decode weight set at
-n=1 on 1 B200"; value = tokens/s (one token per step per GPU).  With N>1
-(torchrun) every rank decodes its own independent token stream on its own
-GPU (replicas, no collective on the data path): value = all ranks' tokens /
-max-over-ranks time, "scaling": "weak".
+n=1 on 1 B200"; value = tokens/s.
+
+--gpus N (N > 1): re-launches itself under torch.distributed.run (one rank per
+GPU, NCCL, 127.0.0.1) unless already under torchrun.  With N > 1 ranks the
+default is Megatron tensor parallelism of the layer set (north_star item 3,
+SURVEY §8(e)): q/k/v and gate/up stacked and column-split, o and down
+row-split with an fp32 all_reduce of the partial y, the lm_head column-split
+with its logits all-gathered -- paper_2311_02103_b200/tp.py, the code the
+gloo and NCCL tests check; one token stream, "scaling": "strong".
+--replicas instead runs N independent decode replicas (no collective,
+"scaling": "weak").
 
 --impl reference times the CPU oracle (oracle/, the only reference that
-exists: the paper ships no code) on the host cores, same metric and config,
-each step a bounded sample (one transformer layer + lm_head, extrapolated).
+exists: the paper ships no code) on the host cores, same metric and config;
+each step is a bounded sample (one linear of layer 0, full outputs, rotating
+through the seven; extrapolated by multiply-accumulate count to the layer set).
 """
 from __future__ import annotations
 
@@ -54,45 +62,28 @@ def load_peaks():
             "src": "fallback"}
 
 
-def tp_shard(name: str, K: int, N: int, p: int):
-    """Rank-local shape of one linear under Megatron tensor parallelism of
-    degree p: q/k/v, gate/up and lm_head split their output
-    features (column split), o and down split their reduction dim (row split,
-    followed by an all_reduce of the partial y)."""
-    if p == 1:
-        return K, N
-    if name in ("o", "down"):
-        assert K % p == 0
-        return K // p, N
-    assert N % p == 0
-    return K, N // p
-
-
 def layer_set(workload: str, fused: bool = False, tp: int = 1):
     """The linears of one token.  fused=True stacks the rows of q/k/v and of
     gate/up (the NK layout makes that a concatenation) into one call each --
     same weights, same bytes, 4 dependent calls per layer instead of 7.
-    tp=p gives rank 0's shard shapes of a p-way tensor-parallel layer set."""
+    tp=p gives the rank-local shard shapes of a p-way Megatron split
+    (tp.shard_shape: column-parallel q/k/v, gate/up, lm_head; row-parallel
+    o, down)."""
+    from paper_2311_02103_b200 import tp as tpm
     model = workload.rsplit("-", 1)[0]          # llama2-7b-decode -> llama2-7b
     spec = inputs.LLAMA_SETS[model]
-    if tp > 1:
-        spec = dict(spec)
-        spec["mats"] = [(nm, *tp_shard(nm, K, N, tp)) for nm, K, N in spec["mats"]]
-        spec["lm_head"] = tp_shard("lm_head", *spec["lm_head"], tp)
     mats = []
     for li in range(spec["layers"]):
         if fused:
             d = {name: (K, N) for name, K, N in spec["mats"]}
             K = d["q"][0]
-            mats.append((f"L{li}.qkv", K, d["q"][1] + d["k"][1] + d["v"][1]))
-            mats.append((f"L{li}.o", *d["o"]))
-            mats.append((f"L{li}.gate_up", K, d["gate"][1] + d["up"][1]))
-            mats.append((f"L{li}.down", *d["down"]))
+            layer = [("qkv", K, d["q"][1] + d["k"][1] + d["v"][1]), ("o", *d["o"]),
+                     ("gate_up", K, d["gate"][1] + d["up"][1]), ("down", *d["down"])]
         else:
-            for name, K, N in spec["mats"]:
-                mats.append((f"L{li}.{name}", K, N))
-    K, N = spec["lm_head"]
-    mats.append(("lm_head", K, N))
+            layer = list(spec["mats"])
+        for name, K, N in layer:
+            mats.append((f"L{li}.{name}", *tpm.shard_shape(name, K, N, tp)))
+    mats.append(("lm_head", *tpm.shard_shape("lm_head", *spec["lm_head"], tp)))
     return model, mats
 
 
@@ -232,23 +223,29 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2311_02103_b200 import ops
+    from paper_2311_02103_b200 import tp as tpm
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     ops.lib()
-    tp_world = world if args.tp else 1
-    if args.tp and args.tp_shard > 1:
-        raise SystemExit("--tp (real tensor parallelism over the ranks) and --tp-shard are exclusive")
-    model, mats = layer_set(args.workload, args.fused, args.tp_shard if not args.tp else tp_world)
+    tp_mode = args.tp and dist.is_initialized()
+    tp_world = world if tp_mode else 1
+    if tp_mode and args.tp_shard > 1:
+        raise SystemExit("tensor parallelism over the ranks and --tp-shard are exclusive")
+    if tp_mode and args.block != "none":
+        raise SystemExit("--block runs on one GPU (or as --replicas)")
+    # TP runs the Megatron layout: q/k/v and gate/up stacked, as Megatron does
+    fused = args.fused or tp_mode
+    model, mats = layer_set(args.workload, fused, tp_world if tp_mode else args.tp_shard)
     n = args.n
     t_gen = time.time()
-    # One realistic weight per distinct shape (seed 1000*config + index),
-    # copied into a distinct HBM buffer per layer.
+    # One realistic weight per distinct shape (seed 1000*config + index; each
+    # TP rank its own shard values), copied into a distinct HBM buffer per layer.
     cfg_id = {"llama2-7b": 2, "llama2-13b": 4, "llama2-70b": 5}[model]
     shapes = sorted({(K, N) for _, K, N in mats})
     proto = {}
     for i, (K, N) in enumerate(shapes):
-        pk, sc = inputs.realistic_weights(1000 * cfg_id + i, K, N)
+        pk, sc = inputs.realistic_weights(1000 * cfg_id + i + 100 * (rank if tp_mode else 0), K, N)
         proto[(K, N)] = (torch.from_numpy(pk.view(np.int32)).to(dev),
                          torch.from_numpy(sc.view(np.float16)).to(dev))
     weights = []
@@ -274,19 +271,30 @@ def run_ours(args, rank, world, local_rank):
         for (name, K, N), (pk, sc), y in zip(mats, weights, ys):
             ops.q4_matmul_ex(xs[K], pk, sc, y=y, ws=wss[(K, N)], flags=flags, stream=stream)
 
+    out_last = lambda: ys[-1]          # noqa: E731  the step's result (logits)
     block_io = None
     if args.block != "none":
         step, block_io = block_step(args, mats, weights, n, dev, stream)
-    elif args.tp and dist.is_initialized():
-        # Megatron TP over the NCCL group: q/k/v, gate/up and
-        # lm_head column-split (no exchange), o and down row-split followed by
-        # an all_reduce of the partial y (fp16, reading 14).
+    elif tp_mode:
+        # Megatron TP over the NCCL group through tp.py -- the
+        # code tests/test_tp_gloo.py and tests/test_gpu_tp.py check: column-
+        # parallel qkv / gate_up (no exchange), row-parallel o / down (fp32
+        # all_reduce of the fp16 partials, reading 14), column-parallel
+        # lm_head with its logits all-gathered to [n, vocab].
+        def mm_for(K, N):
+            ws = wss[(K, N)]
+            return lambda x, pk, sc: ops.q4_matmul_ex(x, pk, sc, ws=ws, flags=flags, stream=stream)
+
+        lin = [tpm.megatron_linear(name.split(".")[-1], pk, sc, matmul=mm_for(K, N))
+               for (name, K, N), (pk, sc) in zip(mats, weights)]
+        tp_out = [None]
+
         def step():
-            for (name, K, N), (pk, sc), y in zip(mats, weights, ys):
-                ops.q4_matmul_ex(xs[K], pk, sc, y=y, ws=wss[(K, N)], flags=flags, stream=stream)
-                if name.split(".")[-1] in ("o", "down"):
-                    with torch.cuda.stream(stream):
-                        dist.all_reduce(y, op=dist.ReduceOp.SUM)
+            with torch.cuda.stream(stream):
+                for (name, K, N), f in zip(mats, lin):
+                    tp_out[0] = f(xs[K])
+
+        out_last = lambda: tp_out[0]   # noqa: E731
 
     # capture the step
     torch.cuda.synchronize()
@@ -295,16 +303,9 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     graph = None
     if not args.no_graph:
-        try:
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=stream):
-                step()
-        except RuntimeError as e:                # e.g. a collective that cannot be captured
-            if not (args.tp and dist.is_initialized()):
-                raise
-            print(f"graph capture failed ({e}); timing eagerly", file=sys.stderr)
-            torch.cuda.synchronize()
-            graph = None
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
 
     def replay():
         if graph is not None:
@@ -333,43 +334,60 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     ck = clocks.stop()
     ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        return float(t.item())
+
+    ms = max_over_ranks(ms)
+    if world > 1:
         dist.barrier()
 
-    # ---- end to end through the public API: pinned host x in, logits out
+    # ---- end to end through the public API: pinned host x in, logits out,
+    # (a) replaying the captured step, (b) eagerly -- every C-ABI call
+    # dispatched from Python each step (binding + host dispatch included).
     x_host = torch.from_numpy(inputs.activations(99, n, mats[0][1]).view(np.float16)).pin_memory()
-    x_dev, y_last = (xs[mats[0][1]], ys[-1]) if block_io is None else block_io
+    x_dev = xs[mats[0][1]] if block_io is None else block_io[0]
+    y_last = out_last() if block_io is None else block_io[1]
     out_host = torch.empty(y_last.shape, dtype=torch.float16).pin_memory()
-    with torch.cuda.stream(stream):
-        for _ in range(2):
-            x_dev.copy_(x_host, non_blocking=True)
-            replay()
-            out_host.copy_(y_last, non_blocking=True)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(args.steps):
-            x_dev.copy_(x_host, non_blocking=True)
-            replay()
-            out_host.copy_(y_last, non_blocking=True)
-        e1.record(stream)
-    torch.cuda.synchronize()
-    ms_e2e = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+
+    def e2e_run(fn, steps):
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                x_dev.copy_(x_host, non_blocking=True)
+                fn()
+                out_host.copy_(out_last() if block_io is None else block_io[1], non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                x_dev.copy_(x_host, non_blocking=True)
+                fn()
+                out_host.copy_(out_last() if block_io is None else block_io[1], non_blocking=True)
+            e1.record(stream)
+        t_host = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1)), t_host
+
+    ms_e2e, _ = e2e_run(replay, args.steps)
+
+    def eager_step():
+        with torch.cuda.stream(stream):
+            step()
+
+    ms_eager, host_eager_s = e2e_run(eager_step, args.steps)
 
     bytes_step, flops_step = algorithmic(mats, n)
     ms_step = ms / args.steps
-    streams = 1 if args.tp else world            # TP: the ranks decode one stream together
+    streams = 1 if tp_mode else world            # TP: the ranks decode one stream together
     tok_s = streams * n * args.steps / (ms / 1e3)
-    gbs = bytes_step / (ms_step / 1e3) / 1e9
+    gbs = bytes_step / (ms_step / 1e3) / 1e9      # per GPU (each rank streams its own shards)
     tflops = flops_step / (ms_step / 1e3) / 1e12
     peaks = load_peaks()
     tc = n >= 128
@@ -380,15 +398,18 @@ def run_ours(args, rank, world, local_rank):
     else:
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / peaks["hbm_gbs"], 4), "peak_src": f"{peaks['src']} hbm copy"}
-    label = (args.workload + ("-fused-qkv-gateup" if args.fused else "")
+    label = (args.workload + ("-fused-qkv-gateup" if fused else "")
              + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else "")
+             + (f"-megatron-tp{tp_world}" if tp_mode else "")
              + (f"-block-{args.block}" if args.block != "none" else ""))
     roof["traffic"] = traffic_per_launch(label, n)
     roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
-    roof["kernel"] = "gemv_stream_kernel (streamed GEMV)" if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" \
-        else "tc_q4_kernel"
+    roof["kernel"] = ("q4_decode_stream_kernel (streamed decode GEMV)"
+                      if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" else "tc_q4_kernel")
     roof["per"] = "average over all launches of the step (every launch is this kernel family)"
-    launches = sum(1 if sched[f"{K}x{N}"]["variant"] == "tc" else -(-n // 8) for _, K, N in mats)
+    if tp_mode:
+        roof["per"] += "; per GPU: each rank streams its own shards"
+    launches = sum(1 if sched[f"{K}x{N}"]["variant"] == "tc" else -(-n // 2) for _, K, N in mats)
     res = {
         "metric": METRIC,
         "value": round(tok_s, 2),
@@ -398,21 +419,26 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 5),
         "higher_is_better": True,
-        "scaling": "strong" if args.tp else "weak",
+        "scaling": "strong" if tp_mode else "weak",
         "vs_baseline": None,
         "dtype": "q4f16 (int4 codes x fp16 -> fp32 accumulate, fp16 out)",
         "data": "synthetic (seeded realistic q4f16 weights, N(0,1) fp16 x)",
         "config": {"workload": label,
                    "model": model, "tokens_per_step": n,
                    "layers_linears": len(mats), "weight_bytes": int(sum(inputs.q4_bytes(K, N) for _, K, N in mats)),
-                   "parallelism": (f"tp{world}" if args.tp else f"replicas{world}") if world > 1 else "single",
+                   "parallelism": (f"megatron-tp{world}" if tp_mode else f"replicas{world}") if world > 1 else "single",
                    "l2": "not flushed: per-step working set %.2f GB >> 126 MB L2" % (bytes_step / 1e9),
                    "graph": graph is not None, "pdl": not args.no_pdl, "schedule": sched},
         "hbm_gbs": round(gbs, 1),
         "tflops": round(tflops, 3),
         "roofline": roof,
         "e2e": {"value": round(streams * n * args.steps / (ms_e2e / 1e3), 2), "unit": "tok/s",
-                "h2d_bytes_per_step": int(x_host.numel() * 2), "d2h_bytes_per_step": int(out_host.numel() * 2)},
+                "h2d_bytes_per_step": int(x_host.numel() * 2), "d2h_bytes_per_step": int(out_host.numel() * 2),
+                "how": "public API, captured step replayed; H2D of x and D2H of the logits inside the timed region"},
+        "e2e_eager": {"value": round(streams * n * args.steps / (ms_eager / 1e3), 2), "unit": "tok/s",
+                      "host_us_per_step": round(1e6 * host_eager_s / args.steps, 1),
+                      "how": "every C-ABI call dispatched from Python each step (ctypes binding + host dispatch), "
+                             "same copies"},
         "gpu_launches": launches * args.steps,
         "clocks": ck,
         "setup_s": round(t_gen, 1),
@@ -430,54 +456,89 @@ def traffic_per_launch(workload, n):
 
 
 # --------------------------------------------------------------------- oracle
-def oracle_sample(workload, n):
-    """Oracle time for one transformer layer + lm_head at n tokens on all host
-    cores; extrapolated to the full layer set.  Returns (tok/s, info)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(workload, n, nthreads=None, which=None):
+    """Time the oracle (oracle.matmul_f64, full outputs) on a bounded sample of
+    one step's workload: layer 0's linears at n tokens -- all seven, or only
+    linear `which` (the reference arm rotates through them, one per step).
+    Returns (extrapolated tok/s, measured sample seconds, info): the sample's
+    multiply-accumulates are a known fraction of the layer set's, so
+    t_step = t_sample * MAC(set) / MAC(sample)."""
     import oracle
     model, mats = layer_set(workload)
-    spec = inputs.LLAMA_SETS[model]
-    layer = [(nm, K, N) for nm, K, N in mats if nm.startswith("L0.")]
-    head = [m for m in mats if m[0] == "lm_head"]
-    cores = oracle.max_threads()
+    layer0 = [(nm, K, N) for nm, K, N in mats if nm.startswith("L0.")]
+    sample = layer0 if which is None else [layer0[which % len(layer0)]]
+    # all host cores the process may run on (torchrun sets OMP_NUM_THREADS=1)
+    cores = nthreads or len(os.sched_getaffinity(0))
     gen = {}
-    for nm, K, N in layer + head:
+    for nm, K, N in sample:
         if (K, N) not in gen:
             gen[(K, N)] = inputs.stress_weights(5 + K + N, K, N)
-    xs = {K: inputs.activations(7 + n + K, n, K) for _, K, _ in layer + head}
+    xs = {K: inputs.activations(7 + n + K, n, K) for _, K, _ in sample}
     t0 = time.perf_counter()
-    for nm, K, N in layer:
+    for nm, K, N in sample:
         pk, sc = gen[(K, N)]
         oracle.matmul_f64(xs[K], pk, sc, K, N, nthreads=cores)
-    t_layer = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    for nm, K, N in head:
-        pk, sc = gen[(K, N)]
-        oracle.matmul_f64(xs[K], pk, sc, K, N, nthreads=cores)
-    t_head = time.perf_counter() - t0
-    t_tok = spec["layers"] * t_layer + t_head
-    return n / t_tok, {"cores": cores, "sample_s": round(t_layer + t_head, 3),
-                       "sample": f"oracle (fp64, {cores} threads) on 1 of {spec['layers']} layers "
-                                 f"(7 linears) + lm_head at n={n}; extrapolated x{spec['layers']} layers"}
+    t_sample = time.perf_counter() - t0
+    mac_sample = sum(n * K * N for _, K, N in sample)
+    mac_step = sum(n * K * N for _, K, N in mats)
+    t_step = t_sample * mac_step / mac_sample
+    what = "layer 0's 7 linears" if which is None else "one linear of layer 0 per step (rotating q..down)"
+    return n / t_step, t_sample, {"cores": cores,
+                                  "sample": f"oracle (fp64, {cores} threads) on {what} at n={n}, full outputs; "
+                                            f"extrapolated by multiply-accumulate count to the "
+                                            f"{len(mats)}-linear layer set"}
 
 
 def run_reference(args):
-    val, info = oracle_sample(args.workload, args.n)
-    # steps: each step re-times a bounded sample; keep it to a few minutes total
-    vals = [val]
-    for _ in range(max(0, min(args.steps, 3) - 1)):
-        v, info = oracle_sample(args.workload, args.n)
+    """The reference arm: the oracle, as it stands, on the host cores.  Each of
+    the W warm-up and K timed steps times one bounded sample (one linear of
+    layer 0, rotating); ms_per_step is the measured wall time of one sample
+    (what the driver's clock sees), value the extrapolated whole-layer-set
+    tok/s (median over the K steps)."""
+    import oracle
+    oracle.build()
+    for i in range(args.warmup):
+        oracle_sample(args.workload, args.n, which=i)
+    vals, secs = [], []
+    for i in range(args.steps):
+        v, t, info = oracle_sample(args.workload, args.n, which=i)
         vals.append(v)
+        secs.append(t)
     v = float(np.median(vals))
+    # single-thread oracle on one sample (once)
+    v1, t1, _ = oracle_sample(args.workload, args.n, nthreads=1, which=0)
     return {
         "metric": METRIC, "value": round(v, 6), "unit": "tok/s", "n_gpus": 1,
-        "steps": len(vals), "warmup": 0, "ms_per_step": round(1e3 * args.n / v, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * float(np.median(secs)), 3),
+        "ms_per_step_is": "measured wall time of one bounded oracle sample (value is extrapolated to the layer set)",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 (oracle)", "data": "synthetic", "impl": "reference",
         "config": {"workload": args.workload, "tokens_per_step": args.n},
-        "cpu_baseline": {"value": round(v, 6), "unit": "tok/s", "cores": info["cores"],
-                         "kind": "oracle", "sample": info["sample"]},
+        "cpu_baseline": {"value": round(v, 6), "unit": "tok/s", "cores": info["cores"], "kind": "oracle",
+                         "sample": info["sample"], "cpu_model": cpu_model(),
+                         "single_thread": {"value": round(v1, 6), "unit": "tok/s", "sample_s": round(t1, 3)}},
         "e2e": {"value": round(v, 6), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
 
 
 def main():
@@ -488,7 +549,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama2-7b-decode",
                     choices=["llama2-7b-decode", "llama2-13b-decode", "llama2-70b-decode",
-                             "llama2-7b-prefill", "llama2-13b-prefill"])
+                             "llama2-7b-prefill", "llama2-13b-prefill", "llama2-70b-prefill"])
     ap.add_argument("--n", type=int, default=None, help="tokens per step (decode: 1)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
@@ -498,10 +559,11 @@ def main():
     ap.add_argument("--fused", action="store_true",
                     help="stack q/k/v and gate/up rows into one call each (same weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="with N > 1 ranks: independent decode replicas instead of tensor parallelism")
     ap.add_argument("--tp", action="store_true",
-                    help="with torchrun: real Megatron tensor parallelism of the layer set over the ranks "
-                         "(column/row split, NCCL all_reduce after o and down); value = tokens of the one "
-                         "stream, scaling strong")
+                    help="tensor parallelism over the ranks even at N = 1 (one NCCL rank: exercises the "
+                         "collectives of the TP step on one GPU); the default for N > 1")
     ap.add_argument("--block", default="none", choices=["none", "fused", "unfused"],
                     help="decoder-block chain with RMSNorm / SiLU-mul / residual fused into the linears "
                          "(fused) or as separate kernels (unfused); implies the fused q/k/v, gate/up layout")
@@ -513,6 +575,14 @@ def main():
     if args.block != "none":
         args.fused = True
 
+    under_torchrun = "WORLD_SIZE" in os.environ and "LOCAL_RANK" in os.environ
+    if args.gpus > 1 and not under_torchrun:
+        # one process per GPU: re-launch under torch.distributed.run (127.0.0.1 rendezvous)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+               os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -523,17 +593,24 @@ def main():
         print(json.dumps(run_reference(args)))
         return 0
 
-    if world > 1 or (args.tp and "MASTER_ADDR" in os.environ):
+    if world > 1 and not args.replicas:
+        args.tp = True
+    if world > 1 or args.tp:
+        # NCCL logs to stdout; keep rank 0's stdout the one JSON line
+        os.environ["NCCL_DEBUG"] = os.environ.get("RELAX_BENCH_NCCL_DEBUG", "WARN")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
+        if world == 1 and "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()), RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            v, info = oracle_sample(args.workload, args.n)
+            v, t_s, info = oracle_sample(args.workload, args.n)
             res["cpu_baseline"] = {"value": round(v, 6), "unit": "tok/s", "cores": info["cores"],
-                                   "kind": "oracle", "sample": info["sample"]}
+                                   "kind": "oracle", "sample": info["sample"], "sample_s": round(t_s, 3),
+                                   "cpu_model": cpu_model()}
         print(json.dumps(res))
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():

@@ -62,6 +62,9 @@ def _default_matmul():
 
 @dataclass
 class ColumnParallelQ4:
+    """y_r = x . W_r on this rank's N/p output features; with gather=True the
+    shards are all-gathered (NCCL all_gather_into_tensor over NVLink on the
+    box) into the full [n, N] in feature order -- the lm_head's logits."""
     packed: object
     scales: object
     group: object = None
@@ -76,13 +79,19 @@ class ColumnParallelQ4:
         if not self.gather:
             return y
         world = dist.get_world_size(self.group)
-        parts = [torch.empty_like(y) for _ in range(world)]
-        dist.all_gather(parts, y.contiguous(), group=self.group)
-        return torch.cat(parts, dim=1)                    # [n, N]
+        n, npart = y.shape
+        buf = torch.empty((world * n, npart), dtype=y.dtype, device=y.device)
+        dist.all_gather_into_tensor(buf, y.contiguous(), group=self.group)
+        # [p*n][N/p] = [p][n][N/p] -> [n][N]: rank r's features are columns [r N/p, (r+1) N/p)
+        return buf.view(world, n, npart).permute(1, 0, 2).reshape(n, world * npart)
 
 
 @dataclass
 class RowParallelQ4:
+    """Partial y_r = x_r . W_r over this rank's K/p slice, summed over the
+    ranks by one all_reduce.  The kernel's partials are fp16 (its output
+    type); the sum runs in fp32 and is rounded to fp16 once (DESIGN.md §3
+    reading 14), so the result does not depend on p beyond the fp16 partials."""
     packed: object
     scales: object
     group: object = None
@@ -100,6 +109,31 @@ class RowParallelQ4:
             return y32.to(torch.float16)
         dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
         return y
+
+
+# Megatron placement of the Llama linears: column-parallel
+# producers, row-parallel consumers, one all_reduce after each row-parallel
+# linear; the lm_head column-parallel with its logits gathered.
+MEGATRON_KIND = {"q": "col", "k": "col", "v": "col", "qkv": "col", "gate": "col", "up": "col",
+                 "gate_up": "col", "o": "row", "down": "row", "lm_head": "col"}
+
+
+def shard_shape(name: str, K: int, N: int, world: int):
+    """Rank-local (K, N) of a linear under Megatron TP of degree `world`."""
+    if world == 1:
+        return K, N
+    if MEGATRON_KIND[name] == "row":
+        lo, hi = shard_bounds(K, 0, world, GROUP)
+        return hi - lo, N
+    lo, hi = shard_bounds(N, 0, world)
+    return K, hi - lo
+
+
+def megatron_linear(name: str, packed, scales, group=None, matmul=None):
+    """The TP wrapper of one Llama linear given this rank's shard."""
+    if MEGATRON_KIND[name] == "row":
+        return RowParallelQ4(packed, scales, group=group, matmul=matmul)
+    return ColumnParallelQ4(packed, scales, group=group, gather=(name == "lm_head"), matmul=matmul)
 
 
 def split_x_for_rows(x, rank: int, world: int):

@@ -47,6 +47,14 @@ def t32(words):
 
 
 def _worker(rank, world, port, q):
+    try:
+        _worker_body(rank, world, port, q)
+    except BaseException as e:  # noqa: BLE001  -- fail the test now, not at the queue timeout
+        q.put((rank, {"error": repr(e)}))
+        raise
+
+
+def _worker_body(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -71,6 +79,14 @@ def _worker(rank, world, port, q):
         g = tp.ColumnParallelQ4(*tp.shard_columns(t32(gpk), t16(gsc), rank, world), matmul=oracle_mm)
         d = tp.RowParallelQ4(*tp.shard_rows(t32(dpk), t16(dsc), rank, world), matmul=oracle_mm)
         out["pair"] = d(g(x)).numpy().view(np.uint16)
+        # lm_head: column split, logits all-gathered (all_gather_into_tensor) back
+        # into feature order for n = 3 tokens
+        hpk, hsc = inputs.realistic_weights(5004, K, 320)
+        head = tp.megatron_linear("lm_head", *tp.shard_columns(t32(hpk), t16(hsc), rank, world), matmul=oracle_mm)
+        out["head"] = head(x).numpy().view(np.uint16)
+        # the shard shapes the bench uses agree with the shards themselves
+        out["shapes"] = [tuple(tp.shard_columns(t32(hpk), t16(hsc), rank, world)[0].shape),
+                         tp.shard_shape("lm_head", K, 320, world), tp.shard_shape("down", 512, K2, world)]
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -87,6 +103,8 @@ def results():
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))
+    for r, out in res.items():
+        assert "error" not in out, f"rank {r}: {out['error']}"
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -120,6 +138,22 @@ def test_megatron_pair(results):
     r = oracle.matmul_f64(h, dpk, dsc, 512, 256)
     assert np.array_equal(results[0]["pair"], results[1]["pair"])
     assert_within_tol(results[0]["pair"], r, "pair")
+
+
+def test_lm_head_gather_feature_order(results):
+    """Column-split logits, all-gathered: identical on both ranks and equal,
+    bitwise, to the unsharded oracle for n > 1 (the [p][n][N/p] gather buffer is
+    reordered to [n][N])."""
+    K, n = 512, 3
+    xb = inputs.activations(5001, n, K)
+    hpk, hsc = inputs.realistic_weights(5004, K, 320)
+    want = oracle.round_f16(oracle.matmul_f64(xb, hpk, hsc, K, 320))
+    for r in (0, 1):
+        assert results[r]["head"].shape == (n, 320)
+        assert np.array_equal(results[r]["head"], want)
+    assert results[0]["shapes"][0] == (160, 512 // 8)
+    assert results[0]["shapes"][1] == (512, 160)
+    assert results[0]["shapes"][2] == (256, 256)
 
 
 def test_shard_bounds_errors():
