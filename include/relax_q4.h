@@ -84,7 +84,9 @@ enum relax_status {
 enum relax_variant {
     RELAX_VARIANT_AUTO = 0,
     RELAX_VARIANT_GEMV = 1,   /* CUDA-core split-free GEMV, 128-bit loads, warp-shuffle reduce */
-    RELAX_VARIANT_TC = 2      /* TMA + tcgen05/TMEM GEMM with in-kernel dequant (K % 256 == 0) */
+    RELAX_VARIANT_TC = 2,     /* TMA + tcgen05/TMEM GEMM with in-kernel dequant (K % 256 == 0) */
+    RELAX_VARIANT_SMALLN = 3  /* small batches: streamed warp-MMA (mma.sync) GEMV, 8 tokens per
+                                 launch, no workspace (K % 256 == 0) */
 };
 
 /* Flags for relax_q4_matmul_ex. */
@@ -206,9 +208,9 @@ RELAX_API int relax_q4_matmul_fused(const void* x, int64_t n, int64_t K, int64_t
                                     size_t ws_bytes, void* stream);
 
 /* Host-only report of the schedule relax_q4_matmul_ws would use for (n,K,N):
- * out pointers may be NULL.  variant: enum relax_variant; tile: GEMV tokens
- * per launch or TC token tile; split_k: TC split factor; ws_bytes: bytes
- * needed.  Errors: RELAX_ERR_INVALID_ARG, RELAX_ERR_UNSUPPORTED_SHAPE. */
+ * out pointers may be NULL.  variant: enum relax_variant; tile: GEMV / SMALLN
+ * tokens per launch or TC token tile; split_k: TC split factor; ws_bytes:
+ * bytes needed.  Errors: RELAX_ERR_INVALID_ARG, RELAX_ERR_UNSUPPORTED_SHAPE. */
 RELAX_API int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile,
                          int* split_k, size_t* ws_bytes);
 

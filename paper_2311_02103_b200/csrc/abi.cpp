@@ -23,6 +23,17 @@ int gemv_max_n() {
 
 static int ctas_per_sm_tc(int bn) { return bn <= 64 ? 2 : 1; }
 
+// Small batches (3 <= n <= 8): the warp-MMA streamed kernel or the tcgen05
+// kernel, from the measured crossover (profiles/r02/sweep_smalln_r02.jsonl,
+// DESIGN.md §6): the streamed kernel wins where K is short relative to N
+// (K <= 5120: 4096^2 n = 8 5.4 vs 7.0 us; 4096 x 11008 9.2 vs 11.3 us) and
+// at n <= 4 up to K = 8192; the split-K tensor-core tiles win for long K
+// (11008 x 4096 n = 8: 13.4 vs 11.9 us) and narrow N (8192 x 1024).
+static bool smalln_preferred(int64_t n, int64_t K, int64_t N) {
+    if (n < 3 || n > smalln_max_n() || N < 2048) return false;
+    return K <= 5120 || (K <= 8192 && n <= 4);
+}
+
 // Split-K clusters of s CTAs that all start in the first wave on a B200
 // (148 SMs), measured per resident-CTA count by tools/tc_waves.py
 // (profiles/tc_waves_r01.txt): the GPC placement of clusters holds fewer than
@@ -111,6 +122,7 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
         const int nt = static_cast<int>(n < kGemvMaxNT ? n : kGemvMaxNT);
         const int nt1 = nt < 1 ? 1 : nt;
         if (n <= gemv_max_n() && (gemv_stream_ok(nt1, K, N) || gemv_fits(nt1, K))) v = kVariantGemv;
+        else if (smalln_preferred(n, K, N) && smalln_mma_ok(n, K, N)) v = kVariantSmallN;
         else if (tc_ok) v = kVariantTc;
         else v = kVariantGemv;
     }
@@ -121,6 +133,11 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
         if (!gemv_fits(nt, K) && !gemv_stream_ok(nt, K, N)) return RELAX_ERR_UNSUPPORTED_SHAPE;
         p.variant = kVariantGemv;
         p.nt = nt;
+        p.ws_bytes = 0;
+    } else if (v == kVariantSmallN) {
+        if (!smalln_mma_ok(n < 1 ? 1 : n, K, N)) return RELAX_ERR_UNSUPPORTED_SHAPE;
+        p.variant = kVariantSmallN;
+        p.nt = 8;
         p.ws_bytes = 0;
     } else if (v == kVariantTc) {
         if (!tc_ok) return RELAX_ERR_UNSUPPORTED_SHAPE;
@@ -200,7 +217,7 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
                        int split_k, int bn, unsigned flags, void* stream) {
     if (n < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
     if (K % kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
-    if (variant < 0 || variant > 2 || split_k < 0) return RELAX_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 3 || split_k < 0) return RELAX_ERR_INVALID_ARG;
     if (n == 0) return RELAX_OK;
     if (!x || !packed_w || !scales || !y) return RELAX_ERR_INVALID_ARG;
     if (ws_bytes > 0 && !ws) return RELAX_ERR_INVALID_ARG;
@@ -232,6 +249,9 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
     if (plan.variant == kVariantGemv)
         e = launch_gemv(static_cast<const uint16_t*>(x), n, K, N, packed_w,
                         static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), plan.nt, pdl, st);
+    else if (plan.variant == kVariantSmallN)
+        e = launch_smalln_mma(static_cast<const uint16_t*>(x), n, K, N, packed_w,
+                              static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), pdl, st);
     else
         e = launch_tc(static_cast<const uint16_t*>(x), n, K, N, packed_w,
                       static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), plan, ws, pdl, st);
@@ -300,7 +320,8 @@ static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint
         rc = make_plan(n, K, N, kVariantAuto, sp, 0, &plan, false);
     }
     if (rc != RELAX_OK) return rc;
-    if (plan.variant == kVariantGemv && !gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1)) {
+    if (plan.variant == kVariantSmallN ||
+        (plan.variant == kVariantGemv && !gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1))) {
         // the fused neighbours live in the streamed decode kernel and the
         // tensor-core kernel only: a shape the former cannot hold takes the latter
         rc = make_plan(n, K, N, kVariantTc, 0, 0, &plan, false);
@@ -359,8 +380,9 @@ int relax_plan_workspace_fused(int64_t n_max, int64_t K, int64_t N, uint32_t ops
         rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
         if (rc != RELAX_OK) return rc;
         // a GEMV plan the streamed decode kernel cannot hold runs on the TC path (fused_impl)
-        if (p.variant == rq4::kVariantGemv &&
-            !rq4::gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1)) {
+        if (p.variant == rq4::kVariantSmallN ||
+            (p.variant == rq4::kVariantGemv &&
+             !rq4::gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1))) {
             rc = rq4::make_plan(n, K, N, rq4::kVariantTc, 0, 0, &p, false);
             if (rc != RELAX_OK) return rc;
         }
@@ -407,7 +429,7 @@ int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* til
     const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
     if (rc != RELAX_OK) return rc;
     if (variant) *variant = p.variant;
-    if (tile) *tile = p.variant == rq4::kVariantGemv ? p.nt : p.bn;
+    if (tile) *tile = (p.variant == rq4::kVariantGemv || p.variant == rq4::kVariantSmallN) ? p.nt : p.bn;
     if (split_k) *split_k = p.split;
     if (ws_bytes) *ws_bytes = p.ws_bytes;
     return RELAX_OK;

@@ -51,7 +51,7 @@ struct Fusion {
     const uint16_t* res = nullptr;     // RESIDUAL, fp16 [n][N_out]
 };
 
-enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2 };
+enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2, kVariantSmallN = 3 };
 
 struct Plan {
     int variant = 0;
@@ -83,6 +83,12 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
 // (K % 256 == 0, N < 2^24, its shared-memory footprint within the attribute);
 // pair = 2 with the SiLU-mul epilogue (CTAs own whole (gate, up) row pairs).
 bool gemv_stream_ok(int nt, int64_t K, int64_t N, int pair = 1);
+// Small-batch warp-MMA streamed kernel (smalln_mma.cu): any n (8 tokens per
+// launch), K % 256 == 0.
+bool smalln_mma_ok(int64_t n, int64_t K, int64_t N);
+int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+                      const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
+int smalln_max_n();                 // largest n the automatic dispatch sends to it
 // RMSNorm of fp16 rows into `out` (the TC path's RMSNORM_X prologue; the
 // decode GEMV normalises in registers instead).
 int launch_rmsnorm(const uint16_t* x, int64_t n, int64_t K, const uint16_t* gamma, float eps,

@@ -24,6 +24,9 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 // ----------------------------------------------------------------- PDL
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" :: "l"(p));
+}
 __device__ __forceinline__ void pdl_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }

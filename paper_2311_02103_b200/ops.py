@@ -32,7 +32,7 @@ STATUS = {
     3: "RELAX_ERR_MISALIGNED", 4: "RELAX_ERR_ALIAS", 5: "RELAX_ERR_WORKSPACE",
     6: "RELAX_ERR_DEVICE", 7: "RELAX_ERR_CUDA",
 }
-VARIANT_AUTO, VARIANT_GEMV, VARIANT_TC = 0, 1, 2
+VARIANT_AUTO, VARIANT_GEMV, VARIANT_TC, VARIANT_SMALLN = 0, 1, 2, 3
 FLAG_NO_PDL = 1
 FLAG_SPLIT_WORKSPACE = 2
 
@@ -127,7 +127,7 @@ def query_schedule(n: int, K: int, N: int) -> dict:
     ws = ctypes.c_size_t(0)
     _check(lib().relax_query_schedule(n, K, N, ctypes.byref(v), ctypes.byref(t), ctypes.byref(s),
                                       ctypes.byref(ws)), "relax_query_schedule")
-    name = {VARIANT_GEMV: "gemv", VARIANT_TC: "tc"}[v.value]
+    name = {VARIANT_GEMV: "gemv", VARIANT_TC: "tc", VARIANT_SMALLN: "smalln"}[v.value]
     return {"variant": name, "tile": t.value, "split_k": s.value, "ws_bytes": int(ws.value)}
 
 

@@ -93,7 +93,10 @@ def test_dispatch_shape_specialisation():
     prefill; K % 256 != 0 keeps GEMV at any n."""
     assert ops.query_schedule(1, 4096, 4096)["variant"] == "gemv"
     assert ops.query_schedule(2, 4096, 4096)["variant"] == "gemv"
-    assert ops.query_schedule(3, 4096, 4096)["variant"] == "tc"
+    assert ops.query_schedule(3, 4096, 4096)["variant"] == "smalln"
+    assert ops.query_schedule(8, 4096, 11008)["variant"] == "smalln"
+    assert ops.query_schedule(9, 4096, 4096)["variant"] == "tc"
+    assert ops.query_schedule(8, 11008, 4096)["variant"] == "tc"
     s = ops.query_schedule(4096, 4096, 4096)
     assert s["variant"] == "tc" and s["tile"] in (128, 256) and s["split_k"] == 1
     assert ops.query_schedule(512, 4128, 4096)["variant"] == "gemv"

@@ -77,7 +77,7 @@ def test_config1_auto(kind, n):
 
 
 WSF = 2   # RELAX_FLAG_SPLIT_WORKSPACE
-VARIANTS = [("gemv", 1, 0, 0, 0), ("tc16", 2, 1, 16, 0), ("tc32", 2, 1, 32, 0), ("tc64", 2, 1, 64, 0),
+VARIANTS = [("gemv", 1, 0, 0, 0), ("smalln", 3, 0, 0, 0), ("tc16", 2, 1, 16, 0), ("tc32", 2, 1, 32, 0), ("tc64", 2, 1, 64, 0),
             ("tc128", 2, 1, 128, 0), ("tc256", 2, 1, 256, 0),
             ("tc16s3c", 2, 3, 16, 0), ("tc64s2c", 2, 2, 64, 0), ("tc128s2c", 2, 2, 128, 0),
             ("tc256s3c", 2, 3, 256, 0),
@@ -89,8 +89,8 @@ VARIANTS = [("gemv", 1, 0, 0, 0), ("tc16", 2, 1, 16, 0), ("tc32", 2, 1, 32, 0), 
 def test_every_variant_ragged(name, variant, split, bn, flags, n):
     """Several M tiles and a ragged tail (N = 328 = 2*128 + 72), 3 weight
     stages of 256 k (K = 768), ragged token tiles."""
-    if name == "gemv" and n > 17:
-        pytest.skip("GEMV exercised at small n")
+    if name in ("gemv", "smalln") and n > 17:
+        pytest.skip("GEMV / small-n kernels exercised at small n")
     K, N = 768, 328
     packed, scales = inputs.realistic_weights(2000, K, N)
     x = inputs.activations(7 + n, n, K)

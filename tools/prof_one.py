@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 from paper_2311_02103_b200 import inputs, ops  # noqa: E402
 
 K, N, n = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
-var = {"auto": 0, "gemv": 1, "tc": 2}[sys.argv[4] if len(sys.argv) > 4 else "auto"]
+var = {"auto": 0, "gemv": 1, "tc": 2, "smalln": 3}[sys.argv[4] if len(sys.argv) > 4 else "auto"]
 reps = int(sys.argv[5]) if len(sys.argv) > 5 else 5
 pk, sc = inputs.realistic_weights(5 + K + N, K, N)
 pw = torch.from_numpy(pk.view(np.int32)).cuda()

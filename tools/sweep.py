@@ -72,9 +72,12 @@ def main():
             for var in a.variants.split(","):
                 if var == "gemv" and n > 8:
                     continue
+                if var == "smalln" and n > 32:
+                    continue
                 base, _, sp = var.partition(":")        # "tc:S" forces split-K S (cluster reduction)
                 split = int(sp) if sp else 0
-                v = {"auto": ops.VARIANT_AUTO, "gemv": ops.VARIANT_GEMV, "tc": ops.VARIANT_TC}[base]
+                v = {"auto": ops.VARIANT_AUTO, "gemv": ops.VARIANT_GEMV, "tc": ops.VARIANT_TC,
+                     "smalln": ops.VARIANT_SMALLN}[base]
                 # a rotation long enough to stream >= 4 L2 of weights per replay
                 fns = [lambda p=p, s=s: ops.q4_matmul_ex(x, p, s, y=y, ws=ws, variant=v, flags=flags,
                                                          split_k=split, stream=stream) for p, s in copies]
