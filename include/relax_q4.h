@@ -222,6 +222,30 @@ RELAX_API int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant
 RELAX_API int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int64_t K, int64_t N,
                      void* w_out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Format variants: "lift out quantization and layout
+ * transforms in tensor programs to enable pre-computation".  A
+ * weight stored in another layout or group size is converted ONCE into the
+ * native format above; the converted weight dequantizes to the same W bit for
+ * bit (codes move unchanged; every 32-group takes the scale of the G-group
+ * that contains it).  Source formats (DESIGN.md §3 readings 19-20):
+ *   RELAX_LAYOUT_NK  src_packed uint32 [N][K/8], src_scales fp16 [N][K/G]
+ *   RELAX_LAYOUT_KN  src_packed uint32 [K/8][N] (word (k/8, j) holds codes
+ *                    k..k+7 of output column j, low nibble first -- the
+ *                    per-column packing of GPTQ-style checkpoints),
+ *                    src_scales fp16 [K/G][N]
+ *   group G in {32, 64, 128}; W(k, j) = fp16_RNE((q - 7) * s(k/G, j)).
+ * Outputs: packed_w uint32 [N][K/8], scales fp16 [N][K/32] (device, caller-
+ * owned, must not overlap the inputs).  Asynchronous on `stream`.
+ * Errors: RELAX_ERR_INVALID_ARG (unknown layout, NULL, K <= 0, N < 0),
+ * RELAX_ERR_UNSUPPORTED_SHAPE (G not in {32, 64, 128} or K % G != 0),
+ * RELAX_ERR_MISALIGNED, RELAX_ERR_ALIAS, RELAX_ERR_DEVICE, RELAX_ERR_CUDA.
+ * N == 0 is a no-op. */
+#define RELAX_LAYOUT_NK 0
+#define RELAX_LAYOUT_KN 1
+RELAX_API int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t K, int64_t N,
+                              int layout, int group, uint32_t* packed_w, void* scales, void* stream);
+
 /* Static description of a status code; never NULL. */
 RELAX_API const char* relax_status_str(int status);
 

@@ -23,15 +23,20 @@ int gemv_max_n() {
 
 static int ctas_per_sm_tc(int bn) { return bn <= 64 ? 2 : 1; }
 
-// Small batches (3 <= n <= 8): the warp-MMA streamed kernel or the tcgen05
-// kernel, from the measured crossover (profiles/r02/sweep_smalln_r02.jsonl,
-// DESIGN.md §6): the streamed kernel wins where K is short relative to N
-// (K <= 5120: 4096^2 n = 8 5.4 vs 7.0 us; 4096 x 11008 9.2 vs 11.3 us) and
-// at n <= 4 up to K = 8192; the split-K tensor-core tiles win for long K
-// (11008 x 4096 n = 8: 13.4 vs 11.9 us) and narrow N (8192 x 1024).
+// Small batches (3 <= n <= 8): the warp-MMA streamed kernel or the split-K
+// tcgen05 tiles.  Measured in the decode chain, not per kernel
+// (profiles/r02/smalln_dispatch_ab_r02.txt): in isolated
+// same-shape chains the tcgen05 kernel leads for long K (11008 x 4096 n = 8:
+// 11.9 vs 13.4 us, profiles/r02/sweep_smalln_r02.jsonl), but its two 384-thread
+// CTAs per SM leave no room for a neighbour under PDL, so a tcgen05 linear
+// between streamed ones costs its neighbours their weight prefetch: 7B decode
+// n = 8 4655 tok/s all-streamed vs 3637 with the down projection on tcgen05
+// (13B: 2417 vs 1872).  Only the 70B down projection (K = 28672) still gains
+// from the tensor-core tiles (560 vs 474 tok/s), and narrow outputs
+// (N < 2048, the 70B k/v) keep them.
 static bool smalln_preferred(int64_t n, int64_t K, int64_t N) {
-    if (n < 3 || n > smalln_max_n() || N < 2048) return false;
-    return K <= 5120 || (K <= 8192 && n <= 4);
+    static const int64_t kmax = knob_int("RELAX_Q4_SMALLN_MAX_K", 16384);
+    return n >= 3 && n <= smalln_max_n() && N >= 2048 && K <= kmax;
 }
 
 // Split-K clusters of s CTAs that all start in the first wave on a B200
@@ -468,6 +473,35 @@ int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int64_t K, in
     if (rc != RELAX_OK) return rc;
     const int e = rq4::launch_dequant(packed_w, static_cast<const uint16_t*>(scales), K, N,
                                       static_cast<uint16_t*>(w_out), static_cast<cudaStream_t>(stream));
+    if (e != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
+int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t K, int64_t N, int layout,
+                    int group, uint32_t* packed_w, void* scales, void* stream) {
+    if (K <= 0 || N < 0) return RELAX_ERR_INVALID_ARG;
+    if (layout != RELAX_LAYOUT_NK && layout != RELAX_LAYOUT_KN) return RELAX_ERR_INVALID_ARG;
+    if (group != 32 && group != 64 && group != 128) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if (K % group != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if (N == 0) return RELAX_OK;
+    if (!src_packed || !src_scales || !packed_w || !scales) return RELAX_ERR_INVALID_ARG;
+    if (!rq4::aligned16(src_packed) || !rq4::aligned16(src_scales) || !rq4::aligned16(packed_w) ||
+        !rq4::aligned16(scales))
+        return RELAX_ERR_MISALIGNED;
+    const size_t wb = static_cast<size_t>(N) * K / 2;
+    const size_t sb_out = static_cast<size_t>(N) * (K / rq4::kGroup) * 2;
+    const size_t sb_in = static_cast<size_t>(N) * (K / group) * 2;
+    if (rq4::overlap(packed_w, wb, src_packed, wb) || rq4::overlap(packed_w, wb, src_scales, sb_in) ||
+        rq4::overlap(scales, sb_out, src_packed, wb) || rq4::overlap(scales, sb_out, src_scales, sb_in) ||
+        rq4::overlap(packed_w, wb, scales, sb_out))
+        return RELAX_ERR_ALIAS;
+    const int rc = rq4::check_device();
+    if (rc != RELAX_OK) return rc;
+    const int e = rq4::launch_repack(src_packed, static_cast<const uint16_t*>(src_scales), K, N, layout, group,
+                                     packed_w, static_cast<uint16_t*>(scales), static_cast<cudaStream_t>(stream));
     if (e != 0) {
         cudaGetLastError();
         return RELAX_ERR_CUDA;

@@ -89,6 +89,9 @@ bool smalln_mma_ok(int64_t n, int64_t K, int64_t N);
 int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 int smalln_max_n();                 // largest n the automatic dispatch sends to it
+// One-time format conversion into the native layout (repack.cu).
+int launch_repack(const uint32_t* src_w, const uint16_t* src_s, int64_t K, int64_t N, int layout, int group,
+                  uint32_t* w, uint16_t* s, cudaStream_t stream);
 // RMSNorm of fp16 rows into `out` (the TC path's RMSNORM_X prologue; the
 // decode GEMV normalises in registers instead).
 int launch_rmsnorm(const uint16_t* x, int64_t n, int64_t K, const uint16_t* gamma, float eps,

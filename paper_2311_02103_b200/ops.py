@@ -39,7 +39,7 @@ FLAG_SPLIT_WORKSPACE = 2
 # every symbol include/relax_q4.h declares
 EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",
            "relax_query_schedule", "relax_q4_dequant", "relax_status_str", "relax_version",
-           "relax_plan_workspace_fused", "relax_q4_matmul_fused")
+           "relax_plan_workspace_fused", "relax_q4_matmul_fused", "relax_q4_repack")
 
 # fused neighbours (include/relax_q4.h RELAX_OP_*)
 OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL = 1, 2, 4
@@ -95,6 +95,8 @@ def lib() -> ctypes.CDLL:
         L.relax_plan_workspace_fused.restype = I
         L.relax_q4_matmul_fused.argtypes = [P, I64, I64, I64, P, P, P, ctypes.POINTER(Fusion), P, SZ, P]
         L.relax_q4_matmul_fused.restype = I
+        L.relax_q4_repack.argtypes = [P, P, I64, I64, I, I, P, P, P]
+        L.relax_q4_repack.restype = I
         _lib = L
         return L
 
@@ -266,6 +268,37 @@ def q4_matmul_fused(x, packed_w, scales, y=None, rms_weight=None, rms_eps: float
                                      _ptr(ws), nb, _stream_ptr(stream))
     _check(rc, "relax_q4_matmul_fused")
     return y
+
+
+LAYOUT_NK, LAYOUT_KN = 0, 1
+
+
+def q4_repack(src_packed, src_scales, K: int, N: int, layout: str = "kn", group: int = 32,
+              packed_w=None, scales=None, stream=None):
+    """relax_q4_repack: convert a weight stored as `layout` ("nk" / "kn") with
+    group size `group` into the native packed_w [N, K/8] (int32) and scales
+    [N, K/32] (fp16); bit-exact (include/relax_q4.h)."""
+    import torch
+    lay = {"nk": LAYOUT_NK, "kn": LAYOUT_KN}[layout]
+    dev = _device_of_call()
+    if K % group != 0 or group not in (32, 64, 128):
+        raise ValueError(f"group {group} must be 32, 64 or 128 and divide K = {K}")
+    want_p = (N, K // 8) if lay == LAYOUT_NK else (K // 8, N)
+    want_s = (N, K // group) if lay == LAYOUT_NK else (K // group, N)
+    _check_tensor(src_packed, "src_packed", (torch.int32, torch.uint32), want_p, dev=dev)
+    _check_tensor(src_scales, "src_scales", torch.float16, want_s, dev=dev)
+    if packed_w is None:
+        packed_w = torch.empty((N, K // 8), dtype=torch.int32, device=dev)
+    else:
+        _check_tensor(packed_w, "packed_w", (torch.int32, torch.uint32), (N, K // 8), dev=dev)
+    if scales is None:
+        scales = torch.empty((N, K // 32), dtype=torch.float16, device=dev)
+    else:
+        _check_tensor(scales, "scales", torch.float16, (N, K // 32), dev=dev)
+    rc = lib().relax_q4_repack(_ptr(src_packed), _ptr(src_scales), K, N, lay, group, _ptr(packed_w),
+                               _ptr(scales), _stream_ptr(stream))
+    _check(rc, "relax_q4_repack")
+    return packed_w, scales
 
 
 def interleave_rows(a, b):

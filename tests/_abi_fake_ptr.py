@@ -109,10 +109,23 @@ def fused_plan_soundness(L):
                          gamma=A + 512 * MB, ws=A + 1024 * MB, wsb=nb) == 6
 
 
+def repack_validation(L):
+    P = A + 64 * MB
+    assert L.relax_q4_repack(A, A + MB, 256, 64, 2, 32, P, P + MB, None) == 1      # unknown layout
+    assert L.relax_q4_repack(A, A + MB, 256, 64, 1, 48, P, P + MB, None) == 2      # group not 32/64/128
+    assert L.relax_q4_repack(A, A + MB, 320, 64, 1, 128, P, P + MB, None) == 2     # K % G != 0
+    assert L.relax_q4_repack(A, A + MB, 256, 64, 1, 64, 0, P + MB, None) == 1
+    assert L.relax_q4_repack(A + 4, A + MB, 256, 64, 1, 64, P, P + MB, None) == 3
+    assert L.relax_q4_repack(A, A + MB, 256, 64, 1, 64, A, P + MB, None) == 4      # output over the input
+    assert L.relax_q4_repack(A, A + MB, 256, 0, 1, 64, P, P + MB, None) == 0       # N == 0: no-op
+    assert L.relax_q4_repack(A, A + MB, 256, 64, 1, 64, P, P + MB, None) == 6      # valid: device check
+
+
 def main():
     assert os.environ.get("CUDA_VISIBLE_DEVICES", None) == "", "run with CUDA_VISIBLE_DEVICES=''"
     L = ops.lib()
-    for f in (validation_codes, workspace_too_small, plan_invalid, fused_validation_codes, fused_plan_soundness):
+    for f in (validation_codes, workspace_too_small, plan_invalid, fused_validation_codes, fused_plan_soundness,
+              repack_validation):
         f(L)
         print("ok", f.__name__)
     print("ALL OK")

@@ -30,7 +30,7 @@ def header_symbols():
 
 def test_exports_every_declared_symbol(L):
     syms = header_symbols()
-    assert len(syms) == 10
+    assert len(syms) == 11
     assert sorted(ops.EXPORTS) == syms
     for s in syms:
         assert hasattr(L, s), s
@@ -96,7 +96,8 @@ def test_dispatch_shape_specialisation():
     assert ops.query_schedule(3, 4096, 4096)["variant"] == "smalln"
     assert ops.query_schedule(8, 4096, 11008)["variant"] == "smalln"
     assert ops.query_schedule(9, 4096, 4096)["variant"] == "tc"
-    assert ops.query_schedule(8, 11008, 4096)["variant"] == "tc"
+    assert ops.query_schedule(8, 11008, 4096)["variant"] == "smalln"
+    assert ops.query_schedule(8, 8192, 1024)["variant"] == "tc"
     s = ops.query_schedule(4096, 4096, 4096)
     assert s["variant"] == "tc" and s["tile"] in (128, 256) and s["split_k"] == 1
     assert ops.query_schedule(512, 4128, 4096)["variant"] == "gemv"
