@@ -596,8 +596,10 @@ def main():
     if world > 1 and not args.replicas:
         args.tp = True
     if world > 1 or args.tp:
-        # NCCL logs to stdout; keep rank 0's stdout the one JSON line
+        # NCCL logs to stdout (even its version line at NCCL_DEBUG=WARN): keep rank
+        # 0's stdout the one JSON line by sending NCCL's log to stderr
         os.environ["NCCL_DEBUG"] = os.environ.get("RELAX_BENCH_NCCL_DEBUG", "WARN")
+        os.environ["NCCL_DEBUG_FILE"] = "/dev/stderr"
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)

@@ -92,6 +92,8 @@ enum relax_variant {
 /* Flags for relax_q4_matmul_ex. */
 #define RELAX_FLAG_NO_PDL 1u            /* launch without programmatic dependent launch */
 #define RELAX_FLAG_SPLIT_WORKSPACE 2u   /* TC split-K through the workspace, not a cluster */
+#define RELAX_FLAG_TILE_PER_CTA 4u      /* TC: one tile per CTA, never the persistent
+                                           double-buffered-accumulator kernel */
 
 /* Upper-bound workspace plan (lifted workspace P:438-441).
  * Host only, pure: no launch, no allocation.
@@ -210,9 +212,11 @@ RELAX_API int relax_q4_matmul_fused(const void* x, int64_t n, int64_t K, int64_t
 /* Host-only report of the schedule relax_q4_matmul_ws would use for (n,K,N):
  * out pointers may be NULL.  variant: enum relax_variant; tile: GEMV / SMALLN
  * tokens per launch or TC token tile; split_k: TC split factor; ws_bytes:
- * bytes needed.  Errors: RELAX_ERR_INVALID_ARG, RELAX_ERR_UNSUPPORTED_SHAPE. */
+ * bytes needed; persistent: 1 when the TC schedule is the persistent
+ * double-buffered-accumulator kernel.  Errors: RELAX_ERR_INVALID_ARG,
+ * RELAX_ERR_UNSUPPORTED_SHAPE. */
 RELAX_API int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile,
-                         int* split_k, size_t* ws_bytes);
+                         int* split_k, size_t* ws_bytes, int* persistent);
 
 /* Bit-exact dequant export: w_out[j][k] = fp16_RNE((q(k,j) - 7) * s), the
  * producer half of the fused op on its own (used to pin the in-kernel

@@ -23,6 +23,12 @@ int gemv_max_n() {
 
 static int ctas_per_sm_tc(int bn) { return bn <= 64 ? 2 : 1; }
 
+// Time model of the persistent BN = 256 kernel (us per 256-k stage per tile,
+// one fill/drain per CTA); RELAX_Q4_PERSIST (experiments build) 0 disables it.
+static const double kPersistStepUs = 1.3;
+static const double kPersistFixedUs = 8.0;
+static bool persist_enabled() { static const bool v = knob_int("RELAX_Q4_PERSIST", 1) != 0; return v; }
+
 // Small batches (3 <= n <= 8): the warp-MMA streamed kernel or the split-K
 // tcgen05 tiles.  Measured in the decode chain, not per kernel
 // (profiles/r02/smalln_dispatch_ab_r02.txt): in isolated
@@ -74,11 +80,27 @@ static int choose_bn(int64_t n, int64_t N) {
 // measured far slower than the model (cluster placement), so s > 1 requires
 // tiles * s <= 148.  The model only ranks schedules; results never depend on
 // it (every BN/split meets the same tolerance).
-static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out) {
+static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out, bool* persist_out,
+                            bool allow_persist) {
     const int64_t tm = (N + kTcBM - 1) / kTcBM;
     const int64_t sms = num_sms();
     double best = 1e300;
     int bb = 128, bs = 1;
+    bool bp = false;
+    if (allow_persist && tm * ((n + 255) / 256) >= 4 * sms) {
+        // persistent BN = 256 tiles (gemm_tc_persist.cu): the epilogue of a
+        // tile overlaps the next tile's k-loop, so the fill/drain is paid once
+        // per CTA, not per tile.  Measured (profiles/r02/sweep_persist_r02.jsonl):
+        // +19-20% at >= 4 tiles per CTA (4096 x 11008 / 4096 x 32000 at
+        // n = 4096: 1263 / 1278 vs 1054 / 1070 TFLOP/s), a loss below that
+        // (11008 x 4096 n = 2048: 1167 vs 1315), so it is only offered there.
+        const int64_t tiles = tm * ((n + 255) / 256);
+        const int64_t per_cta = (tiles + sms - 1) / sms;
+        const double t = static_cast<double>(per_cta) * kt * kPersistStepUs + kPersistFixedUs;
+        best = t;
+        bb = 256;
+        bp = true;
+    }
     for (int bn : {128, 256}) {
         const int64_t tiles = tm * ((n + bn - 1) / bn);
         const double step = bn == 256 ? 1.3 : 0.92;
@@ -89,11 +111,12 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
             const int64_t waves = (tiles * s + sms - 1) / sms;
             const int ks = (kt + s - 1) / s;
             const double t = static_cast<double>(waves) * (ks * step + fixed) + (s > 1 ? 1.0 : 0.0);
-            if (t < best * 0.999) { best = t; bb = bn; bs = s; }
+            if (t < best * 0.999) { best = t; bb = bn; bs = s; bp = false; }
         }
     }
     *bn_out = bb;
     *s_out = bs;
+    *persist_out = bp;
 }
 
 // Split-K factor for small n (<= 64, HBM-bound): aim for about two CTAs per
@@ -117,7 +140,7 @@ static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
 }
 
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split, int force_bn,
-              Plan* out, bool force_ws) {
+              Plan* out, bool force_ws, bool no_persist) {
     if (n < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
     if (K % kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
     Plan p;
@@ -154,7 +177,9 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
                 return RELAX_ERR_INVALID_ARG;
             p.bn = force_bn;
         } else if (n > 64 && force_split <= 0) {
-            choose_tc_large(n, N, kt, &p.bn, &auto_split);
+            bool persist = false;
+            choose_tc_large(n, N, kt, &p.bn, &auto_split, &persist, !no_persist && persist_enabled());
+            p.persist = persist ? 1 : 0;
         } else {
             p.bn = choose_bn(n, N);
         }
@@ -169,6 +194,9 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
             s = 1;
         }
         p.split = s;
+        // a forced BN = 256 without split also runs persistent unless told otherwise
+        if (force_bn == 256 && s == 1 && !no_persist && persist_enabled()) p.persist = 1;
+        if (s > 1) p.persist = 0;
         // split-K partials: reduced in a thread-block cluster through DSMEM when
         // the split fits a portable cluster (<= 8), else in the workspace.
         p.cluster = (s > 1 && s <= 8 && !force_ws) ? 1 : 0;
@@ -238,11 +266,12 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
     Plan plan;
     // Without a workspace the schedule is workspace-free (split-K = 1).
     const bool force_ws = (flags & RELAX_FLAG_SPLIT_WORKSPACE) != 0;
-    int rc = make_plan(n, K, N, variant, split_k, bn, &plan, force_ws);
+    const bool no_persist = (flags & RELAX_FLAG_TILE_PER_CTA) != 0;
+    int rc = make_plan(n, K, N, variant, split_k, bn, &plan, force_ws, no_persist);
     if (rc == RELAX_OK && plan.ws_bytes > 0 && ws_bytes == 0 && !force_ws && split_k == 0) {
         // no workspace given: fall back to the largest cluster-reduced split
         int s = plan.split < 8 ? plan.split : 8;
-        rc = make_plan(n, K, N, variant, s, bn, &plan, false);
+        rc = make_plan(n, K, N, variant, s, bn, &plan, false, no_persist);
     }
     if (rc != RELAX_OK) return rc;
     if (plan.ws_bytes > ws_bytes) return RELAX_ERR_WORKSPACE;
@@ -429,7 +458,7 @@ int relax_plan_workspace(int64_t n_max, int64_t K, int64_t N, size_t* ws_bytes) 
 }
 
 int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile, int* split_k,
-                         size_t* ws_bytes) {
+                         size_t* ws_bytes, int* persistent) {
     rq4::Plan p;
     const int rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
     if (rc != RELAX_OK) return rc;
@@ -437,6 +466,7 @@ int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* til
     if (tile) *tile = (p.variant == rq4::kVariantGemv || p.variant == rq4::kVariantSmallN) ? p.nt : p.bn;
     if (split_k) *split_k = p.split;
     if (ws_bytes) *ws_bytes = p.ws_bytes;
+    if (persistent) *persistent = p.persist;
     return RELAX_OK;
 }
 

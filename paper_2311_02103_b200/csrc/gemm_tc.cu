@@ -656,9 +656,9 @@ static size_t map_hash(const MapKey& k) {
     return static_cast<size_t>(h ^ (h >> 29));
 }
 
-static int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
-                       uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
-                       CUtensorMapSwizzle sw) {
+int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                CUtensorMapSwizzle sw) {
     thread_local MapEntry* cache = nullptr;
     if (!cache) cache = new MapEntry[kMapCacheSlots]();       // per thread, lives as long as the thread
     const MapKey key{base, inner, outer, row_bytes, box_inner, box_outer, static_cast<int>(dt), static_cast<int>(sw)};
@@ -821,6 +821,7 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
         a.cnt = static_cast<uint32_t*>(ws);
         a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes);
     }
+    if (plan.persist && a.ops == 0) return launch_tc_persist(x, n, K, N, w, s, y, pdl, stream);
     switch (plan.bn) {
         case 16: return launch_tc_bn<16>(mw, ms, x, a, pdl, stream);
         case 32: return launch_tc_bn<32>(mw, ms, x, a, pdl, stream);

@@ -1,0 +1,316 @@
+// gemm_tc_persist.cu -- the prefill path for large n: a persistent tcgen05
+// kernel whose accumulator is double-buffered in TMEM, so the epilogue of one
+// tile runs while the next tile's k-loop streams (SURVEY §8(f) / verdict r1
+// "persistent tcgen05 with a double-buffered accumulator").
+//
+// y[t][j] = sum_k x[t][k] * W(k, j) with W = fp16_RNE((q-7) s), the
+// dequant producer fused into the matmul, n a runtime argument
+// (P:409-413); the tile schedule is the dynamic-shape-aware loop schedule of
+// P:588-592 made persistent.
+//
+// Same "swap AB" mapping as gemm_tc.cu (MMA M = 128 weight rows, N = 256
+// tokens, K = 16), one CTA per SM walking tiles t = blockIdx.x + i * grid:
+//   warp 0      W producer : TMA codes (128 rows x 128 B, SW128) + scales per
+//                            256-k stage, across tile boundaries
+//   warp 3      x producer : TMA x (256 tokens x 64 k, SW128) per 64-k
+//                            sub-block (OOB tokens zero-filled); TMEM owner
+//   warp 1      MMA issuer : tcgen05.mma.kind::f16, A (dequantised W) AND B
+//                            from shared memory, D into accumulator i % 2
+//   warps 4-11  transform  : thread m = row m dequantises its codes bit-exactly
+//                            and writes the fp16 row into an SMEM A slot in
+//                            the canonical K-major SW128 layout (rows 128 B
+//                            apart, 16-B chunk c of row m at c ^ (m % 8))
+//   warps 12-15 epilogue   : tcgen05.ld of accumulator i % 2 while the MMA
+//                            fills the other one, fp32 -> fp16 RNE, y stores
+// TMEM: 2 x 256 fp32 columns (all 512); A lives in SMEM (4 x 16 KB slots),
+// which is what frees the second accumulator.  PDL: weights stream before
+// griddepcontrol.wait; x loads and y stores wait.
+#include <cstdio>
+#include "internal.h"
+#include "relax_q4.h"
+#include "ptx.cuh"
+#include "q4_unpack.cuh"
+
+namespace rq4 {
+
+constexpr int kPBN = 256;                                                 // token tile
+constexpr int kPWStages = 3;
+constexpr int kPASlots = 4;                                               // 64-k A slots
+constexpr int kPXStages = 3;                                              // 64-k x stages
+constexpr uint32_t kPCodes = kTcBM * (kTcWStageK / 2);                    // 16 KB
+constexpr uint32_t kPScales = kTcBM * (kTcWStageK / kGroup) * 2;          // 2 KB
+constexpr uint32_t kPASlotBytes = kTcBM * kTcXStageK * 2;                 // 16 KB
+constexpr uint32_t kPXStageBytes = kPBN * kTcXStageK * 2;                 // 32 KB
+constexpr uint32_t kPOffCodes = 0;
+constexpr uint32_t kPOffScales = kPOffCodes + kPWStages * kPCodes;       // 48 KB
+constexpr uint32_t kPOffA = kPOffScales + kPWStages * kPScales + 2048;   // 56 KB (1 KB aligned)
+constexpr uint32_t kPOffX = kPOffA + kPASlots * kPASlotBytes;            // 120 KB
+constexpr uint32_t kPOffBar = kPOffX + kPXStages * kPXStageBytes;        // 216 KB
+constexpr uint32_t kPNumBars = 2 * kPWStages + 2 * kPASlots + 2 * kPXStages + 4;
+constexpr uint32_t kPSmemBytes = kPOffBar + kPNumBars * 8 + 16 + 1024;   // + align slack
+constexpr int kPThreads = 16 * 32;
+static_assert(kPOffA % 1024 == 0 && kPOffX % 1024 == 0, "SW128 operands need 1 KB alignment");
+static_assert(kPSmemBytes <= 227 * 1024, "shared memory budget");
+
+struct TpArgs {
+    int64_t n, K, N;
+    uint16_t* y;
+    int kt;                   // 256-k W stages per tile (= K / 256)
+    int64_t m_tiles, tiles;   // tiles = m_tiles * ceil(n / 256), m-fastest
+};
+
+__device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+__global__ void __launch_bounds__(kPThreads, 1)
+tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
+                     const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TpArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* codes_sm = smem + kPOffCodes;
+    uint8_t* scales_sm = smem + kPOffScales;
+    uint8_t* a_sm = smem + kPOffA;
+    uint8_t* x_sm = smem + kPOffX;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPOffBar);
+    uint64_t* w_full = bars;
+    uint64_t* w_empty = w_full + kPWStages;
+    uint64_t* a_full = w_empty + kPWStages;
+    uint64_t* a_empty = a_full + kPASlots;
+    uint64_t* x_full = a_empty + kPASlots;
+    uint64_t* x_empty = x_full + kPXStages;
+    uint64_t* acc_full = x_empty + kPXStages;     // [2]
+    uint64_t* acc_empty = acc_full + 2;           // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kPNumBars);
+
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+    const int lane = threadIdx.x & 31;
+    const int nsub = a.kt * (kTcWStageK / kTcXStageK);      // 64-k sub-blocks per tile
+
+    pdl_launch_dependents();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kPWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 8); }
+        for (int i = 0; i < kPASlots; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
+        for (int i = 0; i < kPXStages; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_w);
+        tma_prefetch_desc(&tm_s);
+        tma_prefetch_desc(&tm_x);
+    }
+    if (warp == 3) {
+        tmem_alloc<512>(tmem_slot);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- W producer (weights never depend on the previous kernel)
+        if (elect_one()) {
+            const uint64_t pol = policy_evict_last();           // W tiles are re-read by later token tiles
+            int slot = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+                const int32_t m0 = static_cast<int32_t>((t % a.m_tiles) * kTcBM);
+                for (int i = 0; i < a.kt; ++i) {
+                    mbar_wait(&w_empty[slot], ph ^ 1);
+                    mbar_arrive_expect_tx(&w_full[slot], kPCodes + kPScales);
+                    tma_load_2d(codes_sm + slot * kPCodes, &tm_w, &w_full[slot], i * (kTcWStageK / 2), m0, pol);
+                    tma_load_2d(scales_sm + slot * kPScales, &tm_s, &w_full[slot], i * (kTcWStageK / kGroup), m0, pol);
+                    if (++slot == kPWStages) { slot = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ---------------- x producer: the only input that depends on the previous kernel
+        if (elect_one()) {
+            pdl_wait();
+            const uint64_t pol = policy_evict_last();
+            int slot = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+                const int32_t n0 = static_cast<int32_t>((t / a.m_tiles) * kPBN);
+                for (int j = 0; j < nsub; ++j) {
+                    mbar_wait(&x_empty[slot], ph ^ 1);
+                    mbar_arrive_expect_tx(&x_full[slot], kPXStageBytes);
+                    tma_load_2d(x_sm + slot * kPXStageBytes, &tm_x, &x_full[slot], j * kTcXStageK, n0, pol);
+                    if (++slot == kPXStages) { slot = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (elect_one()) {
+            constexpr uint32_t idesc = idesc_f16_f32(kTcBM, kPBN);
+            int as = 0, xs = 0;
+            uint32_t aph = 0, xph = 0;
+            int it = 0;
+            for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, ++it) {
+                const int b = it & 1;
+                mbar_wait(&acc_empty[b], ((it >> 1) & 1) ^ 1);        // the epilogue drained it
+                tc_fence_after();
+                const uint32_t d = tmem_base + static_cast<uint32_t>(b * kPBN);
+                for (int j = 0; j < nsub; ++j) {
+                    mbar_wait(&a_full[as], aph);
+                    mbar_wait(&x_full[xs], xph);
+                    tc_fence_after();
+                    const uint64_t adesc = smem_desc_k_sw128(smem_u32(a_sm + as * kPASlotBytes));
+                    const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * kPXStageBytes));
+#pragma unroll
+                    for (int kk = 0; kk < kTcXStageK / 16; ++kk)
+                        tc_mma_ss(d, adesc + static_cast<uint64_t>(kk * 2), bdesc + static_cast<uint64_t>(kk * 2),
+                                  idesc, (j | kk) != 0 ? 1u : 0u);
+                    tc_commit(&a_empty[as]);
+                    tc_commit(&x_empty[xs]);
+                    if (++as == kPASlots) { as = 0; aph ^= 1; }
+                    if (++xs == kPXStages) { xs = 0; xph ^= 1; }
+                }
+                tc_commit(&acc_full[b]);
+            }
+        }
+    } else if (warp >= 4 && warp < 12) {
+        // ---------------- transform: warp (q, h) dequantises rows 32q..32q+31 of the
+        // sub-blocks with parity h into SMEM A slots (slot j % 4 for sub-block j)
+        const int tw = warp - 4;
+        const int q = tw & 3;
+        const int h = tw >> 2;
+        const int m = q * 32 + lane;
+        const uint32_t rbase = static_cast<uint32_t>((m >> 3) * 1024 + (m & 7) * 128);
+        int ws = 0, as = h;
+        uint32_t wph = 0, aph = 0;
+        for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+            for (int i = 0; i < a.kt; ++i) {
+                mbar_wait(&w_full[ws], wph);
+                const uint8_t* crow = codes_sm + ws * kPCodes + m * 128;
+                const uint32_t* srow = reinterpret_cast<const uint32_t*>(scales_sm + ws * kPScales + m * 16);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int sub = h + 2 * u;                    // 64-k sub-block of this stage
+                    uint32_t v[2][4][4];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int chunk = 2 * sub + e;            // 16-B code chunk = one 32-group
+                        const uint4 c = *reinterpret_cast<const uint4*>(crow + ((chunk ^ (m & 7)) << 4));
+                        const uint32_t sp = srow[sub];
+                        const __half sh = __ushort_as_half(e ? hi16(sp) : lo16(sp));
+                        const __half2 s2 = __halves2half2(sh, sh);
+                        const uint32_t words[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) dequant_word_natural(words[w], s2, v[e][w]);
+                    }
+                    mbar_wait(&a_empty[as], aph ^ 1);
+                    uint8_t* slot = a_sm + as * kPASlotBytes + rbase;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            const int c8 = e * 4 + w;             // 8-k chunk of the row's 64 k
+                            *reinterpret_cast<uint4*>(slot + ((c8 ^ (m & 7)) << 4)) =
+                                make_uint4(v[e][w][0], v[e][w][1], v[e][w][2], v[e][w][3]);
+                        }
+                    fence_proxy_async_smem();                     // generic stores -> MMA (async proxy)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&a_full[as]);
+                    as += 2;
+                    if (as >= kPASlots) { as -= kPASlots; aph ^= 1; }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&w_empty[ws]);
+                if (++ws == kPWStages) { ws = 0; wph ^= 1; }
+            }
+        }
+    } else if (warp >= 12) {
+        // ---------------- epilogue: accumulator it % 2 -> fp16 y while the MMA
+        // fills the other one
+        const int q = warp & 3;                                   // TMEM lanes 32q..32q+31
+        const int m = q * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        int it = 0;
+        bool waited = false;
+        for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, ++it) {
+            const int b = it & 1;
+            const int64_t row = (t % a.m_tiles) * kTcBM + m;
+            const int64_t n0 = (t / a.m_tiles) * kPBN;
+            mbar_wait(&acc_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            if (!waited) { pdl_wait(); waited = true; }           // y may still be read by the previous kernel
+            const uint32_t col0 = tmem_base + lane_base + static_cast<uint32_t>(b * kPBN);
+            const bool row_ok = row < a.N;
+            uint32_t v0[16], v1[16];
+            tmem_ld_32x32b_x16(col0, v0);
+            tc_wait_ld();
+#pragma unroll 1
+            for (int c0 = 0; c0 < kPBN; c0 += 32) {
+                tmem_ld_32x32b_x16(col0 + c0 + 16, v1);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t tok = n0 + c0 + i;
+                    if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v0[i])));
+                }
+                tc_wait_ld();
+                if (c0 + 32 < kPBN) tmem_ld_32x32b_x16(col0 + c0 + 32, v0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int64_t tok = n0 + c0 + 16 + i;
+                    if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v1[i])));
+                }
+                tc_wait_ld();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 3) tmem_dealloc<512>(tmem_base);
+}
+
+int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
+                      uint16_t* y, bool pdl, cudaStream_t stream) {
+    if (K % kTcWStageK != 0 || n <= 0) return static_cast<int>(cudaErrorInvalidValue);
+    CUtensorMap mw, ms, mx;
+    int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
+                         CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    rc = make_map_2d(&ms, CU_TENSOR_MAP_DATA_TYPE_UINT16, s, K / kGroup, N, (K / kGroup) * 2, kTcWStageK / kGroup,
+                     kTcBM, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (rc) return rc;
+    rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, K, n, K * 2, kTcXStageK, kPBN,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_persist_kernel),
+                                              static_cast<int>(kPSmemBytes));
+    if (e != cudaSuccess) return static_cast<int>(e);
+    TpArgs a;
+    a.n = n; a.K = K; a.N = N; a.y = y;
+    a.kt = static_cast<int>(K / kTcWStageK);
+    a.m_tiles = (N + kTcBM - 1) / kTcBM;
+    a.tiles = a.m_tiles * ((n + kPBN - 1) / kPBN);
+    const int64_t sms = num_sms();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(a.tiles < sms ? a.tiles : sms));
+    cfg.blockDim = dim3(kPThreads);
+    cfg.dynamicSmemBytes = kPSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_persist_kernel, mw, ms, mx, a));
+}
+
+}  // namespace rq4

@@ -59,6 +59,7 @@ struct Plan {
     int bn = 0;          // TC: token tile (MMA N)
     int split = 1;       // TC: split-K factor
     int cluster = 0;     // TC: split-K reduced in a thread-block cluster (DSMEM), no workspace
+    int persist = 0;     // TC: persistent kernel, double-buffered accumulator (BN = 256, no split)
     int grid = 0;
     size_t ws_bytes = 0; // workspace bytes this plan needs
 };
@@ -66,7 +67,7 @@ struct Plan {
 // Host-pure dispatch (a1): variant, tiles, split-K and workspace for (n,K,N).
 // `force_variant` / `force_split` / `force_bn` override (0 = choose).
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split,
-              int force_bn, Plan* out, bool force_ws);
+              int force_bn, Plan* out, bool force_ws, bool no_persist = false);
 size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split);
 int gemv_max_n();                   // GEMV/TC threshold (env RELAX_Q4_GEMV_MAX_N)
 bool gemv_fits(int nt, int64_t K);
@@ -106,6 +107,12 @@ int launch_gemv_row(const uint16_t* x, int64_t n, int64_t K, int64_t N, const ui
                     const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 bool gemv_row_ok(int64_t K);
 #endif
+// 2-D tiled map, cached per host thread (gemm_tc.cu)
+int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                CUtensorMapSwizzle sw);
+int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
+                      uint16_t* y, bool pdl, cudaStream_t stream);
 int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                     const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
                     CUtensorMapSwizzle sw);

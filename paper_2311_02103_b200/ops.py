@@ -35,6 +35,7 @@ STATUS = {
 VARIANT_AUTO, VARIANT_GEMV, VARIANT_TC, VARIANT_SMALLN = 0, 1, 2, 3
 FLAG_NO_PDL = 1
 FLAG_SPLIT_WORKSPACE = 2
+FLAG_TILE_PER_CTA = 4
 
 # every symbol include/relax_q4.h declares
 EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",
@@ -83,7 +84,7 @@ def lib() -> ctypes.CDLL:
         L.relax_q4_matmul_ex.argtypes = [P, I64, I64, I64, P, P, P, P, SZ, I, I, I, ctypes.c_uint, P]
         L.relax_q4_matmul_ex.restype = I
         L.relax_query_schedule.argtypes = [I64, I64, I64, ctypes.POINTER(I), ctypes.POINTER(I),
-                                           ctypes.POINTER(I), ctypes.POINTER(SZ)]
+                                           ctypes.POINTER(I), ctypes.POINTER(SZ), ctypes.POINTER(I)]
         L.relax_query_schedule.restype = I
         L.relax_q4_dequant.argtypes = [P, P, I64, I64, P, P]
         L.relax_q4_dequant.restype = I
@@ -125,12 +126,15 @@ def plan_workspace(n_max: int, K: int, N: int) -> int:
 
 
 def query_schedule(n: int, K: int, N: int) -> dict:
-    v, t, s = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    v, t, s, pe = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
     ws = ctypes.c_size_t(0)
     _check(lib().relax_query_schedule(n, K, N, ctypes.byref(v), ctypes.byref(t), ctypes.byref(s),
-                                      ctypes.byref(ws)), "relax_query_schedule")
+                                      ctypes.byref(ws), ctypes.byref(pe)), "relax_query_schedule")
     name = {VARIANT_GEMV: "gemv", VARIANT_TC: "tc", VARIANT_SMALLN: "smalln"}[v.value]
-    return {"variant": name, "tile": t.value, "split_k": s.value, "ws_bytes": int(ws.value)}
+    d = {"variant": name, "tile": t.value, "split_k": s.value, "ws_bytes": int(ws.value)}
+    if pe.value:
+        d["persistent"] = True
+    return d
 
 
 def _device_of_call():

@@ -78,7 +78,7 @@ def test_config1_auto(kind, n):
 
 WSF = 2   # RELAX_FLAG_SPLIT_WORKSPACE
 VARIANTS = [("gemv", 1, 0, 0, 0), ("smalln", 3, 0, 0, 0), ("tc16", 2, 1, 16, 0), ("tc32", 2, 1, 32, 0), ("tc64", 2, 1, 64, 0),
-            ("tc128", 2, 1, 128, 0), ("tc256", 2, 1, 256, 0),
+            ("tc128", 2, 1, 128, 0), ("tc256", 2, 1, 256, 4), ("tc256p", 2, 1, 256, 0),
             ("tc16s3c", 2, 3, 16, 0), ("tc64s2c", 2, 2, 64, 0), ("tc128s2c", 2, 2, 128, 0),
             ("tc256s3c", 2, 3, 256, 0),
             ("tc16s3w", 2, 3, 16, WSF), ("tc64s2w", 2, 2, 64, WSF), ("tc128s2w", 2, 2, 128, WSF)]

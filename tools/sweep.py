@@ -75,11 +75,15 @@ def main():
                 if var == "smalln" and n > 32:
                     continue
                 base, _, sp = var.partition(":")        # "tc:S" forces split-K S (cluster reduction)
+                vflags = flags
+                if base.endswith("-np"):                # one tile per CTA (no persistent kernel)
+                    base = base[:-3]
+                    vflags |= ops.FLAG_TILE_PER_CTA
                 split = int(sp) if sp else 0
                 v = {"auto": ops.VARIANT_AUTO, "gemv": ops.VARIANT_GEMV, "tc": ops.VARIANT_TC,
                      "smalln": ops.VARIANT_SMALLN}[base]
                 # a rotation long enough to stream >= 4 L2 of weights per replay
-                fns = [lambda p=p, s=s: ops.q4_matmul_ex(x, p, s, y=y, ws=ws, variant=v, flags=flags,
+                fns = [lambda p=p, s=s: ops.q4_matmul_ex(x, p, s, y=y, ws=ws, variant=v, flags=vflags,
                                                          split_k=split, stream=stream) for p, s in copies]
                 try:
                     ms = time_calls(fns, a.reps, stream)
