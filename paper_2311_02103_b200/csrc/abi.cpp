@@ -87,7 +87,8 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
     double best = 1e300;
     int bb = 128, bs = 1;
     bool bp = false;
-    if (allow_persist && tm * ((n + 255) / 256) >= 4 * sms) {
+    static const int64_t min_per_sm = knob_int("RELAX_Q4_PERSIST_MIN_TILES", 4);
+    if (allow_persist && tm * ((n + 255) / 256) >= min_per_sm * sms) {
         // persistent BN = 256 tiles (gemm_tc_persist.cu): the epilogue of a
         // tile overlaps the next tile's k-loop, so the fill/drain is paid once
         // per CTA, not per tile.  Measured (profiles/r02/sweep_persist_r02.jsonl):

@@ -9,11 +9,14 @@
 // P:588-592 made persistent.
 //
 // Same "swap AB" mapping as gemm_tc.cu (MMA M = 128 weight rows, N = 256
-// tokens, K = 16), one CTA per SM walking tiles t = blockIdx.x + i * grid:
+// tokens, K = 16), one CTA per SM, CTA pairs (thread-block clusters of 2)
+// walking pair tiles p = cluster + i * clusters (two m-tiles of one token
+// tile; each CTA loads half of every x stage and multicasts it to both):
 //   warp 0      W producer : TMA codes (128 rows x 128 B, SW128) + scales per
 //                            256-k stage, across tile boundaries
-//   warp 3      x producer : TMA x (256 tokens x 64 k, SW128) per 64-k
-//                            sub-block (OOB tokens zero-filled); TMEM owner
+//   warp 3      x producer : TMA x (its 128 of the 256 tokens x 64 k, SW128,
+//                            multicast to the pair) per 64-k sub-block (OOB
+//                            tokens zero-filled); TMEM owner
 //   warp 1      MMA issuer : tcgen05.mma.kind::f16, A (dequantised W) AND B
 //                            from shared memory, D into accumulator i % 2
 //   warps 4-11  transform  : thread m = row m dequantises its codes bit-exactly
@@ -56,7 +59,7 @@ struct TpArgs {
     int64_t n, K, N;
     uint16_t* y;
     int kt;                   // 256-k W stages per tile (= K / 256)
-    int64_t m_tiles, tiles;   // tiles = m_tiles * ceil(n / 256), m-fastest
+    int64_t m_tiles, tiles;   // m-tile pairs, and pair tiles = m_tiles * ceil(n / 256), pairs fastest
 };
 
 __device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -66,6 +69,22 @@ __device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
         :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+// x tile load multicast to both CTAs of the pair (same SMEM offset and
+// mbarrier in each; every destination's barrier receives the bytes).
+__device__ __forceinline__ void tma_load_2d_mc(void* smem_dst, const void* desc, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;"
+        :: "r"(smem_u32(smem_dst)), "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+        : "memory");
+}
+// Arrive on the same mbarrier of every CTA in `mask` once this thread's prior MMAs complete.
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 :: "r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
 __global__ void __launch_bounds__(kPThreads, 1)
@@ -91,12 +110,19 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
     const int nsub = a.kt * (kTcWStageK / kTcXStageK);      // 64-k sub-blocks per tile
+    // CTA pairs (clusters of 2) share each token tile: pair p covers m-tiles
+    // 2 (p % m_pairs) + {0, 1} of token tile p / m_pairs; each CTA loads half
+    // of every x stage and multicasts it to both, halving the L2 -> SM traffic
+    // of x, which bounds this kernel (x is re-read once per m-tile).
+    const uint32_t rank = cluster_ctarank();
+    const int64_t cid = blockIdx.x >> 1, nclu = gridDim.x >> 1;
 
     pdl_launch_dependents();
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 8); }
         for (int i = 0; i < kPASlots; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
-        for (int i = 0; i < kPXStages; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+        // x_empty collects one MMA commit from each CTA of the pair
+        for (int i = 0; i < kPXStages; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 2); }
         for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
         fence_mbar_init();
     }
@@ -111,6 +137,8 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     }
     tc_fence_before();
     __syncthreads();
+    cluster_arrive_release();
+    cluster_wait_acquire();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -120,8 +148,8 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
             const uint64_t pol = policy_evict_last();           // W tiles are re-read by later token tiles
             int slot = 0;
             uint32_t ph = 0;
-            for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
-                const int32_t m0 = static_cast<int32_t>((t % a.m_tiles) * kTcBM);
+            for (int64_t p = cid; p < a.tiles; p += nclu) {
+                const int32_t m0 = static_cast<int32_t>((2 * (p % a.m_tiles) + rank) * kTcBM);
                 for (int i = 0; i < a.kt; ++i) {
                     mbar_wait(&w_empty[slot], ph ^ 1);
                     mbar_arrive_expect_tx(&w_full[slot], kPCodes + kPScales);
@@ -138,12 +166,13 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
             const uint64_t pol = policy_evict_last();
             int slot = 0;
             uint32_t ph = 0;
-            for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
-                const int32_t n0 = static_cast<int32_t>((t / a.m_tiles) * kPBN);
+            for (int64_t p = cid; p < a.tiles; p += nclu) {
+                const int32_t n0 = static_cast<int32_t>((p / a.m_tiles) * kPBN + rank * (kPBN / 2));
                 for (int j = 0; j < nsub; ++j) {
-                    mbar_wait(&x_empty[slot], ph ^ 1);
-                    mbar_arrive_expect_tx(&x_full[slot], kPXStageBytes);
-                    tma_load_2d(x_sm + slot * kPXStageBytes, &tm_x, &x_full[slot], j * kTcXStageK, n0, pol);
+                    mbar_wait(&x_empty[slot], ph ^ 1);                // both CTAs released the slot
+                    mbar_arrive_expect_tx(&x_full[slot], kPXStageBytes);     // own half + the peer's half
+                    tma_load_2d_mc(x_sm + slot * kPXStageBytes + rank * (kPXStageBytes / 2), &tm_x, &x_full[slot],
+                                   j * kTcXStageK, n0, 0x3, pol);
                     if (++slot == kPXStages) { slot = 0; ph ^= 1; }
                 }
             }
@@ -155,7 +184,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
             int as = 0, xs = 0;
             uint32_t aph = 0, xph = 0;
             int it = 0;
-            for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, ++it) {
+            for (int64_t p = cid; p < a.tiles; p += nclu, ++it) {
                 const int b = it & 1;
                 mbar_wait(&acc_empty[b], ((it >> 1) & 1) ^ 1);        // the epilogue drained it
                 tc_fence_after();
@@ -171,7 +200,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                         tc_mma_ss(d, adesc + static_cast<uint64_t>(kk * 2), bdesc + static_cast<uint64_t>(kk * 2),
                                   idesc, (j | kk) != 0 ? 1u : 0u);
                     tc_commit(&a_empty[as]);
-                    tc_commit(&x_empty[xs]);
+                    tc_commit_mc(&x_empty[xs], 0x3);                  // release the slot in both CTAs
                     if (++as == kPASlots) { as = 0; aph ^= 1; }
                     if (++xs == kPXStages) { xs = 0; xph ^= 1; }
                 }
@@ -188,7 +217,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
         const uint32_t rbase = static_cast<uint32_t>((m >> 3) * 1024 + (m & 7) * 128);
         int ws = 0, as = h;
         uint32_t wph = 0, aph = 0;
-        for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+        for (int64_t p = cid; p < a.tiles; p += nclu) {
             for (int i = 0; i < a.kt; ++i) {
                 mbar_wait(&w_full[ws], wph);
                 const uint8_t* crow = codes_sm + ws * kPCodes + m * 128;
@@ -237,10 +266,10 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int it = 0;
         bool waited = false;
-        for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, ++it) {
+        for (int64_t p = cid; p < a.tiles; p += nclu, ++it) {
             const int b = it & 1;
-            const int64_t row = (t % a.m_tiles) * kTcBM + m;
-            const int64_t n0 = (t / a.m_tiles) * kPBN;
+            const int64_t row = (2 * (p % a.m_tiles) + rank) * kTcBM + m;
+            const int64_t n0 = (p / a.m_tiles) * kPBN;
             mbar_wait(&acc_full[b], (it >> 1) & 1);
             tc_fence_after();
             if (!waited) { pdl_wait(); waited = true; }           // y may still be read by the previous kernel
@@ -274,6 +303,8 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
 
     tc_fence_before();
     __syncthreads();
+    cluster_arrive_release();          // the peer may still multicast into / commit onto this CTA
+    cluster_wait_acquire();
     tc_fence_after();
     if (warp == 3) tmem_dealloc<512>(tmem_base);
 }
@@ -288,28 +319,32 @@ int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
     rc = make_map_2d(&ms, CU_TENSOR_MAP_DATA_TYPE_UINT16, s, K / kGroup, N, (K / kGroup) * 2, kTcWStageK / kGroup,
                      kTcBM, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
-    rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, K, n, K * 2, kTcXStageK, kPBN,
+    rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, K, n, K * 2, kTcXStageK, kPBN / 2,
                      CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
     const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_persist_kernel),
-                                              static_cast<int>(kPSmemBytes));
+                                              static_cast<int>(kPSmemBytes), true);
     if (e != cudaSuccess) return static_cast<int>(e);
     TpArgs a;
     a.n = n; a.K = K; a.N = N; a.y = y;
     a.kt = static_cast<int>(K / kTcWStageK);
-    a.m_tiles = (N + kTcBM - 1) / kTcBM;
-    a.tiles = a.m_tiles * ((n + kPBN - 1) / kPBN);
-    const int64_t sms = num_sms();
+    a.m_tiles = ((N + kTcBM - 1) / kTcBM + 1) / 2;             // m-tile PAIRS (an odd last one is zero-filled)
+    a.tiles = a.m_tiles * ((n + kPBN - 1) / kPBN);              // pair tiles
+    const int64_t clusters = num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(a.tiles < sms ? a.tiles : sms));
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * (a.tiles < clusters ? a.tiles : clusters)));
     cfg.blockDim = dim3(kPThreads);
     cfg.dynamicSmemBytes = kPSmemBytes;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_persist_kernel, mw, ms, mx, a));
 }
 
