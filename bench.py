@@ -62,6 +62,10 @@ def load_peaks():
             "src": "fallback"}
 
 
+# (query heads, kv heads) of each model; head_dim 128
+HEADS = {"llama2-7b": (32, 32), "llama2-13b": (40, 40), "llama2-70b": (64, 8)}
+
+
 def layer_set(workload: str, fused: bool = False, tp: int = 1):
     """The linears of one token.  fused=True stacks the rows of q/k/v and of
     gate/up (the NK layout makes that a concatenation) into one call each --
@@ -153,16 +157,37 @@ def block_step(args, mats, weights, n, dev, stream):
     """Decoder-block chain over the fused-layout linears:
     per layer  qkv = W_qkv . RMSNorm(h);  h += W_o . a;  act = SiLU(g) * u with
     [g; u] = W_gate_up . RMSNorm(h);  h += W_down . act;  then logits =
-    W_head . RMSNorm(h).  Attention itself is out of scope: `a` is a fixed
-    fp16 tensor standing in for its output.  --block fused runs each linear
+    W_head . RMSNorm(h).  Without --kv the attention is a fixed fp16 tensor `a`
+    standing in for its output; with --kv L (fused block, n = 1) it is the
+    library's decode attention: the new token's k, v (slices
+    of the qkv output) appended at position L - 1 of the layer's fp16 KV cache
+    (relax_kv_append) and q attending over the L cached keys
+    (relax_attn_decode) -- the whole decode step, attention over a symbolic KV
+    length included (RoPE is not applied: it does not change what is read or
+    computed per byte).  --block fused runs each linear
     with its neighbours fused (relax_q4_matmul_fused: 4 kernels per layer,
     gate/up rows interleaved); --block unfused runs the same linears through
     relax_q4_matmul with the element-wise ops as separate torch kernels (the
-    unfused program)."""
+    unfused program: our matmuls + torch eager glue, not launched with PDL)."""
     import torch
     from paper_2311_02103_b200 import ops
     model = args.workload.rsplit("-", 1)[0]
     hidden = inputs.LLAMA_SETS[model]["mats"][0][1]
+    hq, hkv = HEADS[model]
+    kv = None
+    if args.kv > 0:
+        if args.block != "fused" or n != 1:
+            raise SystemExit("--kv needs --block fused at n = 1 (the qkv output slices are the new q, k, v)")
+        L = args.kv
+        g = torch.Generator(device=dev)
+        g.manual_seed(11)
+        nl = sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))
+        kv = {"k": [torch.randn((1, hkv, L, 128), generator=g, device=dev).half() for _ in range(nl)],
+              "v": [torch.randn((1, hkv, L, 128), generator=g, device=dev).half() for _ in range(nl)],
+              "lens": torch.tensor([L], dtype=torch.int32, device=dev),
+              "pos": torch.tensor([L - 1], dtype=torch.int32, device=dev),
+              "out": torch.empty((1, hq, 128), dtype=torch.float16, device=dev)}
+        kv["ws"] = torch.empty(ops.attn_decode_workspace(1, hq, L), dtype=torch.uint8, device=dev)
     h0 = torch.from_numpy(inputs.activations(3, n, hidden).view(np.float16)).to(dev)
     h = h0.clone()
     attn = torch.from_numpy(inputs.activations(4, n, hidden).view(np.float16)).to(dev)
@@ -189,14 +214,25 @@ def block_step(args, mats, weights, n, dev, stream):
     def step():
         h.copy_(h0)                                      # every step decodes the same token
         act = None
+        li = 0
         for (name, K, N), (pk, sc) in zip(mats, weights):
             kind = name.split(".")[-1]
             if args.block == "fused":
                 if kind in ("qkv", "lm_head"):
                     ops.q4_matmul_fused(h, pk, sc, y=outs[name], rms_weight=gamma, rms_eps=eps, ws=wss[name],
                                         stream=stream)
+                    if kind == "qkv" and kv is not None:
+                        y = outs[name]
+                        qv = y[:, :hq * 128].view(1, hq, 128)
+                        kn = y[:, hq * 128:(hq + hkv) * 128].view(1, hkv, 128)
+                        vn = y[:, (hq + hkv) * 128:].view(1, hkv, 128)
+                        ops.kv_append(kn, vn, kv["pos"], kv["k"][li], kv["v"][li], stream=stream)
+                        ops.attn_decode(qv, kv["k"][li], kv["v"][li], kv["lens"], out=kv["out"], ws=kv["ws"],
+                                        stream=stream)
+                        li += 1
                 elif kind == "o":
-                    ops.q4_matmul_fused(attn, pk, sc, y=h, residual=h, stream=stream)
+                    a_in = attn if kv is None else kv["out"].view(1, hq * 128)
+                    ops.q4_matmul_fused(a_in, pk, sc, y=h, residual=h, stream=stream)
                 elif kind == "gate_up":
                     act = outs[name]
                     ops.q4_matmul_fused(h, pk, sc, y=act, rms_weight=gamma, rms_eps=eps, silu_mul=True,
@@ -384,6 +420,12 @@ def run_ours(args, rank, world, local_rank):
     ms_eager, host_eager_s = e2e_run(eager_step, args.steps)
 
     bytes_step, flops_step = algorithmic(mats, n)
+    if args.kv > 0:
+        # attention per layer: read L keys and values, append one of each (fp16, head_dim 128)
+        hq, hkv = HEADS[model]
+        nl = sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))
+        bytes_step += nl * (2 * args.kv * hkv * 128 * 2 + 2 * hkv * 128 * 2 + 2 * hq * 128 * 2)
+        flops_step += nl * (4 * args.kv * hq * 128)
     ms_step = ms / args.steps
     streams = 1 if tp_mode else world            # TP: the ranks decode one stream together
     tok_s = streams * n * args.steps / (ms / 1e3)
@@ -401,7 +443,8 @@ def run_ours(args, rank, world, local_rank):
     label = (args.workload + ("-fused-qkv-gateup" if fused else "")
              + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else "")
              + (f"-megatron-tp{tp_world}" if tp_mode else "")
-             + (f"-block-{args.block}" if args.block != "none" else ""))
+             + (f"-block-{args.block}" if args.block != "none" else "")
+             + (f"-attn-kv{args.kv}" if args.kv > 0 else ""))
     roof["traffic"] = traffic_per_launch(label, n)
     roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
     roof["kernel"] = ("q4_decode_stream_kernel (streamed decode GEMV)"
@@ -409,7 +452,10 @@ def run_ours(args, rank, world, local_rank):
     roof["per"] = "average over all launches of the step (every launch is this kernel family)"
     if tp_mode:
         roof["per"] += "; per GPU: each rank streams its own shards"
-    launches = sum(1 if sched[f"{K}x{N}"]["variant"] == "tc" else -(-n // 2) for _, K, N in mats)
+    per_kind = {"tc": lambda: 1, "smalln": lambda: -(-n // 8), "gemv": lambda: -(-n // 2)}
+    launches = sum(per_kind[sched[f"{K}x{N}"]["variant"]]() for _, K, N in mats)
+    if args.kv > 0:
+        launches += 3 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))   # append, partial, combine
     res = {
         "metric": METRIC,
         "value": round(tok_s, 2),
@@ -564,6 +610,9 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="tensor parallelism over the ranks even at N = 1 (one NCCL rank: exercises the "
                          "collectives of the TP step on one GPU); the default for N > 1")
+    ap.add_argument("--kv", type=int, default=0,
+                    help="with --block fused at n = 1: run the decode attention over a KV cache of this length "
+                         "in every layer (relax_kv_append + relax_attn_decode), the whole decode step")
     ap.add_argument("--block", default="none", choices=["none", "fused", "unfused"],
                     help="decoder-block chain with RMSNorm / SiLU-mul / residual fused into the linears "
                          "(fused) or as separate kernels (unfused); implies the fused q/k/v, gate/up layout")

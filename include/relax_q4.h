@@ -250,6 +250,39 @@ RELAX_API int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int
 RELAX_API int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t K, int64_t N,
                               int layout, int group, uint32_t* packed_w, void* scales, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Decode attention over a symbolic KV length ("the KV-cache
+ * context length" as a dynamic dimension; single-batch decode):
+ * the other operator of a decode step, so the whole step runs on this library
+ * (bench.py --block fused --kv L).  One query token per sequence, DESIGN.md
+ * reading 21:
+ *   q        device fp16 [batch][n_heads][head_dim]
+ *   k_cache, v_cache  device fp16 [batch][n_kv_heads][kv_len_max][head_dim]
+ *   kv_lens  device int32 [batch], 0 <= kv_lens[b] <= kv_len_max: the keys
+ *            j < kv_lens[b] of sequence b are attended (the symbolic length;
+ *            values outside the range are the caller's error and are clamped
+ *            by nothing -- keep them in range)
+ *   out      device fp16 [batch][n_heads][head_dim]
+ *   s_j = (q . k_j) / sqrt(head_dim), out = softmax(s) . V in fp32, fp16 RNE;
+ *   query head h uses kv head h / (n_heads / n_kv_heads) (grouped-query
+ *   attention); a sequence with kv_lens[b] == 0 gets out = 0.
+ * head_dim must be 128 and n_heads / n_kv_heads one of 1, 2, 4, 8.
+ * Split over 256-key chunks (flash decoding); the fp32 partials live in a
+ * caller-owned workspace of relax_attn_decode_workspace(batch, n_heads,
+ * kv_len_max) bytes (no zero-fill needed).  Deterministic.
+ * Errors: RELAX_ERR_INVALID_ARG, RELAX_ERR_UNSUPPORTED_SHAPE, RELAX_ERR_MISALIGNED,
+ * RELAX_ERR_ALIAS, RELAX_ERR_WORKSPACE, RELAX_ERR_DEVICE, RELAX_ERR_CUDA.
+ * relax_kv_append writes k_new, v_new [batch][n_kv_heads][head_dim] at
+ * position pos[b] of each sequence's cache (positions outside
+ * [0, kv_len_max) write nothing). */
+RELAX_API int relax_attn_decode_workspace(int64_t batch, int64_t n_heads, int64_t kv_len_max, size_t* ws_bytes);
+RELAX_API int relax_attn_decode(const void* q, const void* k_cache, const void* v_cache, const int32_t* kv_lens,
+                                int64_t batch, int64_t n_heads, int64_t n_kv_heads, int64_t head_dim,
+                                int64_t kv_len_max, void* out, void* workspace, size_t ws_bytes, void* stream);
+RELAX_API int relax_kv_append(const void* k_new, const void* v_new, const int32_t* pos, int64_t batch,
+                              int64_t n_kv_heads, int64_t head_dim, int64_t kv_len_max, void* k_cache,
+                              void* v_cache, void* stream);
+
 /* Static description of a status code; never NULL. */
 RELAX_API const char* relax_status_str(int status);
 

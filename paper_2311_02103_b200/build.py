@@ -30,7 +30,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "librelax_q4.so")
 
-SOURCES = ["abi.cpp", "device.cpp", "gemv.cu", "gemv_stream.cu", "smalln_mma.cu", "gemm_tc.cu", "gemm_tc_persist.cu", "fused.cu", "repack.cu"]
+SOURCES = ["abi.cpp", "device.cpp", "gemv.cu", "gemv_stream.cu", "smalln_mma.cu", "gemm_tc.cu", "gemm_tc_persist.cu", "fused.cu", "repack.cu", "attention.cu"]
 HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh", "fusion.cuh", "knobs.h"]
 EXP_DIR = os.path.join(ROOT, "experiments", "csrc")
 EXP_SOURCES = ["gemv_mma.cu", "gemv_row.cu"]

@@ -540,6 +540,83 @@ int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t 
     return RELAX_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Decode attention (F4; include/relax_q4.h).
+static int attn_shape_check(int64_t batch, int64_t Hq, int64_t Hkv, int64_t D, int64_t Lmax) {
+    if (batch < 0 || Hq <= 0 || Hkv <= 0 || D <= 0 || Lmax < 0) return RELAX_ERR_INVALID_ARG;
+    if (D != 128 || Hq % Hkv != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    const int64_t G = Hq / Hkv;
+    if (G != 1 && G != 2 && G != 4 && G != 8) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    return RELAX_OK;
+}
+
+int relax_attn_decode_workspace(int64_t batch, int64_t n_heads, int64_t kv_len_max, size_t* ws_bytes) {
+    if (!ws_bytes || batch < 0 || n_heads <= 0 || kv_len_max < 0) return RELAX_ERR_INVALID_ARG;
+    *ws_bytes = rq4::attn_workspace_bytes(batch, n_heads, kv_len_max);
+    return RELAX_OK;
+}
+
+int relax_attn_decode(const void* q, const void* k_cache, const void* v_cache, const int32_t* kv_lens,
+                      int64_t batch, int64_t n_heads, int64_t n_kv_heads, int64_t head_dim, int64_t kv_len_max,
+                      void* out, void* workspace, size_t ws_bytes, void* stream) {
+    int rc = attn_shape_check(batch, n_heads, n_kv_heads, head_dim, kv_len_max);
+    if (rc != RELAX_OK) return rc;
+    if (batch == 0) return RELAX_OK;
+    if (!q || !k_cache || !v_cache || !kv_lens || !out || (kv_len_max > 0 && !workspace)) return RELAX_ERR_INVALID_ARG;
+    if (!rq4::aligned16(q) || !rq4::aligned16(k_cache) || !rq4::aligned16(v_cache) || !rq4::aligned16(out) ||
+        (workspace && !rq4::aligned16(workspace)) || (reinterpret_cast<uintptr_t>(kv_lens) & 3u))
+        return RELAX_ERR_MISALIGNED;
+    const size_t need = rq4::attn_workspace_bytes(batch, n_heads, kv_len_max);
+    if (ws_bytes < need) return RELAX_ERR_WORKSPACE;
+    const size_t qb = static_cast<size_t>(batch * n_heads * head_dim) * 2;
+    const size_t cb = static_cast<size_t>(batch * n_kv_heads * kv_len_max * head_dim) * 2;
+    const size_t lb = static_cast<size_t>(batch) * 4;
+    if (rq4::overlap(out, qb, q, qb) || rq4::overlap(out, qb, k_cache, cb) || rq4::overlap(out, qb, v_cache, cb) ||
+        rq4::overlap(out, qb, kv_lens, lb) || rq4::overlap(out, qb, workspace, need) ||
+        rq4::overlap(workspace, need, q, qb) || rq4::overlap(workspace, need, k_cache, cb) ||
+        rq4::overlap(workspace, need, v_cache, cb) || rq4::overlap(workspace, need, kv_lens, lb))
+        return RELAX_ERR_ALIAS;
+    rc = rq4::check_device();
+    if (rc != RELAX_OK) return rc;
+    const int e = rq4::launch_attention_decode(static_cast<const uint16_t*>(q), static_cast<const uint16_t*>(k_cache),
+                                               static_cast<const uint16_t*>(v_cache), kv_lens, batch, n_heads,
+                                               n_kv_heads, kv_len_max, static_cast<uint16_t*>(out), workspace, true,
+                                               static_cast<cudaStream_t>(stream));
+    if (e != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
+int relax_kv_append(const void* k_new, const void* v_new, const int32_t* pos, int64_t batch, int64_t n_kv_heads,
+                    int64_t head_dim, int64_t kv_len_max, void* k_cache, void* v_cache, void* stream) {
+    int rc = attn_shape_check(batch, n_kv_heads, n_kv_heads, head_dim, kv_len_max);
+    if (rc != RELAX_OK) return rc;
+    if (batch == 0) return RELAX_OK;
+    if (!k_new || !v_new || !pos || !k_cache || !v_cache) return RELAX_ERR_INVALID_ARG;
+    if (!rq4::aligned16(k_new) || !rq4::aligned16(v_new) || !rq4::aligned16(k_cache) || !rq4::aligned16(v_cache) ||
+        (reinterpret_cast<uintptr_t>(pos) & 3u))
+        return RELAX_ERR_MISALIGNED;
+    const size_t nb = static_cast<size_t>(batch * n_kv_heads * head_dim) * 2;
+    const size_t cb = static_cast<size_t>(batch * n_kv_heads * kv_len_max * head_dim) * 2;
+    if (rq4::overlap(k_cache, cb, v_cache, cb) || rq4::overlap(k_cache, cb, k_new, nb) ||
+        rq4::overlap(k_cache, cb, v_new, nb) || rq4::overlap(v_cache, cb, k_new, nb) ||
+        rq4::overlap(v_cache, cb, v_new, nb) || rq4::overlap(k_cache, cb, pos, batch * 4) ||
+        rq4::overlap(v_cache, cb, pos, batch * 4))
+        return RELAX_ERR_ALIAS;
+    rc = rq4::check_device();
+    if (rc != RELAX_OK) return rc;
+    const int e = rq4::launch_kv_append(static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), pos,
+                                        batch, n_kv_heads, kv_len_max, static_cast<uint16_t*>(k_cache),
+                                        static_cast<uint16_t*>(v_cache), true, static_cast<cudaStream_t>(stream));
+    if (e != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
 const char* relax_status_str(int status) {
     switch (status) {
         case RELAX_OK: return "RELAX_OK";

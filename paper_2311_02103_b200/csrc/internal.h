@@ -90,6 +90,13 @@ bool smalln_mma_ok(int64_t n, int64_t K, int64_t N);
 int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 int smalln_max_n();                 // largest n the automatic dispatch sends to it
+// Decode attention over a symbolic KV length and the KV append (attention.cu).
+size_t attn_workspace_bytes(int64_t batch, int64_t Hq, int64_t Lmax);
+int launch_attention_decode(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* lens,
+                            int64_t batch, int64_t Hq, int64_t Hkv, int64_t Lmax, uint16_t* out, void* ws,
+                            bool pdl, cudaStream_t st);
+int launch_kv_append(const uint16_t* kn, const uint16_t* vn, const int32_t* pos, int64_t batch, int64_t Hkv,
+                     int64_t Lmax, uint16_t* kc, uint16_t* vc, bool pdl, cudaStream_t st);
 // One-time format conversion into the native layout (repack.cu).
 int launch_repack(const uint32_t* src_w, const uint16_t* src_s, int64_t K, int64_t N, int layout, int group,
                   uint32_t* w, uint16_t* s, cudaStream_t stream);

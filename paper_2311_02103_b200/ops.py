@@ -40,7 +40,8 @@ FLAG_TILE_PER_CTA = 4
 # every symbol include/relax_q4.h declares
 EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",
            "relax_query_schedule", "relax_q4_dequant", "relax_status_str", "relax_version",
-           "relax_plan_workspace_fused", "relax_q4_matmul_fused", "relax_q4_repack")
+           "relax_plan_workspace_fused", "relax_q4_matmul_fused", "relax_q4_repack",
+           "relax_attn_decode_workspace", "relax_attn_decode", "relax_kv_append")
 
 # fused neighbours (include/relax_q4.h RELAX_OP_*)
 OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL = 1, 2, 4
@@ -98,6 +99,12 @@ def lib() -> ctypes.CDLL:
         L.relax_q4_matmul_fused.restype = I
         L.relax_q4_repack.argtypes = [P, P, I64, I64, I, I, P, P, P]
         L.relax_q4_repack.restype = I
+        L.relax_attn_decode_workspace.argtypes = [I64, I64, I64, ctypes.POINTER(SZ)]
+        L.relax_attn_decode_workspace.restype = I
+        L.relax_attn_decode.argtypes = [P, P, P, P, I64, I64, I64, I64, I64, P, P, SZ, P]
+        L.relax_attn_decode.restype = I
+        L.relax_kv_append.argtypes = [P, P, P, I64, I64, I64, I64, P, P, P]
+        L.relax_kv_append.restype = I
         _lib = L
         return L
 
@@ -272,6 +279,52 @@ def q4_matmul_fused(x, packed_w, scales, y=None, rms_weight=None, rms_eps: float
                                      _ptr(ws), nb, _stream_ptr(stream))
     _check(rc, "relax_q4_matmul_fused")
     return y
+
+
+def attn_decode_workspace(batch: int, n_heads: int, kv_len_max: int) -> int:
+    out = ctypes.c_size_t(0)
+    _check(lib().relax_attn_decode_workspace(batch, n_heads, kv_len_max, ctypes.byref(out)),
+           "relax_attn_decode_workspace")
+    return int(out.value)
+
+
+def attn_decode(q, k_cache, v_cache, kv_lens, out=None, ws=None, stream=None):
+    """relax_attn_decode: q [batch, Hq, 128] fp16, caches [batch, Hkv, L_max, 128]
+    fp16, kv_lens int32 [batch] (device) -> out [batch, Hq, 128] fp16."""
+    import torch
+    dev = _device_of_call()
+    if q.dim() != 3 or k_cache.dim() != 4:
+        raise ValueError("q must be [batch, Hq, D] and the caches [batch, Hkv, L_max, D]")
+    batch, hq, d = q.shape
+    _, hkv, lmax, _ = k_cache.shape
+    _check_tensor(q, "q", torch.float16, dev=dev)
+    _check_tensor(k_cache, "k_cache", torch.float16, (batch, hkv, lmax, d), dev=dev)
+    _check_tensor(v_cache, "v_cache", torch.float16, (batch, hkv, lmax, d), dev=dev)
+    _check_tensor(kv_lens, "kv_lens", torch.int32, (batch,), dev=dev)
+    out = _out(out.view(batch, hq * d) if out is not None else None, batch, hq * d, q).view(batch, hq, d)
+    if ws is None:
+        nb = attn_decode_workspace(batch, hq, lmax)
+        ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
+    nb = _ws_bytes(ws, dev)
+    rc = lib().relax_attn_decode(_ptr(q), _ptr(k_cache), _ptr(v_cache), _ptr(kv_lens), batch, hq, hkv, d, lmax,
+                                 _ptr(out), _ptr(ws), nb, _stream_ptr(stream))
+    _check(rc, "relax_attn_decode")
+    return out
+
+
+def kv_append(k_new, v_new, pos, k_cache, v_cache, stream=None):
+    """relax_kv_append: write k_new, v_new [batch, Hkv, 128] at pos[b] of each cache."""
+    import torch
+    dev = _device_of_call()
+    batch, hkv, lmax, d = k_cache.shape
+    _check_tensor(k_new, "k_new", torch.float16, (batch, hkv, d), dev=dev)
+    _check_tensor(v_new, "v_new", torch.float16, (batch, hkv, d), dev=dev)
+    _check_tensor(pos, "pos", torch.int32, (batch,), dev=dev)
+    _check_tensor(k_cache, "k_cache", torch.float16, dev=dev)
+    _check_tensor(v_cache, "v_cache", torch.float16, (batch, hkv, lmax, d), dev=dev)
+    rc = lib().relax_kv_append(_ptr(k_new), _ptr(v_new), _ptr(pos), batch, hkv, d, lmax, _ptr(k_cache),
+                               _ptr(v_cache), _stream_ptr(stream))
+    _check(rc, "relax_kv_append")
 
 
 LAYOUT_NK, LAYOUT_KN = 0, 1
