@@ -88,6 +88,13 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
     int bb = 128, bs = 1;
     bool bp = false;
     static const int64_t min_per_sm = knob_int("RELAX_Q4_PERSIST_MIN_TILES", 4);
+    static const int force_pbn = knob_int("RELAX_Q4_PERSIST_BN", 0);        // experiments: force the persistent BN
+    if (allow_persist && (force_pbn == 128 || force_pbn == 256)) {
+        *bn_out = force_pbn;
+        *s_out = 1;
+        *persist_out = true;
+        return;
+    }
     if (allow_persist && tm * ((n + 255) / 256) >= min_per_sm * sms) {
         // persistent BN = 256 tiles (gemm_tc_persist.cu): the epilogue of a
         // tile overlaps the next tile's k-loop, so the fill/drain is paid once

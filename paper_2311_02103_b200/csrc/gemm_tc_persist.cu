@@ -36,24 +36,29 @@
 
 namespace rq4 {
 
-constexpr int kPBN = 256;                                                 // token tile
 constexpr int kPWStages = 3;
 constexpr int kPASlots = 4;                                               // 64-k A slots
 constexpr int kPXStages = 3;                                              // 64-k x stages
 constexpr uint32_t kPCodes = kTcBM * (kTcWStageK / 2);                    // 16 KB
 constexpr uint32_t kPScales = kTcBM * (kTcWStageK / kGroup) * 2;          // 2 KB
 constexpr uint32_t kPASlotBytes = kTcBM * kTcXStageK * 2;                 // 16 KB
-constexpr uint32_t kPXStageBytes = kPBN * kTcXStageK * 2;                 // 32 KB
-constexpr uint32_t kPOffCodes = 0;
-constexpr uint32_t kPOffScales = kPOffCodes + kPWStages * kPCodes;       // 48 KB
-constexpr uint32_t kPOffA = kPOffScales + kPWStages * kPScales + 2048;   // 56 KB (1 KB aligned)
-constexpr uint32_t kPOffX = kPOffA + kPASlots * kPASlotBytes;            // 120 KB
-constexpr uint32_t kPOffBar = kPOffX + kPXStages * kPXStageBytes;        // 216 KB
 constexpr uint32_t kPNumBars = 2 * kPWStages + 2 * kPASlots + 2 * kPXStages + 4;
-constexpr uint32_t kPSmemBytes = kPOffBar + kPNumBars * 8 + 16 + 1024;   // + align slack
 constexpr int kPThreads = 16 * 32;
-static_assert(kPOffA % 1024 == 0 && kPOffX % 1024 == 0, "SW128 operands need 1 KB alignment");
-static_assert(kPSmemBytes <= 227 * 1024, "shared memory budget");
+
+// BN = token tile (MMA N): 256 (long prefill) or 128 (more tiles for n ~ 512)
+template <int BN>
+struct PCfg {
+    static constexpr uint32_t kXStageBytes = BN * kTcXStageK * 2;          // 32 / 16 KB
+    static constexpr uint32_t kOffCodes = 0;
+    static constexpr uint32_t kOffScales = kOffCodes + kPWStages * kPCodes;       // 48 KB
+    static constexpr uint32_t kOffA = kOffScales + kPWStages * kPScales + 2048;   // 56 KB (1 KB aligned)
+    static constexpr uint32_t kOffX = kOffA + kPASlots * kPASlotBytes;            // 120 KB
+    static constexpr uint32_t kOffBar = kOffX + kPXStages * kXStageBytes;
+    static constexpr uint32_t kSmemBytes = kOffBar + kPNumBars * 8 + 16 + 1024;  // + align slack
+    static constexpr uint32_t kTmemCols = 2 * BN;                          // two accumulators
+    static_assert(kOffA % 1024 == 0 && kOffX % 1024 == 0, "SW128 operands need 1 KB alignment");
+    static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
+};
 
 struct TpArgs {
     int64_t n, K, N;
@@ -87,16 +92,20 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
                  :: "r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
+template <int BN>
 __global__ void __launch_bounds__(kPThreads, 1)
 tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
                      const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TpArgs a) {
+    using C = PCfg<BN>;
+    constexpr int kPBN = BN;
+    constexpr uint32_t kPXStageBytes = C::kXStageBytes;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* codes_sm = smem + kPOffCodes;
-    uint8_t* scales_sm = smem + kPOffScales;
-    uint8_t* a_sm = smem + kPOffA;
-    uint8_t* x_sm = smem + kPOffX;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPOffBar);
+    uint8_t* codes_sm = smem + C::kOffCodes;
+    uint8_t* scales_sm = smem + C::kOffScales;
+    uint8_t* a_sm = smem + C::kOffA;
+    uint8_t* x_sm = smem + C::kOffX;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
     uint64_t* w_full = bars;
     uint64_t* w_empty = w_full + kPWStages;
     uint64_t* a_full = w_empty + kPWStages;
@@ -132,7 +141,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
         tma_prefetch_desc(&tm_x);
     }
     if (warp == 3) {
-        tmem_alloc<512>(tmem_slot);
+        tmem_alloc<C::kTmemCols>(tmem_slot);
         tmem_relinquish();
     }
     tc_fence_before();
@@ -306,12 +315,13 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     cluster_arrive_release();          // the peer may still multicast into / commit onto this CTA
     cluster_wait_acquire();
     tc_fence_after();
-    if (warp == 3) tmem_dealloc<512>(tmem_base);
+    if (warp == 3) tmem_dealloc<C::kTmemCols>(tmem_base);
 }
 
-int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, bool pdl, cudaStream_t stream) {
-    if (K % kTcWStageK != 0 || n <= 0) return static_cast<int>(cudaErrorInvalidValue);
+template <int BN>
+static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+                                const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
+    using C = PCfg<BN>;
     CUtensorMap mw, ms, mx;
     int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
@@ -319,22 +329,22 @@ int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
     rc = make_map_2d(&ms, CU_TENSOR_MAP_DATA_TYPE_UINT16, s, K / kGroup, N, (K / kGroup) * 2, kTcWStageK / kGroup,
                      kTcBM, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (rc) return rc;
-    rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, K, n, K * 2, kTcXStageK, kPBN / 2,
+    rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, K, n, K * 2, kTcXStageK, BN / 2,
                      CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
-    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_persist_kernel),
-                                              static_cast<int>(kPSmemBytes), true);
+    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_persist_kernel<BN>),
+                                              static_cast<int>(C::kSmemBytes), true);
     if (e != cudaSuccess) return static_cast<int>(e);
     TpArgs a;
     a.n = n; a.K = K; a.N = N; a.y = y;
     a.kt = static_cast<int>(K / kTcWStageK);
     a.m_tiles = ((N + kTcBM - 1) / kTcBM + 1) / 2;             // m-tile PAIRS (an odd last one is zero-filled)
-    a.tiles = a.m_tiles * ((n + kPBN - 1) / kPBN);              // pair tiles
+    a.tiles = a.m_tiles * ((n + BN - 1) / BN);                  // pair tiles
     const int64_t clusters = num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * (a.tiles < clusters ? a.tiles : clusters)));
     cfg.blockDim = dim3(kPThreads);
-    cfg.dynamicSmemBytes = kPSmemBytes;
+    cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -345,7 +355,15 @@ int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_persist_kernel, mw, ms, mx, a));
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_persist_kernel<BN>, mw, ms, mx, a));
+}
+
+int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
+                      uint16_t* y, int bn, bool pdl, cudaStream_t stream) {
+    if (K % kTcWStageK != 0 || n <= 0) return static_cast<int>(cudaErrorInvalidValue);
+    if (bn == 128) return launch_tc_persist_bn<128>(x, n, K, N, w, s, y, pdl, stream);
+    if (bn == 256) return launch_tc_persist_bn<256>(x, n, K, N, w, s, y, pdl, stream);
+    return static_cast<int>(cudaErrorInvalidValue);
 }
 
 }  // namespace rq4

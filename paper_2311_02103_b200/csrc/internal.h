@@ -59,7 +59,7 @@ struct Plan {
     int bn = 0;          // TC: token tile (MMA N)
     int split = 1;       // TC: split-K factor
     int cluster = 0;     // TC: split-K reduced in a thread-block cluster (DSMEM), no workspace
-    int persist = 0;     // TC: persistent kernel, double-buffered accumulator (BN = 256, no split)
+    int persist = 0;     // TC: persistent kernel, double-buffered accumulator (BN = 128 / 256, no split)
     int grid = 0;
     size_t ws_bytes = 0; // workspace bytes this plan needs
 };
@@ -119,7 +119,7 @@ int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64
                 uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
                 CUtensorMapSwizzle sw);
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, bool pdl, cudaStream_t stream);
+                      uint16_t* y, int bn, bool pdl, cudaStream_t stream);
 int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                     const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
                     CUtensorMapSwizzle sw);

@@ -248,6 +248,12 @@ q4_smalln_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_consta
     }
 }
 
+// consumer warps (8; 16 in the experiments build with RELAX_Q4_SN_WARPS=16)
+static int sn_warps() {
+    static const int w = knob_int("RELAX_Q4_SN_WARPS", kSnDefaultWarps) == 16 ? 16 : 8;
+    return w;
+}
+
 struct SnConfig {
     int grid, NS, rows_max;
     int64_t nrb;
@@ -264,7 +270,7 @@ static SnConfig sn_config(int64_t K, int64_t N) {
     c.grid = static_cast<int>(c.nrb < gmax ? c.nrb : gmax);
     const int64_t nrb_max = (c.nrb + c.grid - 1) / c.grid;
     c.rows_max = static_cast<int>(nrb_max * kSnRows);
-    const size_t part_bytes = static_cast<size_t>(nrb_max) * kSnRows * kSnMaxWarps * kSnTok * 4;
+    const size_t part_bytes = static_cast<size_t>(nrb_max) * kSnRows * sn_warps() * kSnTok * 4;
     const size_t fixed = 1024 + 256 + part_bytes;
     if (fixed + 3 * static_cast<size_t>(kSnStageBytes) > kSnSmemCap) return c;
     const int ns = static_cast<int>((kSnSmemCap - fixed) / kSnStageBytes);
@@ -298,7 +304,7 @@ int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
                              CU_TENSOR_MAP_SWIZZLE_128B);
         if (rc) return rc;
     }
-    static const int W = knob_int("RELAX_Q4_SN_WARPS", kSnDefaultWarps) == 16 ? 16 : 8;
+    const int W = sn_warps();
     auto kern = W == 16 ? q4_smalln_mma_kernel<16> : q4_smalln_mma_kernel<8>;
     const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), static_cast<int>(kSnSmemCap));
     if (e != cudaSuccess) return static_cast<int>(e);
