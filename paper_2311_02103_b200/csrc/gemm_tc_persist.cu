@@ -361,7 +361,11 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
                       uint16_t* y, int bn, bool pdl, cudaStream_t stream) {
     if (K % kTcWStageK != 0 || n <= 0) return static_cast<int>(cudaErrorInvalidValue);
+#ifdef RQ4_EXPERIMENTS
+    // BN = 128 tiles: measured slower than both BN = 256 and one tile per CTA at
+    // every n (the A transform is re-done per 128 tokens; profiles/r02/sweep_persist_bn_r02.txt)
     if (bn == 128) return launch_tc_persist_bn<128>(x, n, K, N, w, s, y, pdl, stream);
+#endif
     if (bn == 256) return launch_tc_persist_bn<256>(x, n, K, N, w, s, y, pdl, stream);
     return static_cast<int>(cudaErrorInvalidValue);
 }
