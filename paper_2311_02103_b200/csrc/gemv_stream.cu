@@ -199,6 +199,94 @@ __device__ __forceinline__ void row_dot(const uint4& cw, uint16_t sbits, const u
     }
 }
 
+// ZPF = 2 (default): integer dot products.  x of the lane's 32-code group is
+// converted once per kernel to 16-bit fixed point with the group's own power
+// of two (x_int = rint(x * 2^e), e chosen so max |x_int| is in [2^14, 2^15):
+// exact for every x within 2^4 of the group's largest, within 2^-15 of it
+// otherwise), and the codes stay bytes: per 8 codes 1 SHF + 2 LOP3 and four
+// dp2a (int16 x int8 pairs -> int32, exact).  Per group
+//   v = sum q x_int - 7 sum x_int      (int32, exact; |v| < 2^24)
+// and out = float(v) * s * 2^-e.  An all-7 group gives v = 0 exactly; one-hot
+// and integer x are exact (reading 6).  dp2a issues at
+// 2 warp-instr/clk/SM and co-issues with the ALU (profiles/r02/ubench_idp_r02.txt):
+// ~2.7x the FHFMA loop's math rate.
+__device__ __forceinline__ int dp2a_lo(uint32_t a16x2, uint32_t b8x4, int c) {
+    int d;
+    asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a16x2), "r"(b8x4), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp2a_hi(uint32_t a16x2, uint32_t b8x4, int c) {
+    int d;
+    asm("dp2a.hi.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a16x2), "r"(b8x4), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t pack16(int lo, int hi) {
+    return (static_cast<uint32_t>(lo) & 0xFFFFu) | (static_cast<uint32_t>(hi) << 16);
+}
+
+// x (4 uint4 = 32 fp16 of one group) -> int16 pairs in the dp2a order
+// (x0,x2) (x4,x6) (x1,x3) (x5,x7) per 8 k, 7 * sum x_int, and 2^-e.
+__device__ __forceinline__ void x_to_fixed(const uint4 (&xr)[4], uint32_t (&xi)[4][4], int& sx7, float& inv) {
+    float f[32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t w4[4] = {xr[q].x, xr[q].y, xr[q].z, xr[q].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float2 v = __half22float2(u32_as_h2(w4[u]));
+            f[q * 8 + 2 * u] = v.x;
+            f[q * 8 + 2 * u + 1] = v.y;
+        }
+    }
+    float m = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) m = fmaxf(m, fabsf(f[i]));
+    int e = 0;                                       // scale 2^e with max|x| * 2^e in [2^14, 2^15)
+    if (m > 0.f) e = 14 - (((__float_as_int(m) >> 23) & 0xFF) - 127);
+    const float up = __int_as_float((127 + e) << 23);
+    inv = __int_as_float((127 - e) << 23);
+    int xi_[32];
+    int sx = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        xi_[i] = __float2int_rn(f[i] * up);
+        sx += xi_[i];
+    }
+    sx7 = 7 * sx;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int* v = xi_ + q * 8;
+        xi[q][0] = pack16(v[0], v[2]);
+        xi[q][1] = pack16(v[4], v[6]);
+        xi[q][2] = pack16(v[1], v[3]);
+        xi[q][3] = pack16(v[5], v[7]);
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void row_dot_idp(const uint4& cw, uint16_t sbits, const uint32_t (&xi)[NT][4][4],
+                                            const int (&sx7)[NT], const float (&inv)[NT], float (&out)[NT]) {
+    const uint32_t words[4] = {cw.x, cw.y, cw.z, cw.w};
+    int acc_e[NT], acc_o[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) { acc_e[t] = 0; acc_o[t] = 0; }
+#pragma unroll
+    for (int wi = 0; wi < 4; ++wi) {
+        const uint32_t ev = words[wi] & 0x0F0F0F0Fu;            // bytes q0 q2 q4 q6
+        const uint32_t od = (words[wi] >> 4) & 0x0F0F0F0Fu;     // bytes q1 q3 q5 q7
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            acc_e[t] = dp2a_lo(xi[t][wi][0], ev, acc_e[t]);
+            acc_e[t] = dp2a_hi(xi[t][wi][1], ev, acc_e[t]);
+            acc_o[t] = dp2a_lo(xi[t][wi][2], od, acc_o[t]);
+            acc_o[t] = dp2a_hi(xi[t][wi][3], od, acc_o[t]);
+        }
+    }
+    const float sc = __half2float(__ushort_as_half(sbits));
+#pragma unroll
+    for (int t = 0; t < NT; ++t) out[t] = __int2float_rn(acc_e[t] + acc_o[t] - sx7[t]) * (sc * inv[t]);
+}
+
 // ---- fused neighbours (RELAX_OP_*, include/relax_q4.h) -------------------
 // RMSNorm prologue on the x registers: r_t = 1/sqrt(mean x^2 + eps) over the
 // whole row (per-lane sums -> warp shuffle -> one partial per K-column warp in
@@ -344,9 +432,17 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
         // (exactly what row_dot computes for an all-7 group)
 #pragma unroll
         for (int t = 0; t < NT; ++t) { ze[t] = 0.f; zo[t] = 0.f; }
-        if (ZPF) {
+        if (ZPF == 1) {
             const uint32_t sevens[4] = {0x77777777u, 0x77777777u, 0x77777777u, 0x77777777u};
             group_chains<NT, 1>(sevens, xr, ze, zo);
+        }
+        // ZPF = 2: x of the group in 16-bit fixed point for the dp2a loop
+        uint32_t xi[NT][4][4];
+        int sx7[NT];
+        float xinv[NT];
+        if (ZPF == 2) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) x_to_fixed(xr[t], xi[t], sx7[t], xinv[t]);
         }
         if (ops & RELAX_OP_RESIDUAL) {
             // prefetch this thread's first residual value of the final loop (its
@@ -382,7 +478,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
                 uint16_t sbits = *reinterpret_cast<const uint16_t*>(stage + soff + i * sb_row);
                 if (!FULLG && !gv) sbits = 0;                 // lanes past K: x = 0 and s = 0
                 float o[NT];
-                row_dot<NT, ZPF>(cw, sbits, xr, ze, zo, o);
+                if (ZPF == 2) row_dot_idp<NT>(cw, sbits, xi, sx7, xinv, o);
+                else row_dot<NT, ZPF>(cw, sbits, xr, ze, zo, o);
 #pragma unroll
                 for (int t = 0; t < NT; ++t) acc[t][i] = o[t];
             }
@@ -401,7 +498,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
     }
     __syncthreads();
     // fixed-order sum over the WK K-columns; fp32 -> fp16 RNE
-    const float rescale = ZPF ? 16777216.0f : 1.0f;          // exact power-of-two rescale
+    const float rescale = ZPF == 1 ? 16777216.0f : 1.0f;     // exact power-of-two rescale
     if (ops & RELAX_OP_SILU_MUL) {
         const int np = rows / 2;
         for (int o = threadIdx.x; o < np * NT; o += blockDim.x) {
@@ -453,8 +550,9 @@ static bool gs_trace() { return RQ4_TRACE && knob_int("RELAX_Q4_TRACE", 0) == 1;
 static int gs_prefetch() { static const int v = knob_int("RELAX_Q4_GS_PREFETCH", -1); return v < 0 ? (1 << 30) : v; }
 // where each CTA signals griddepcontrol.launch_dependents (0: at its start)
 static int gs_trigger() { static const int v = knob_int("RELAX_Q4_GS_TRIGGER", 0); return v; }
-// factored zero point (default); 0 = exact centering (experiments build)
-static int gs_zpf() { static const int v = knob_int("RELAX_Q4_GEMV_ZPF", 1); return v; }
+// 2 = integer dot products (default); 1 = FHFMA with the factored
+// zero point, 0 = exact centering (experiments build)
+static int gs_zpf() { static const int v = knob_int("RELAX_Q4_GEMV_ZPF", 2); return v; }
 
 static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
     GsConfig c{};
@@ -587,12 +685,13 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
         int rc;
 #ifdef RQ4_EXPERIMENTS
-        if (!zpf) rc = cnt == 1 ? launch_gs_z<1, 0>(a, c, pdl, stream) : launch_gs_z<2, 0>(a, c, pdl, stream);
+        if (zpf == 0) rc = cnt == 1 ? launch_gs_z<1, 0>(a, c, pdl, stream) : launch_gs_z<2, 0>(a, c, pdl, stream);
+        else if (zpf == 1) rc = cnt == 1 ? launch_gs_z<1, 1>(a, c, pdl, stream) : launch_gs_z<2, 1>(a, c, pdl, stream);
         else
 #else
         (void)zpf;
 #endif
-        rc = cnt == 1 ? launch_gs_z<1, 1>(a, c, pdl, stream) : launch_gs_z<2, 1>(a, c, pdl, stream);
+        rc = cnt == 1 ? launch_gs_z<1, 2>(a, c, pdl, stream) : launch_gs_z<2, 2>(a, c, pdl, stream);
         if (rc != 0) return rc;
     }
     return 0;
