@@ -303,10 +303,37 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.Stream(device=dev)
     flags = ops.FLAG_NO_PDL if args.no_pdl else 0
 
-    def step():
+    def serial_step():
         for (name, K, N), (pk, sc), y in zip(mats, weights, ys):
             ops.q4_matmul_ex(xs[K], pk, sc, y=y, ws=wss[(K, N)], flags=flags, stream=stream)
 
+    # The linears that read the same x in a Llama layer -- q, k, v and gate, up --
+    # go out as one relax_q4_matmul_grouped call each (one launch at decode), the
+    # others one call each: the layer's true dependency chain (qkv -> o ->
+    # gate/up -> down), on the same per-matrix weight buffers.  --serial makes
+    # every linear its own dependent call (round 1's schedule).
+    groups = []
+    i = 0
+    while i < len(mats):
+        kind = mats[i][0].split(".")[-1]
+        span = 3 if kind == "q" else 2 if kind == "gate" else 1
+        groups.append(list(range(i, i + span)))
+        i += span
+    # (a group is one launch only at decode, n <= 2; beyond that its members run
+    # one by one anyway, so the plain chain is used)
+    grouped = not args.serial and not args.no_pdl and n <= 2 and any(len(g) > 1 for g in groups)
+
+    def grouped_step():
+        for g in groups:
+            if len(g) == 1:
+                j = g[0]
+                ops.q4_matmul_ex(xs[mats[j][1]], *weights[j], y=ys[j], ws=wss[(mats[j][1], mats[j][2])],
+                                 flags=flags, stream=stream)
+            else:
+                ops.q4_matmul_grouped(xs[mats[g[0]][1]], [weights[j] for j in g], ys=[ys[j] for j in g],
+                                      stream=stream)
+
+    step = grouped_step if grouped else serial_step
     out_last = lambda: ys[-1]          # noqa: E731  the step's result (logits)
     block_io = None
     if args.block != "none":
@@ -381,6 +408,25 @@ def run_ours(args, rank, world, local_rank):
     ms = max_over_ranks(ms)
     if world > 1:
         dist.barrier()
+    serial_line = None
+    if grouped and block_io is None and not tp_mode:
+        # the same layer set with every linear its own dependent call, for reference
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2, stream=stream):
+            serial_step()
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                g2.replay()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(args.steps):
+                g2.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms_s = max_over_ranks(e0.elapsed_time(e1))
+        serial_line = {"value": round((world * n * args.steps) / (ms_s / 1e3), 2), "unit": "tok/s",
+                       "ms_per_step": round(ms_s / args.steps, 5), "launch_chain": len(mats),
+                       "how": "every linear its own dependent relax_q4_matmul call (q, k, v, gate, up not grouped)"}
 
     # ---- end to end through the public API: pinned host x in, logits out,
     # (a) replaying the captured step, (b) eagerly -- every C-ABI call
@@ -444,7 +490,8 @@ def run_ours(args, rank, world, local_rank):
              + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else "")
              + (f"-megatron-tp{tp_world}" if tp_mode else "")
              + (f"-block-{args.block}" if args.block != "none" else "")
-             + (f"-attn-kv{args.kv}" if args.kv > 0 else ""))
+             + (f"-attn-kv{args.kv}" if args.kv > 0 else "")
+             + ("-grouped-qkv-gateup" if grouped else ""))
     roof["traffic"] = traffic_per_launch(label, n)
     roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
     roof["kernel"] = ("q4_decode_stream_kernel (streamed decode GEMV)"
@@ -453,7 +500,13 @@ def run_ours(args, rank, world, local_rank):
     if tp_mode:
         roof["per"] += "; per GPU: each rank streams its own shards"
     per_kind = {"tc": lambda: 1, "smalln": lambda: -(-n // 8), "gemv": lambda: -(-n // 2)}
-    launches = sum(per_kind[sched[f"{K}x{N}"]["variant"]]() for _, K, N in mats)
+    launches = 0
+    for g in (groups if grouped else [[j] for j in range(len(mats))]):
+        kinds = [sched[f"{mats[j][1]}x{mats[j][2]}"]["variant"] for j in g]
+        if len(g) > 1 and all(k == "gemv" for k in kinds):
+            launches += -(-n // 2)                     # one grouped decode launch per token pair
+        else:
+            launches += sum(per_kind[k]() for k in kinds)
     if args.kv > 0:
         launches += 3 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))   # append, partial, combine
     res = {
@@ -486,6 +539,7 @@ def run_ours(args, rank, world, local_rank):
                       "how": "every C-ABI call dispatched from Python each step (ctypes binding + host dispatch), "
                              "same copies"},
         "gpu_launches": launches * args.steps,
+        "serial_chain": serial_line,
         "clocks": ck,
         "setup_s": round(t_gen, 1),
     }
@@ -602,6 +656,9 @@ def main():
     ap.add_argument("--tp-shard", type=int, default=1,
                     help="run rank 0's shard of a p-way tensor-parallel layer set on this GPU "
                          "(per-GPU compute-only time; no collective)")
+    ap.add_argument("--serial", action="store_true",
+                    help="every linear its own dependent call (default: q/k/v and gate/up, which read the same x, "
+                         "as one relax_q4_matmul_grouped call each)")
     ap.add_argument("--fused", action="store_true",
                     help="stack q/k/v and gate/up rows into one call each (same weights)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

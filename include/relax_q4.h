@@ -131,6 +131,23 @@ RELAX_API int relax_q4_matmul_ws(const void* x, int64_t n, int64_t K, int64_t N,
                        const uint32_t* packed_w, const void* scales, void* y,
                        void* workspace, size_t ws_bytes, void* stream);
 
+/* Grouped form: `count` (1..4) linears that read the SAME x (q, k and v of a
+ * layer; gate and up), each with its own weights and output:
+ *   y[i] = x . dequant(packed_w[i], scales[i]),  y[i] fp16 [n][N[i]].
+ * `N`, `packed_w`, `scales`, `y` are HOST arrays of `count` entries (read
+ * during the call only) holding device pointers.  For decode (n <= 2) the
+ * members run as ONE launch of the streamed decode kernel, its CTAs split
+ * among them in proportion to N[i] -- one dependent step of the stream
+ * instead of `count` (horizontal fusion of independent operators); other n
+ * run member by member through relax_q4_matmul.  Results equal `count`
+ * separate relax_q4_matmul calls within the tolerance (bitwise for the
+ * pinned cases).  No workspace.  Errors as relax_q4_matmul, plus
+ * RELAX_ERR_INVALID_ARG for count outside 1..4 and RELAX_ERR_ALIAS when an
+ * output overlaps x, any weight, or another output. */
+RELAX_API int relax_q4_matmul_grouped(const void* x, int64_t n, int64_t K, int count, const int64_t* N,
+                                      const uint32_t* const* packed_w, const void* const* scales,
+                                      void* const* y, void* stream);
+
 /* Explicit-schedule form, for parity tests of every variant and for benches.
  *   variant   enum relax_variant (AUTO = same as relax_q4_matmul_ws)
  *   split_k   TC only: split-K factor, 0 = choose; > 1 needs a workspace

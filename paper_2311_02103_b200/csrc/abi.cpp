@@ -483,6 +483,58 @@ int relax_q4_matmul(const void* x, int64_t n, int64_t K, int64_t N, const uint32
     return rq4::matmul_impl(x, n, K, N, packed_w, scales, y, nullptr, 0, 0, 0, 0, 0u, stream);
 }
 
+int relax_q4_matmul_grouped(const void* x, int64_t n, int64_t K, int count, const int64_t* N,
+                            const uint32_t* const* packed_w, const void* const* scales, void* const* y,
+                            void* stream) {
+    if (count < 1 || count > 4 || !N || !packed_w || !scales || !y) return RELAX_ERR_INVALID_ARG;
+    if (n < 0 || K <= 0) return RELAX_ERR_INVALID_ARG;
+    for (int i = 0; i < count; ++i)
+        if (N[i] <= 0) return RELAX_ERR_INVALID_ARG;
+    if (K % rq4::kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if (n == 0) return RELAX_OK;
+    if (!x) return RELAX_ERR_INVALID_ARG;
+    const size_t xb = static_cast<size_t>(n) * K * 2;
+    for (int i = 0; i < count; ++i) {
+        if (!packed_w[i] || !scales[i] || !y[i]) return RELAX_ERR_INVALID_ARG;
+        if (!rq4::aligned16(packed_w[i]) || !rq4::aligned16(scales[i]) || !rq4::aligned16(y[i]))
+            return RELAX_ERR_MISALIGNED;
+    }
+    if (!rq4::aligned16(x)) return RELAX_ERR_MISALIGNED;
+    for (int i = 0; i < count; ++i) {
+        const size_t yb = static_cast<size_t>(n) * N[i] * 2;
+        if (rq4::overlap(y[i], yb, x, xb)) return RELAX_ERR_ALIAS;
+        for (int j = 0; j < count; ++j) {
+            const size_t wb = static_cast<size_t>(N[j]) * K / 2, sb = static_cast<size_t>(N[j]) * (K / rq4::kGroup) * 2;
+            if (rq4::overlap(y[i], yb, packed_w[j], wb) || rq4::overlap(y[i], yb, scales[j], sb)) return RELAX_ERR_ALIAS;
+            if (j != i && rq4::overlap(y[i], yb, y[j], static_cast<size_t>(n) * N[j] * 2)) return RELAX_ERR_ALIAS;
+        }
+    }
+    // one launch where the streamed decode kernel serves every member (n <= 2)
+    if (n <= rq4::gemv_max_n() && rq4::gemv_stream_grouped_ok(n, K, count, N)) {
+        const int rc = rq4::check_device();
+        if (rc != RELAX_OK) return rc;
+        const uint16_t* sp[4];
+        uint16_t* yp[4];
+        for (int i = 0; i < count; ++i) {
+            sp[i] = static_cast<const uint16_t*>(scales[i]);
+            yp[i] = static_cast<uint16_t*>(y[i]);
+        }
+        const int e = rq4::launch_gemv_stream_grouped(static_cast<const uint16_t*>(x), n, K, count, N, packed_w, sp,
+                                                      yp, true, static_cast<cudaStream_t>(stream));
+        if (e != 0) {
+            cudaGetLastError();
+            return RELAX_ERR_CUDA;
+        }
+        return RELAX_OK;
+    }
+    // otherwise each member through the ordinary dispatch (same results)
+    for (int i = 0; i < count; ++i) {
+        const int rc = rq4::matmul_impl(x, n, K, N[i], packed_w[i], scales[i], y[i], nullptr, 0, 0, 0, 0, 0u, stream);
+        if (rc != RELAX_OK) return rc;
+    }
+    return RELAX_OK;
+}
+
 int relax_q4_matmul_ws(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
                        const void* scales, void* y, void* workspace, size_t ws_bytes, void* stream) {
     return rq4::matmul_impl(x, n, K, N, packed_w, scales, y, workspace, ws_bytes, 0, 0, 0, 0u, stream);

@@ -36,6 +36,8 @@
 
 namespace rq4 {
 
+constexpr int kGsMaxGroup = 4;   // matrices per grouped launch
+
 struct GsArgs {
     const uint16_t* x;     // [NT][K] fp16
     const uint8_t* w;      // [N][K/2] bytes
@@ -54,6 +56,14 @@ struct GsArgs {
     const uint16_t* gamma; // RMSNORM_X: fp16 [K]
     const uint16_t* res;   // RESIDUAL: fp16 [NT][Nout]
     int64_t Nout;          // N/2 with SILU_MUL, else N (row stride of y and res)
+    // grouped launch (relax_q4_matmul_grouped): matrices i = 1 .. nmat-1 take
+    // CTAs [cta0[i], cta0[i+1]); matrix 0 is (w, s, y, N, Nout) above
+    int nmat;
+    int cta0[kGsMaxGroup + 1];
+    const uint8_t* wgp[kGsMaxGroup];
+    const uint8_t* sgp[kGsMaxGroup];
+    uint16_t* ygp[kGsMaxGroup];
+    int64_t Ngp[kGsMaxGroup];
 };
 
 // ---- optional per-CTA timeline (experiments build only, RELAX_Q4_TRACE=1;
@@ -363,9 +373,24 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
     // rows of this CTA; with SILU_MUL whole (gate, up) pairs
     const uint32_t ops = FU ? a.ops : 0u;
     const int psh = (ops & RELAX_OP_SILU_MUL) ? 1 : 0;       // log2 of the row unit
-    const int64_t units = a.N >> psh;
-    const int64_t row0 = (static_cast<int64_t>(blockIdx.x) * units / gridDim.x) << psh;
-    const int64_t row1 = (static_cast<int64_t>(blockIdx.x + 1) * units / gridDim.x) << psh;
+    // grouped launch: this CTA's matrix and its block of that matrix's rows
+    const uint8_t* w_base = a.w;
+    const uint8_t* s_base = a.s;
+    uint16_t* y_base = a.y;
+    int64_t Nm = a.N, Nout = a.Nout;
+    int cb = static_cast<int>(blockIdx.x), nb = static_cast<int>(gridDim.x);
+    if (a.nmat > 1) {
+        int m = 0;
+#pragma unroll 1
+        for (int i = 1; i < a.nmat; ++i) if (static_cast<int>(blockIdx.x) >= a.cta0[i]) m = i;
+        w_base = a.wgp[m]; s_base = a.sgp[m]; y_base = a.ygp[m];
+        Nm = a.Ngp[m]; Nout = Nm;
+        cb = static_cast<int>(blockIdx.x) - a.cta0[m];
+        nb = a.cta0[m + 1] - a.cta0[m];
+    }
+    const int64_t units = Nm >> psh;
+    const int64_t row0 = (static_cast<int64_t>(cb) * units / nb) << psh;
+    const int64_t row1 = (static_cast<int64_t>(cb + 1) * units / nb) << psh;
     const int rows = static_cast<int>(row1 - row0);
     const int nst = (rows + a.RS - 1) / a.RS;
     const uint32_t cb_row = static_cast<uint32_t>(a.K / 2);
@@ -387,8 +412,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
         // ------------------------------------------------ producer (one thread)
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            const uint8_t* wsrc = a.w + row0 * cb_row;
-            const uint8_t* ssrc = a.s + row0 * sb_row;
+            const uint8_t* wsrc = w_base + row0 * cb_row;
+            const uint8_t* ssrc = s_base + row0 * sb_row;
             int slot = 0;
             uint32_t phase = 0;
             int issued = 0;
@@ -452,7 +477,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
                 const int o = threadIdx.x;
                 const int ul = o / NT, t = o - ul * NT;
                 const int64_t col = (ops & RELAX_OP_SILU_MUL) ? row0 / 2 + ul : row0 + ul;
-                res_pre = a.res[static_cast<int64_t>(t) * a.Nout + col];
+                res_pre = a.res[static_cast<int64_t>(t) * Nout + col];
             }
         }
         if (RQ4_TRACE && a.trace_seq && warp == 0 && lane == 0) tr_first = gtime();   // x in registers
@@ -509,9 +534,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
                 sg += part[(static_cast<size_t>(2 * pl) * a.WK + c) * NT + t];
                 su += part[(static_cast<size_t>(2 * pl + 1) * a.WK + c) * NT + t];
             }
-            const int64_t idx = static_cast<int64_t>(t) * a.Nout + row0 / 2 + pl;
+            const int64_t idx = static_cast<int64_t>(t) * Nout + row0 / 2 + pl;
             const bool pre = o == static_cast<int>(threadIdx.x) && warp < nwc;
-            a.y[idx] = residual_add(silu_mul_value(sg * rescale, su * rescale), ops,
+            y_base[idx] = residual_add(silu_mul_value(sg * rescale, su * rescale), ops,
                                     (ops & RELAX_OP_RESIDUAL) ? (pre ? res_pre : a.res[idx]) : uint16_t(0));
         }
     } else {
@@ -520,9 +545,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
             const int t = o - rl * NT;
             float sum = 0.f;
             for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
-            const int64_t idx = static_cast<int64_t>(t) * a.Nout + row0 + rl;
+            const int64_t idx = static_cast<int64_t>(t) * Nout + row0 + rl;
             const bool pre = o == static_cast<int>(threadIdx.x) && warp < nwc;
-            a.y[idx] = residual_add(__half_as_ushort(__float2half_rn(sum * rescale)), ops,
+            y_base[idx] = residual_add(__half_as_ushort(__float2half_rn(sum * rescale)), ops,
                                     (ops & RELAX_OP_RESIDUAL) ? (pre ? res_pre : a.res[idx]) : uint16_t(0));
         }
     }
@@ -678,6 +703,7 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.gamma = fu.gamma;
         a.res = fu.res ? fu.res + t0 * Nout : nullptr;
         a.Nout = Nout;
+        a.nmat = 1;
         a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
         a.rows_cta_max = c.rows_cta_max;
         a.prefetch = gs_prefetch();
@@ -692,6 +718,83 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         (void)zpf;
 #endif
         rc = cnt == 1 ? launch_gs_z<1, 2>(a, c, pdl, stream) : launch_gs_z<2, 2>(a, c, pdl, stream);
+        if (rc != 0) return rc;
+    }
+    return 0;
+}
+
+// Grouped launch (relax_q4_matmul_grouped): `count` matrices sharing x and K
+// in ONE launch -- the CTAs are split among the matrices in proportion to
+// their rows, each CTA streaming a row block of one matrix, so independent
+// linears that read the same x (q/k/v, gate/up) are one dependent step of the
+// PDL chain instead of `count`.
+bool gemv_stream_grouped_ok(int64_t n, int64_t K, int count, const int64_t* N) {
+    if (n < 1 || n > 2 || count < 1 || count > kGsMaxGroup) return false;
+    int64_t tot = 0;
+    for (int i = 0; i < count; ++i) {
+        if (!gemv_stream_ok(static_cast<int>(n), K, N[i])) return false;
+        tot += N[i];
+    }
+    if (tot < 2 * count) return false;
+    const GsConfig c = gs_config(K, tot);
+    return c.smem <= static_cast<size_t>(kGsSmemMax);
+}
+
+int launch_gemv_stream_grouped(const uint16_t* x, int64_t n, int64_t K, int count, const int64_t* N,
+                               const uint32_t* const* w, const uint16_t* const* s, uint16_t* const* y, bool pdl,
+                               cudaStream_t stream) {
+    int64_t tot = 0;
+    for (int i = 0; i < count; ++i) tot += N[i];
+    GsConfig c = gs_config(K, tot);
+    // CTAs per matrix in proportion to its rows (at least one each)
+    int cta0[kGsMaxGroup + 1];
+    cta0[0] = 0;
+    int64_t acc = 0;
+    for (int i = 0; i < count; ++i) {
+        acc += N[i];
+        int e = static_cast<int>(acc * c.grid / tot);
+        if (e < cta0[i] + 1) e = cta0[i] + 1;
+        cta0[i + 1] = e;
+    }
+    c.grid = cta0[count];
+    int rmax = 0;
+    for (int i = 0; i < count; ++i) {
+        const int nb = cta0[i + 1] - cta0[i];
+        const int r = static_cast<int>((N[i] + nb - 1) / nb);
+        if (r > rmax) rmax = r;
+    }
+    c.rows_cta_max = rmax;
+    const size_t part_bytes = static_cast<size_t>(rmax) * c.WK * 2 * 4;
+    c.smem = 256 + static_cast<size_t>(c.NS) * c.RS * (K / 2 + K / 16) + 1024 + part_bytes;
+    if (c.smem < 80 * 1024) c.smem = 80 * 1024;
+    if (c.smem > static_cast<size_t>(kGsSmemMax)) return static_cast<int>(cudaErrorInvalidConfiguration);
+    for (int64_t t0 = 0; t0 < n; t0 += 2) {
+        const int cnt = (n - t0) >= 2 ? 2 : 1;
+        GsArgs a{};
+        a.x = x + t0 * K;
+        a.w = reinterpret_cast<const uint8_t*>(w[0]);
+        a.s = reinterpret_cast<const uint8_t*>(s[0]);
+        a.y = y[0] + t0 * N[0];
+        a.N = N[0];
+        a.K = static_cast<int>(K);
+        a.G = static_cast<int>(K / kGroup);
+        a.WK = c.WK; a.H = c.H; a.RS = c.RS; a.NS = c.NS;
+        a.ops = 0;
+        a.Nout = N[0];
+        a.nmat = count;
+        for (int i = 0; i <= count; ++i) a.cta0[i] = cta0[i];
+        for (int i = 0; i < count; ++i) {
+            a.wgp[i] = reinterpret_cast<const uint8_t*>(w[i]);
+            a.sgp[i] = reinterpret_cast<const uint8_t*>(s[i]);
+            a.ygp[i] = y[i] + t0 * N[i];
+            a.Ngp[i] = N[i];
+        }
+        a.stage_bytes = static_cast<uint32_t>(c.RS * (K / 2 + K / 16));
+        a.rows_cta_max = c.rows_cta_max;
+        a.prefetch = gs_prefetch();
+        a.trigger = gs_trigger();
+        a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
+        const int rc = cnt == 1 ? launch_gs_z<1, 2>(a, c, pdl, stream) : launch_gs_z<2, 2>(a, c, pdl, stream);
         if (rc != 0) return rc;
     }
     return 0;

@@ -84,6 +84,11 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
 // (K % 256 == 0, N < 2^24, its shared-memory footprint within the attribute);
 // pair = 2 with the SiLU-mul epilogue (CTAs own whole (gate, up) row pairs).
 bool gemv_stream_ok(int nt, int64_t K, int64_t N, int pair = 1);
+// Grouped decode launch: up to 4 matrices sharing x and K in one kernel.
+bool gemv_stream_grouped_ok(int64_t n, int64_t K, int count, const int64_t* N);
+int launch_gemv_stream_grouped(const uint16_t* x, int64_t n, int64_t K, int count, const int64_t* N,
+                               const uint32_t* const* w, const uint16_t* const* s, uint16_t* const* y, bool pdl,
+                               cudaStream_t stream);
 // Small-batch warp-MMA streamed kernel (smalln_mma.cu): any n (8 tokens per
 // launch), K % 256 == 0.
 bool smalln_mma_ok(int64_t n, int64_t K, int64_t N);

@@ -41,7 +41,7 @@ FLAG_TILE_PER_CTA = 4
 EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",
            "relax_query_schedule", "relax_q4_dequant", "relax_status_str", "relax_version",
            "relax_plan_workspace_fused", "relax_q4_matmul_fused", "relax_q4_repack",
-           "relax_attn_decode_workspace", "relax_attn_decode", "relax_kv_append")
+           "relax_attn_decode_workspace", "relax_attn_decode", "relax_kv_append", "relax_q4_matmul_grouped")
 
 # fused neighbours (include/relax_q4.h RELAX_OP_*)
 OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL = 1, 2, 4
@@ -99,6 +99,9 @@ def lib() -> ctypes.CDLL:
         L.relax_q4_matmul_fused.restype = I
         L.relax_q4_repack.argtypes = [P, P, I64, I64, I, I, P, P, P]
         L.relax_q4_repack.restype = I
+        L.relax_q4_matmul_grouped.argtypes = [P, I64, I64, I, ctypes.POINTER(I64), ctypes.POINTER(P),
+                                              ctypes.POINTER(P), ctypes.POINTER(P), P]
+        L.relax_q4_matmul_grouped.restype = I
         L.relax_attn_decode_workspace.argtypes = [I64, I64, I64, ctypes.POINTER(SZ)]
         L.relax_attn_decode_workspace.restype = I
         L.relax_attn_decode.argtypes = [P, P, P, P, I64, I64, I64, I64, I64, P, P, SZ, P]
@@ -221,6 +224,26 @@ def q4_matmul(x, packed_w, scales, y=None, ws=None, stream=None):
                                       _ptr(ws), nb, st)
         _check(rc, "relax_q4_matmul_ws")
     return y
+
+
+def q4_matmul_grouped(x, weights, ys=None, stream=None):
+    """relax_q4_matmul_grouped: y_i = x . dequant(packed_w_i, scales_i) for a list
+    of (packed_w, scales) pairs sharing x (q/k/v, gate/up): one launch at decode."""
+    import torch
+    if not 1 <= len(weights) <= 4:
+        raise ValueError("1..4 linears per group")
+    outs = []
+    for i, (pw, sc) in enumerate(weights):
+        n, K, N = _shapes(x, pw, sc)
+        outs.append(_out(None if ys is None else ys[i], n, N, x))
+    cnt = len(weights)
+    Ns = (ctypes.c_int64 * cnt)(*[pw.shape[0] for pw, _ in weights])
+    Ws = (ctypes.c_void_p * cnt)(*[_ptr(pw) for pw, _ in weights])
+    Ss = (ctypes.c_void_p * cnt)(*[_ptr(sc) for _, sc in weights])
+    Ys = (ctypes.c_void_p * cnt)(*[_ptr(y) for y in outs])
+    rc = lib().relax_q4_matmul_grouped(_ptr(x), x.shape[0], x.shape[1], cnt, Ns, Ws, Ss, Ys, _stream_ptr(stream))
+    _check(rc, "relax_q4_matmul_grouped")
+    return outs
 
 
 def q4_matmul_ex(x, packed_w, scales, y=None, ws=None, variant=VARIANT_AUTO, split_k=0, bn=0,
