@@ -22,7 +22,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 
 
-@pytest.mark.parametrize("impl,zpf", [("mma", "1"), ("bdmma", "1"), ("row", "1"), ("v1", "1"), ("stream", "0")])
+@pytest.mark.parametrize("impl,zpf", [("mma", "1"), ("bdmma", "1"), ("row", "1"), ("v1", "1"), ("stream", "0"), ("stream", "1")])
 def test_gemv_impl_parity(impl, zpf):
     sys.path.insert(0, ROOT)
     from paper_2311_02103_b200 import build
