@@ -283,7 +283,7 @@ RELAX_API int relax_q4_repack(const uint32_t* src_packed, const void* src_scales
  *   s_j = (q . k_j) / sqrt(head_dim), out = softmax(s) . V in fp32, fp16 RNE;
  *   query head h uses kv head h / (n_heads / n_kv_heads) (grouped-query
  *   attention); a sequence with kv_lens[b] == 0 gets out = 0.
- * head_dim must be 128 and n_heads / n_kv_heads one of 1, 2, 4, 8.
+ * head_dim must be 128, n_heads / n_kv_heads one of 1, 2, 4, 8, kv_len_max <= 65536.
  * Split over 256-key chunks (flash decoding); the fp32 partials live in a
  * caller-owned workspace of relax_attn_decode_workspace(batch, n_heads,
  * kv_len_max) bytes (no zero-fill needed).  Deterministic.

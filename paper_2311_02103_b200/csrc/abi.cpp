@@ -603,7 +603,7 @@ int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t 
 // Decode attention (F4; include/relax_q4.h).
 static int attn_shape_check(int64_t batch, int64_t Hq, int64_t Hkv, int64_t D, int64_t Lmax) {
     if (batch < 0 || Hq <= 0 || Hkv <= 0 || D <= 0 || Lmax < 0) return RELAX_ERR_INVALID_ARG;
-    if (D != 128 || Hq % Hkv != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if (D != 128 || Hq % Hkv != 0 || Lmax > 65536) return RELAX_ERR_UNSUPPORTED_SHAPE;
     const int64_t G = Hq / Hkv;
     if (G != 1 && G != 2 && G != 4 && G != 8) return RELAX_ERR_UNSUPPORTED_SHAPE;
     return RELAX_OK;

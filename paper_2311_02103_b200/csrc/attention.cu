@@ -48,7 +48,8 @@ template <int G>
 __global__ void __launch_bounds__(kAttThreads) attn_partial_kernel(const __grid_constant__ AttArgs a) {
     __shared__ __align__(16) float qs[G][kAttD];
     __shared__ float sc[G][kAttChunk];
-    __shared__ float red[4][G][kAttD];
+    __shared__ float red[(G <= 2) ? 1 : 4][G][kAttD];
+    __shared__ float red16[(G <= 2) ? 16 : 1][G][kAttD];
     __shared__ float ml[G][2];
     pdl_launch_dependents();
     pdl_wait();                                          // q and the caches come from earlier kernels
@@ -75,8 +76,9 @@ __global__ void __launch_bounds__(kAttThreads) attn_partial_kernel(const __grid_
     const int64_t kvbase = (static_cast<int64_t>(b) * a.Hkv + g) * a.Lmax;
     if constexpr (G >= 4) {
         // scores, G >= 4 (GQA): thread t scores key k0 + t for all G heads (16-B
-        // loads of its key row; q broadcast from shared memory) -- G dots per
-        // key row read, no shuffles
+        // loads of its key row, q broadcast from shared memory) -- G dots per
+        // key row read, no shuffles (measured faster than the 8-lane groups at
+        // G = 8: 28 vs 51 us for the 70B heads at L = 4096)
         float acc[G];
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) acc[gg] = 0.f;
@@ -113,39 +115,45 @@ __global__ void __launch_bounds__(kAttThreads) attn_partial_kernel(const __grid_
         // 1 KB contiguous); lane `sub` holds d in [16 sub, 16 sub + 16); the
         // partial dots are reduced over the group with 3 shuffles
         const int grp = lane >> 3, sub = lane & 7;
-        for (int t = warp * 4 + grp; t < kAttChunk; t += 32) {
-            float acc[G];
+        // all 8 steps' key slices loaded first (16 x 16 B per lane in flight),
+        // then the dots: the phase is one memory round trip, not eight
+        uint4 kv[8][2];
 #pragma unroll
-            for (int gg = 0; gg < G; ++gg) acc[gg] = 0.f;
+        for (int it = 0; it < 8; ++it) {
+            const int t = warp * 4 + grp + 32 * it;
             if (t < nk) {
                 const uint4* kp = reinterpret_cast<const uint4*>(a.k + (kvbase + k0 + t) * kAttD + sub * 16);
-                const uint4 v0 = __ldg(kp), v1 = __ldg(kp + 1);
-                const uint32_t w8[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                float kf[16];
+                kv[it][0] = __ldg(kp);
+                kv[it][1] = __ldg(kp + 1);
+            } else {
+                kv[it][0] = make_uint4(0u, 0u, 0u, 0u);
+                kv[it][1] = make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const float2 f = __half22float2(u32_as_h2(w8[u]));
-                    kf[2 * u] = f.x;
-                    kf[2 * u + 1] = f.y;
-                }
+        for (int it = 0; it < 8; ++it) {
+            const int t = warp * 4 + grp + 32 * it;
+            const uint32_t w8[8] = {kv[it][0].x, kv[it][0].y, kv[it][0].z, kv[it][0].w,
+                                    kv[it][1].x, kv[it][1].y, kv[it][1].z, kv[it][1].w};
+            float kf[16];
 #pragma unroll
-                for (int gg = 0; gg < G; ++gg) {
-                    const float4* qp = reinterpret_cast<const float4*>(&qs[gg][sub * 16]);
-                    float s2 = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float4 qv = qp[i];
-                        s2 = fmaf(qv.x, kf[4 * i], s2);
-                        s2 = fmaf(qv.y, kf[4 * i + 1], s2);
-                        s2 = fmaf(qv.z, kf[4 * i + 2], s2);
-                        s2 = fmaf(qv.w, kf[4 * i + 3], s2);
-                    }
-                    acc[gg] = s2;
-                }
+            for (int u = 0; u < 8; ++u) {
+                const float2 f = __half22float2(u32_as_h2(w8[u]));
+                kf[2 * u] = f.x;
+                kf[2 * u + 1] = f.y;
             }
 #pragma unroll
             for (int gg = 0; gg < G; ++gg) {
-                float s2 = acc[gg];
+                const float4* qp = reinterpret_cast<const float4*>(&qs[gg][sub * 16]);
+                float s2 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float4 qv = qp[i];
+                    s2 = fmaf(qv.x, kf[4 * i], s2);
+                    s2 = fmaf(qv.y, kf[4 * i + 1], s2);
+                    s2 = fmaf(qv.z, kf[4 * i + 2], s2);
+                    s2 = fmaf(qv.w, kf[4 * i + 3], s2);
+                }
                 s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
                 s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
                 s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
@@ -171,6 +179,38 @@ __global__ void __launch_bounds__(kAttThreads) attn_partial_kernel(const __grid_
         if (lane == 0) { ml[warp][0] = m; ml[warp][1] = l; }
     }
     __syncthreads();
+    if constexpr (G <= 2) {
+        // p . V, G <= 2: thread (key group kg, d8) accumulates columns 8 d8 .. 8 d8 + 7
+        // over keys kg, kg + 16, ... -- 16-B loads, 16 threads per value row
+        const int d8 = tid & 15, kg = tid >> 4;
+        float o[G][8];
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[gg][i] = 0.f;
+        const uint4* vp = reinterpret_cast<const uint4*>(a.v + (kvbase + k0) * kAttD) + d8;
+#pragma unroll 8
+        for (int t = kg; t < nk; t += 16) {
+            const uint4 v4 = __ldg(vp + static_cast<int64_t>(t) * (kAttD / 8));
+            const uint32_t w4[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) {
+                const float p = sc[gg][t];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 f = __half22float2(u32_as_h2(w4[u]));
+                    o[gg][2 * u] = fmaf(p, f.x, o[gg][2 * u]);
+                    o[gg][2 * u + 1] = fmaf(p, f.y, o[gg][2 * u + 1]);
+                }
+            }
+        }
+        // the 16 key groups' partial rows go through shared memory and are
+        // summed in fixed order below
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) red16[kg][gg][d8 * 8 + i] = o[gg][i];
+    } else {
     // p . V: thread (quarter, d2) accumulates columns 2*d2, 2*d2+1 over keys
     // quarter, quarter + 4, ... (a key row is 64 threads x 4 B, coalesced)
     {
@@ -192,10 +232,18 @@ __global__ void __launch_bounds__(kAttThreads) attn_partial_kernel(const __grid_
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) { red[qt][gg][2 * d2] = o[gg][0]; red[qt][gg][2 * d2 + 1] = o[gg][1]; }
     }
+    }
     __syncthreads();
     for (int i = tid; i < G * kAttD; i += kAttThreads) {
         const int gg = i / kAttD, d = i - gg * kAttD;
-        const float s = ((red[0][gg][d] + red[1][gg][d]) + red[2][gg][d]) + red[3][gg][d];
+        float s;
+        if constexpr (G <= 2) {
+            s = 0.f;
+#pragma unroll
+            for (int kg = 0; kg < 16; ++kg) s += red16[kg][gg][d];
+        } else {
+            s = ((red[0][gg][d] + red[1][gg][d]) + red[2][gg][d]) + red[3][gg][d];
+        }
         const int64_t row = (static_cast<int64_t>(b) * a.Hq + g * G + gg) * a.nch + c;
         a.part_o[row * kAttD + d] = s;
         if (d == 0) { a.part_ml[row * 2] = ml[gg][0]; a.part_ml[row * 2 + 1] = ml[gg][1]; }
@@ -203,19 +251,33 @@ __global__ void __launch_bounds__(kAttThreads) attn_partial_kernel(const __grid_
 }
 
 __global__ void __launch_bounds__(kAttD) attn_combine_kernel(const __grid_constant__ AttArgs a) {
+    __shared__ float wts[kAttD * 2];                    // per-chunk weights exp(m_c - M) (<= 256 chunks)
+    __shared__ float red[kAttD / 32];
     pdl_launch_dependents();
     pdl_wait();
     const int b = blockIdx.y, h = blockIdx.x, d = threadIdx.x;
     const int L = a.lens[b];
     uint16_t* dst = a.out + (static_cast<int64_t>(b) * a.Hq + h) * kAttD + d;
     if (L <= 0) { *dst = 0; return; }
-    const int nc = (L + a.chunk - 1) / a.chunk;
+    const int nc = (L + a.chunk - 1) / a.chunk;          // <= 2 * kAttD (chunk >= 64, L <= 16384)
     const int64_t base = (static_cast<int64_t>(b) * a.Hq + h) * a.nch;
-    float M = -INFINITY;
-    for (int c = 0; c < nc; ++c) M = fmaxf(M, a.part_ml[(base + c) * 2]);
+    // all chunk maxima in parallel (thread c), the max by a block reduction
+    float mloc = -INFINITY, m2 = -INFINITY;
+    if (d < nc) mloc = a.part_ml[(base + d) * 2];
+    if (d + kAttD < nc) m2 = a.part_ml[(base + d + kAttD) * 2];
+    float M = fmaxf(mloc, m2);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    if ((d & 31) == 0) red[d >> 5] = M;
+    __syncthreads();
+    M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    if (d < nc) wts[d] = __expf(mloc - M);
+    if (d + kAttD < nc) wts[d + kAttD] = __expf(m2 - M);
+    __syncthreads();
     float num = 0.f, den = 0.f;
-    for (int c = 0; c < nc; ++c) {
-        const float w = __expf(a.part_ml[(base + c) * 2] - M);
+#pragma unroll 8
+    for (int c = 0; c < nc; ++c) {                       // fixed order: deterministic
+        const float w = wts[c];
         den = fmaf(w, a.part_ml[(base + c) * 2 + 1], den);
         num = fmaf(w, a.part_o[(base + c) * kAttD + d], num);
     }
@@ -249,11 +311,13 @@ static cudaLaunchConfig_t att_cfg(dim3 grid, dim3 block, bool pdl, cudaStream_t 
     return cfg;
 }
 
-// Keys per partial CTA: for G <= 2, enough CTAs for two per SM when the cache
-// is short (64..256, a multiple of 64; 7B decode with a 512-key cache 656 ->
-// 728 tok/s), else 256.
+// Keys per partial CTA: enough CTAs for two per SM when the grid is short
+// (64..256, a multiple of 64; 7B decode with a 512-key cache 656 -> 728
+// tok/s), else 256.
 static int attn_chunk(int64_t batch, int64_t Hkv, int64_t G, int64_t Lmax) {
-    if (G >= 4) return kAttChunk;                // thread-per-key scoring wants full chunks
+    // (the combine holds <= 256 chunk weights: chunk 256 for Lmax <= 65536, and
+    // smaller chunks only while the grid is short, i.e. for short caches)
+    if (G >= 4 || Lmax > 16384) return kAttChunk;        // thread-per-key scoring wants full chunks
     const int64_t target = 2 * static_cast<int64_t>(num_sms());
     int ch = kAttChunk;
     while (ch > 64 && batch * Hkv * ((Lmax + ch - 1) / ch) < target) ch -= 64;
