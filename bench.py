@@ -335,6 +335,7 @@ def run_ours(args, rank, world, local_rank):
 
     step = grouped_step if grouped else serial_step
     out_last = lambda: ys[-1]          # noqa: E731  the step's result (logits)
+    tp_allreduce = None
     block_io = None
     if args.block != "none":
         step, block_io = block_step(args, mats, weights, n, dev, stream)
@@ -348,7 +349,15 @@ def run_ours(args, rank, world, local_rank):
             ws = wss[(K, N)]
             return lambda x, pk, sc: ops.q4_matmul_ex(x, pk, sc, ws=ws, flags=flags, stream=stream)
 
-        lin = [tpm.megatron_linear(name.split(".")[-1], pk, sc, matmul=mm_for(K, N))
+        # decode: the row-parallel o / down sum fused into the kernel's
+        # epilogue over the ranks' exchange buffers (relax_q4_matmul_allreduce,
+        # SURVEY §8(f) F1) unless --nccl-allreduce
+        row_N = [N for name, K, N in mats if tpm.MEGATRON_KIND[name.split(".")[-1]] == "row"
+                 and tpm.fused_allreduce_ok(n, K)]
+        exchange = tpm.TpExchange(max(row_N)) if row_N and not args.nccl_allreduce else None
+        tp_allreduce = "fused-epilogue" if exchange is not None else "nccl"
+        lin = [tpm.megatron_linear(name.split(".")[-1], pk, sc, matmul=mm_for(K, N), exchange=exchange,
+                                   stream=stream)
                for (name, K, N), (pk, sc) in zip(mats, weights)]
         tp_out = [None]
 
@@ -527,7 +536,8 @@ def run_ours(args, rank, world, local_rank):
                    "layers_linears": len(mats), "weight_bytes": int(sum(inputs.q4_bytes(K, N) for _, K, N in mats)),
                    "parallelism": (f"megatron-tp{world}" if tp_mode else f"replicas{world}") if world > 1 else "single",
                    "l2": "not flushed: per-step working set %.2f GB >> 126 MB L2" % (bytes_step / 1e9),
-                   "graph": graph is not None, "pdl": not args.no_pdl, "schedule": sched},
+                   "graph": graph is not None, "pdl": not args.no_pdl, "schedule": sched,
+                   **({"tp_allreduce": tp_allreduce} if tp_mode else {})},
         "hbm_gbs": round(gbs, 1),
         "tflops": round(tflops, 3),
         "roofline": roof,
@@ -667,6 +677,9 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="tensor parallelism over the ranks even at N = 1 (one NCCL rank: exercises the "
                          "collectives of the TP step on one GPU); the default for N > 1")
+    ap.add_argument("--nccl-allreduce", action="store_true",
+                    help="TP decode: sum the row-parallel partials with an NCCL all_reduce instead of the fused "
+                         "kernel epilogue (relax_q4_matmul_allreduce)")
     ap.add_argument("--kv", type=int, default=0,
                     help="with --block fused at n = 1: run the decode attention over a KV cache of this length "
                          "in every layer (relax_kv_append + relax_attn_decode), the whole decode step")

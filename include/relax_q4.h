@@ -148,6 +148,57 @@ RELAX_API int relax_q4_matmul_grouped(const void* x, int64_t n, int64_t K, int c
                                       const uint32_t* const* packed_w, const void* const* scales,
                                       void* const* y, void* stream);
 
+/* ---- Tensor-parallel row split with the all-reduce fused
+ *
+ * The row-split (K-split) linears of Megatron TP -- o and down of a Llama
+ * block -- end in a sum over the ranks.  The paper fuses a consumer into its
+ * producer's kernel so that intermediate results never make a round trip
+ * through memory (§3.5 FuseOps / FuseTensorIR: "reduce the overall
+ * memory loading cost"); here the consumer is that sum, and it runs
+ * in the decode kernel's epilogue over NVLink peer memory instead of a
+ * separate NCCL all-reduce.  Each CTA stores the fp32 partial of its output
+ * rows (x_r . W_r over this rank's K slice) into every other rank's exchange
+ * buffer as 8-byte (epoch, value) words, waits until the same rows' words of
+ * every other rank carry the call's epoch, and sums the partials in rank
+ * order 0..world-1 (fp32, one fp16 rounding -- DESIGN.md §3 reading 14), so
+ * every rank ends with the same y bit for bit:
+ *   y[n, N] = fp16( sum_p  x_p[n, K] . dequant(W_p)[K, N] )  (+ residual)
+ *
+ * relax_tp_comm: bufs[p] is rank p's exchange buffer as mapped on THIS device
+ * (e.g. torch symmetric memory's buffer_ptrs), buf_bytes its size (>=
+ * relax_tp_comm_bytes(world, N)).  Every buffer must be zero-filled once,
+ * before the first call on any rank, and the ranks must then issue the same
+ * sequence of relax_q4_matmul_allreduce calls (same N and K per call) -- the
+ * per-CTA epoch counters inside the buffers pair up call e of every rank.
+ * A rank that never arrives makes the kernel trap after ~10 s (a CUDA error,
+ * not a hang). */
+#define RELAX_TP_MAX_WORLD 8
+typedef struct relax_tp_comm {
+    int32_t world;                      /* ranks in the group, 1..RELAX_TP_MAX_WORLD */
+    int32_t rank;                       /* this rank, 0..world-1 */
+    void* bufs[RELAX_TP_MAX_WORLD];     /* device pointers valid on this device; 16-B aligned */
+    size_t buf_bytes;                   /* bytes of every rank's buffer */
+} relax_tp_comm;
+
+/* Exchange-buffer bytes per rank for outputs of up to N_max features.
+ * Errors: RELAX_ERR_INVALID_ARG (bytes NULL, world outside 1..8, N_max <= 0). */
+RELAX_API int relax_tp_comm_bytes(int32_t world, int64_t N_max, size_t* bytes);
+
+/* y[n,N] = fp16(sum over ranks of x_r . W_r) (+ residual[n,N] when residual is
+ * non-NULL; it may equal y), for this rank's K slice: x fp16 [n][K], packed_w
+ * [N][K/8], scales [N][K/32] (the plain layout of relax_q4_matmul, K = this
+ * rank's slice).  n <= 2 (decode; larger n: relax_q4_matmul + an NCCL
+ * all-reduce), K % 256 == 0.  Asynchronous on `stream`; CUDA-graph capturable.
+ * Errors: RELAX_ERR_INVALID_ARG (comm NULL, world/rank out of range, a NULL
+ * buffer, n < 0, K <= 0, N <= 0), RELAX_ERR_WORKSPACE (buf_bytes too small),
+ * RELAX_ERR_UNSUPPORTED_SHAPE (n > 2, K % 256 != 0, a shape the decode kernel
+ * cannot hold), RELAX_ERR_MISALIGNED, RELAX_ERR_ALIAS (y overlapping x, the
+ * weights, this rank's buffer, or partially overlapping residual),
+ * RELAX_ERR_DEVICE, RELAX_ERR_CUDA. */
+RELAX_API int relax_q4_matmul_allreduce(const relax_tp_comm* comm, const void* x, int64_t n, int64_t K, int64_t N,
+                                        const uint32_t* packed_w, const void* scales, const void* residual,
+                                        void* y, void* stream);
+
 /* Explicit-schedule form, for parity tests of every variant and for benches.
  *   variant   enum relax_variant (AUTO = same as relax_q4_matmul_ws)
  *   split_k   TC only: split-K factor, 0 = choose; > 1 needs a workspace

@@ -535,6 +535,58 @@ int relax_q4_matmul_grouped(const void* x, int64_t n, int64_t K, int count, cons
     return RELAX_OK;
 }
 
+int relax_tp_comm_bytes(int32_t world, int64_t N_max, size_t* bytes) {
+    if (!bytes || world < 1 || world > RELAX_TP_MAX_WORLD || N_max <= 0) return RELAX_ERR_INVALID_ARG;
+    *bytes = rq4::tp_comm_bytes(world, N_max);
+    return RELAX_OK;
+}
+
+int relax_q4_matmul_allreduce(const relax_tp_comm* comm, const void* x, int64_t n, int64_t K, int64_t N,
+                              const uint32_t* packed_w, const void* scales, const void* residual, void* y,
+                              void* stream) {
+    if (!comm || comm->world < 1 || comm->world > RELAX_TP_MAX_WORLD || comm->rank < 0 ||
+        comm->rank >= comm->world || n < 0 || K <= 0 || N <= 0)
+        return RELAX_ERR_INVALID_ARG;
+    for (int p = 0; p < comm->world; ++p) {
+        if (!comm->bufs[p]) return RELAX_ERR_INVALID_ARG;
+        if (!rq4::aligned16(comm->bufs[p])) return RELAX_ERR_MISALIGNED;
+    }
+    if (comm->buf_bytes < rq4::tp_comm_bytes(comm->world, N)) return RELAX_ERR_WORKSPACE;
+    if (K % rq4::kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    // the fused exchange lives in the streamed decode kernel: n <= 2, K % 256 == 0
+    if (n > 2 || !rq4::gemv_stream_ok(n >= 2 ? 2 : 1, K, N) || rq4::gemv_stream_grid(K, N) > rq4::kTpMaxCta)
+        return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if (n == 0) return RELAX_OK;
+    if (!x || !packed_w || !scales || !y) return RELAX_ERR_INVALID_ARG;
+    if (!rq4::aligned16(x) || !rq4::aligned16(packed_w) || !rq4::aligned16(scales) || !rq4::aligned16(y) ||
+        (residual && !rq4::aligned16(residual)))
+        return RELAX_ERR_MISALIGNED;
+    const size_t xb = static_cast<size_t>(n) * K * 2, yb = static_cast<size_t>(n) * N * 2;
+    const size_t wb = static_cast<size_t>(N) * K / 2, sb = static_cast<size_t>(N) * (K / rq4::kGroup) * 2;
+    const size_t cb = rq4::tp_comm_bytes(comm->world, N);
+    if (rq4::overlap(y, yb, x, xb) || rq4::overlap(y, yb, packed_w, wb) || rq4::overlap(y, yb, scales, sb) ||
+        rq4::overlap(y, yb, comm->bufs[comm->rank], cb) || (residual && residual != y && rq4::overlap(y, yb, residual, yb)))
+        return RELAX_ERR_ALIAS;
+    const int rc = rq4::check_device();
+    if (rc != RELAX_OK) return rc;
+    rq4::TpComm tc;
+    tc.world = comm->world;
+    tc.rank = comm->rank;
+    for (int p = 0; p < comm->world; ++p) tc.bufs[p] = static_cast<uint8_t*>(comm->bufs[p]);
+    rq4::Fusion fu;
+    fu.ops = rq4::kOpTpAllReduce | (residual ? RELAX_OP_RESIDUAL : 0u);
+    fu.res = static_cast<const uint16_t*>(residual);
+    fu.tp = &tc;
+    const int e = rq4::launch_gemv_stream(static_cast<const uint16_t*>(x), n, K, N, packed_w,
+                                          static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), true,
+                                          static_cast<cudaStream_t>(stream), fu);
+    if (e != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
 int relax_q4_matmul_ws(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
                        const void* scales, void* y, void* workspace, size_t ws_bytes, void* stream) {
     return rq4::matmul_impl(x, n, K, N, packed_w, scales, y, workspace, ws_bytes, 0, 0, 0, 0u, stream);

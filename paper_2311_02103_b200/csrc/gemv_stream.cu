@@ -64,7 +64,77 @@ struct GsArgs {
     const uint8_t* sgp[kGsMaxGroup];
     uint16_t* ygp[kGsMaxGroup];
     int64_t Ngp[kGsMaxGroup];
+    // kOpTpAllReduce (relax_q4_matmul_allreduce): rank tp_rank of tp_world,
+    // tp_bufs[p] = rank p's exchange buffer mapped on this device
+    int tp_world, tp_rank;
+    uint8_t* tp_bufs[kTpMaxWorld];
 };
+
+// Fused row-split all-reduce epilogue.  The
+// CTA's fp32 partial of its rows (this rank's K slice) goes to every other
+// rank as 8-byte words (epoch << 32 | value) stored straight into the peers'
+// buffers over NVLink; the CTA then reads the same rows' words of every other
+// rank from its own buffer, spinning until each carries this call's epoch,
+// and sums the world partials in rank order 0..world-1 (its own from
+// registers) -- the same order on every rank, so all ranks hold the same y
+// bit for bit.  The epoch of a call is a per-CTA counter in the rank's own
+// buffer (every rank makes the same sequence of calls, so the epochs agree);
+// the word slots alternate with its parity, which is enough: a rank reaches
+// call e + 2 only after it read every rank's words of call e + 1, which every
+// rank wrote after it had finished reading the slots of call e.  No fences:
+// the flag is part of the word (NCCL's LL idea).
+template <int NT>
+__device__ __forceinline__ void tp_allreduce_epilogue(const GsArgs& a, const float* part, int rows, int64_t row0,
+                                                      float rescale, uint16_t* y, uint32_t ops, uint32_t e) {
+    const int64_t N = a.N;
+    const size_t slot0 = static_cast<size_t>(e & 1u) * a.tp_world;      // [parity][source rank]
+    auto woff = [&](int src, int t, int64_t row) {
+        return kTpHdrBytes + ((((slot0 + src) * 2 + t) * N) + row) * 8;
+    };
+    auto partial = [&](int rl, int t) {
+        float sum = 0.f;
+        for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
+        return sum * rescale;
+    };
+    if (a.tp_world > 1) {
+        for (int o = threadIdx.x; o < rows * NT; o += blockDim.x) {
+            const int rl = o / NT;
+            const int t = o - rl * NT;
+            const uint64_t word = (static_cast<uint64_t>(e) << 32) | __float_as_uint(partial(rl, t));
+            const size_t off = woff(a.tp_rank, t, row0 + rl);
+            for (int p = 0; p < a.tp_world; ++p)
+                if (p != a.tp_rank) st_relaxed_sys_u64(a.tp_bufs[p] + off, word);
+        }
+    }
+    const uint8_t* own = a.tp_bufs[a.tp_rank];
+    for (int o = threadIdx.x; o < rows * NT; o += blockDim.x) {
+        const int rl = o / NT;
+        const int t = o - rl * NT;
+        const float mine = partial(rl, t);
+        float acc = 0.f;
+        for (int p = 0; p < a.tp_world; ++p) {
+            float c = mine;
+            if (p != a.tp_rank) {
+                const uint8_t* src = own + woff(p, t, row0 + rl);
+                uint64_t w = ld_relaxed_sys_u64(src);
+                if (static_cast<uint32_t>(w >> 32) != e) {
+                    const uint64_t t0 = globaltimer();
+                    do {
+                        // a rank that never arrives (call sequences that differ
+                        // between ranks) fails the launch instead of hanging
+                        if (globaltimer() - t0 > 10000000000ull) __trap();
+                        w = ld_relaxed_sys_u64(src);
+                    } while (static_cast<uint32_t>(w >> 32) != e);
+                }
+                c = __uint_as_float(static_cast<uint32_t>(w));
+            }
+            acc = p == 0 ? c : acc + c;
+        }
+        const int64_t idx = static_cast<int64_t>(t) * N + row0 + rl;
+        y[idx] = residual_add(__half_as_ushort(__float2half_rn(acc)), ops,
+                              (ops & RELAX_OP_RESIDUAL) ? a.res[idx] : uint16_t(0));
+    }
+}
 
 // ---- optional per-CTA timeline (experiments build only, RELAX_Q4_TRACE=1;
 // include/relax_q4_debug.h)
@@ -400,6 +470,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
     const uint64_t t_start = (RQ4_TRACE && a.trace_seq) ? gtime() : 0;
     __shared__ uint64_t tr_wait, tr_first;
     __shared__ float rms_red[(FU ? 32 : 1) * NT];        // RMSNorm partials (WK <= 32)
+    __shared__ uint32_t tp_epoch;                         // kOpTpAllReduce: this call's epoch
     uint16_t res_pre = 0;                                 // RESIDUAL: prefetched first value
     if (threadIdx.x == 0) {
         for (int i = 0; i < a.NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], a.WK); }
@@ -444,6 +515,13 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
         }
         pdl_wait();
         if (RQ4_TRACE && a.trace_seq && warp == 0 && lane == 0) tr_wait = gtime();
+        if (FU && (ops & kOpTpAllReduce) && threadIdx.x == 0) {
+            // this call's epoch (the counter is touched by this CTA index only,
+            // and the previous call has completed: griddepcontrol.wait)
+            uint32_t* ctr = reinterpret_cast<uint32_t*>(a.tp_bufs[a.tp_rank]) + blockIdx.x;
+            tp_epoch = *ctr + 1u;
+            *ctr = tp_epoch;
+        }
         uint4 xr[NT][4];
         float ze[NT], zo[NT];
 #pragma unroll
@@ -524,7 +602,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
     __syncthreads();
     // fixed-order sum over the WK K-columns; fp32 -> fp16 RNE
     const float rescale = ZPF == 1 ? 16777216.0f : 1.0f;     // exact power-of-two rescale
-    if (ops & RELAX_OP_SILU_MUL) {
+    if (FU && (ops & kOpTpAllReduce)) {
+        tp_allreduce_epilogue<NT>(a, part, rows, row0, rescale, y_base, ops, tp_epoch);
+    } else if (ops & RELAX_OP_SILU_MUL) {
         const int np = rows / 2;
         for (int o = threadIdx.x; o < np * NT; o += blockDim.x) {
             const int pl = o / NT;
@@ -625,6 +705,8 @@ static GsConfig gs_config(int64_t K, int64_t N, int pair = 1) {
 // attribute set once per device and kernel).
 constexpr int kGsSmemMax = 210 * 1024;
 
+int gemv_stream_grid(int64_t K, int64_t N) { return gs_config(K, N).grid; }
+
 bool gemv_stream_ok(int nt, int64_t K, int64_t N, int pair) {
     if (nt < 1 || nt > 2 || K % 256 != 0 || N < 1 || N >= (int64_t{1} << 24)) return false;
     if (pair != 1 && (pair != 2 || N % 2 != 0)) return false;
@@ -709,6 +791,15 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.prefetch = gs_prefetch();
         a.trigger = gs_trigger();
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
+        a.tp_world = 0;
+        a.tp_rank = 0;
+        for (int p = 0; p < kTpMaxWorld; ++p) a.tp_bufs[p] = nullptr;
+        if (fu.tp) {
+            if (c.grid > kTpMaxCta) return static_cast<int>(cudaErrorInvalidConfiguration);
+            a.tp_world = fu.tp->world;
+            a.tp_rank = fu.tp->rank;
+            for (int p = 0; p < fu.tp->world; ++p) a.tp_bufs[p] = fu.tp->bufs[p];
+        }
         int rc;
 #ifdef RQ4_EXPERIMENTS
         if (zpf == 0) rc = cnt == 1 ? launch_gs_z<1, 0>(a, c, pdl, stream) : launch_gs_z<2, 0>(a, c, pdl, stream);

@@ -43,12 +43,30 @@ inline cudaError_t set_kernel_smem(const void* fn, int dyn_bytes) {
 // steady-state cost is one uncontended lock and a hash lookup.
 cudaError_t ensure_kernel_attrs(const void* fn, int dyn_bytes, bool cluster = false);
 
+// Tensor-parallel row split with the all-reduce fused into the decode
+// kernel's epilogue (relax_q4_matmul_allreduce).  Each rank's
+// exchange buffer: [epoch counters: kTpMaxCta u32][words: 2 parities x world
+// x 2 tokens x N u64], a word = (epoch << 32) | fp32 bits of one partial.
+constexpr int kTpMaxWorld = 8;
+constexpr int kTpMaxCta = 1024;
+constexpr size_t kTpHdrBytes = static_cast<size_t>(kTpMaxCta) * 4;
+constexpr uint32_t kOpTpAllReduce = 1u << 31;     // internal Fusion bit (never in the public ops)
+struct TpComm {
+    int world = 0;
+    int rank = 0;
+    uint8_t* bufs[kTpMaxWorld] = {};
+};
+inline size_t tp_comm_bytes(int world, int64_t N) {
+    return kTpHdrBytes + static_cast<size_t>(2) * world * 2 * static_cast<size_t>(N) * 8;
+}
+
 // Fused neighbours of one call (include/relax_q4.h RELAX_OP_*); ops == 0: none.
 struct Fusion {
     uint32_t ops = 0;
     float eps = 0.f;
     const uint16_t* gamma = nullptr;   // RMSNORM_X, fp16 [K]
     const uint16_t* res = nullptr;     // RESIDUAL, fp16 [n][N_out]
+    const TpComm* tp = nullptr;        // kOpTpAllReduce: the exchange buffers
 };
 
 enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2, kVariantSmallN = 3 };
@@ -84,6 +102,9 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
 // (K % 256 == 0, N < 2^24, its shared-memory footprint within the attribute);
 // pair = 2 with the SiLU-mul epilogue (CTAs own whole (gate, up) row pairs).
 bool gemv_stream_ok(int nt, int64_t K, int64_t N, int pair = 1);
+// CTAs of the decode kernel for this shape (the fused all-reduce keys its
+// epoch counters by CTA, so the grid must be <= kTpMaxCta and co-resident).
+int gemv_stream_grid(int64_t K, int64_t N);
 // Grouped decode launch: up to 4 matrices sharing x and K in one kernel.
 bool gemv_stream_grouped_ok(int64_t n, int64_t K, int count, const int64_t* N);
 int launch_gemv_stream_grouped(const uint16_t* x, int64_t n, int64_t K, int count, const int64_t* N,

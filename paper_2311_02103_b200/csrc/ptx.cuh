@@ -259,6 +259,19 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
+// ------------------------------------------- system-scope (NVLink peer) words
+// 8-byte relaxed stores / loads at system scope: single-copy atomic, so a word
+// carrying (epoch, value) is seen whole or not at all by a peer GPU -- the
+// flag travels with the data and no fence is needed.
+__device__ __forceinline__ void st_relaxed_sys_u64(void* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const void* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ----------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;

@@ -41,7 +41,8 @@ FLAG_TILE_PER_CTA = 4
 EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "relax_q4_matmul_ex",
            "relax_query_schedule", "relax_q4_dequant", "relax_status_str", "relax_version",
            "relax_plan_workspace_fused", "relax_q4_matmul_fused", "relax_q4_repack",
-           "relax_attn_decode_workspace", "relax_attn_decode", "relax_kv_append", "relax_q4_matmul_grouped")
+           "relax_attn_decode_workspace", "relax_attn_decode", "relax_kv_append", "relax_q4_matmul_grouped",
+           "relax_tp_comm_bytes", "relax_q4_matmul_allreduce")
 
 # fused neighbours (include/relax_q4.h RELAX_OP_*)
 OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL = 1, 2, 4
@@ -51,6 +52,15 @@ class Fusion(ctypes.Structure):
     """struct relax_q4_fusion."""
     _fields_ = [("ops", ctypes.c_uint32), ("rms_eps", ctypes.c_float),
                 ("rms_weight", ctypes.c_void_p), ("residual", ctypes.c_void_p)]
+
+
+TP_MAX_WORLD = 8
+
+
+class TpComm(ctypes.Structure):
+    """struct relax_tp_comm: bufs[p] = rank p's exchange buffer mapped on this device."""
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("bufs", ctypes.c_void_p * TP_MAX_WORLD), ("buf_bytes", ctypes.c_size_t)]
 
 
 class RelaxError(RuntimeError):
@@ -108,6 +118,10 @@ def lib() -> ctypes.CDLL:
         L.relax_attn_decode.restype = I
         L.relax_kv_append.argtypes = [P, P, P, I64, I64, I64, I64, P, P, P]
         L.relax_kv_append.restype = I
+        L.relax_tp_comm_bytes.argtypes = [ctypes.c_int32, I64, ctypes.POINTER(SZ)]
+        L.relax_tp_comm_bytes.restype = I
+        L.relax_q4_matmul_allreduce.argtypes = [ctypes.POINTER(TpComm), P, I64, I64, I64, P, P, P, P, P]
+        L.relax_q4_matmul_allreduce.restype = I
         _lib = L
         return L
 
@@ -244,6 +258,40 @@ def q4_matmul_grouped(x, weights, ys=None, stream=None):
     rc = lib().relax_q4_matmul_grouped(_ptr(x), x.shape[0], x.shape[1], cnt, Ns, Ws, Ss, Ys, _stream_ptr(stream))
     _check(rc, "relax_q4_matmul_grouped")
     return outs
+
+
+def tp_comm_bytes(world: int, N_max: int) -> int:
+    """relax_tp_comm_bytes: exchange-buffer bytes per rank for outputs of <= N_max features."""
+    out = ctypes.c_size_t(0)
+    _check(lib().relax_tp_comm_bytes(world, N_max, ctypes.byref(out)), "relax_tp_comm_bytes")
+    return int(out.value)
+
+
+def make_tp_comm(world: int, rank: int, buf_ptrs, buf_bytes: int) -> TpComm:
+    """The relax_tp_comm of this rank from the ranks' buffer pointers (as
+    mapped on this device; e.g. torch symmetric memory's buffer_ptrs)."""
+    if not 1 <= world <= TP_MAX_WORLD or not 0 <= rank < world or len(buf_ptrs) != world:
+        raise ValueError(f"world {world}, rank {rank}, {len(buf_ptrs)} buffers")
+    c = TpComm()
+    c.world, c.rank, c.buf_bytes = world, rank, int(buf_bytes)
+    for p, ptr in enumerate(buf_ptrs):
+        c.bufs[p] = int(ptr)
+    return c
+
+
+def q4_matmul_allreduce(x, packed_w, scales, comm: TpComm, residual=None, y=None, stream=None):
+    """relax_q4_matmul_allreduce: y = fp16(sum over ranks of x_r . W_r) (+ residual)
+    with the sum fused into the decode kernel over the ranks' exchange buffers
+    (n <= 2; every rank must make the same sequence of calls)."""
+    import torch
+    n, K, N = _shapes(x, packed_w, scales)
+    y = _out(y, n, N, x)
+    if residual is not None:
+        _check_tensor(residual, "residual", torch.float16, (n, N), dev=x.device)
+    rc = lib().relax_q4_matmul_allreduce(ctypes.byref(comm), _ptr(x), n, K, N, _ptr(packed_w), _ptr(scales),
+                                         _ptr(residual), _ptr(y), _stream_ptr(stream))
+    _check(rc, "relax_q4_matmul_allreduce")
+    return y
 
 
 def q4_matmul_ex(x, packed_w, scales, y=None, ws=None, variant=VARIANT_AUTO, split_k=0, bn=0,

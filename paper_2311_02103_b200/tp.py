@@ -86,21 +86,63 @@ class ColumnParallelQ4:
         return buf.view(world, n, npart).permute(1, 0, 2).reshape(n, world * npart)
 
 
+class TpExchange:
+    """The exchange buffers of relax_q4_matmul_allreduce (the row split with
+    its all-reduce fused into the decode kernel) for one
+    process group.  torch symmetric memory is the plumbing: it allocates each
+    rank's buffer and maps every peer's buffer into this process (NVLink peer
+    memory on the box); the library only sees the pointers.  The buffers are
+    zero-filled and the group synchronised once here; afterwards every rank
+    must issue the same sequence of fused calls (include/relax_q4.h)."""
+
+    def __init__(self, N_max: int, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        from . import ops
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.N_max = N_max
+        self.nbytes = ops.tp_comm_bytes(self.world, N_max)
+        self.buf = symm.empty(self.nbytes, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+        name = (group if group is not None else dist.group.WORLD).group_name
+        self.handle = symm.rendezvous(self.buf, name)
+        ptrs = list(self.handle.buffer_ptrs)
+        off = self.buf.data_ptr() - ptrs[self.rank]          # the same offset in every rank's allocation
+        self.buf.zero_()
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+        self.comm = ops.make_tp_comm(self.world, self.rank, [p + off for p in ptrs], self.nbytes)
+
+
+def fused_allreduce_ok(n: int, K: int) -> bool:
+    """Whether relax_q4_matmul_allreduce takes this call (decode n <= 2, K % 256 == 0)."""
+    return 1 <= n <= 2 and K % 256 == 0
+
+
 @dataclass
 class RowParallelQ4:
     """Partial y_r = x_r . W_r over this rank's K/p slice, summed over the
-    ranks by one all_reduce.  The kernel's partials are fp16 (its output
-    type); the sum runs in fp32 and is rounded to fp16 once (DESIGN.md §3
-    reading 14), so the result does not depend on p beyond the fp16 partials."""
+    ranks.  With an `exchange` (TpExchange) and a decode-sized x, the sum is
+    fused into the kernel (relax_q4_matmul_allreduce: fp32 partials over
+    NVLink peer memory, summed in rank order, one fp16 rounding).  Otherwise
+    one NCCL all_reduce: the kernel's partials are fp16 (its output type), the
+    sum runs in fp32 and is rounded to fp16 once (DESIGN.md §3 reading 14)."""
     packed: object
     scales: object
     group: object = None
     matmul: Optional[Callable] = None
     reduce_fp32: bool = True
+    exchange: Optional[TpExchange] = None
+    stream: object = None
 
     def __call__(self, x_shard):
         import torch
         import torch.distributed as dist
+        if self.exchange is not None and fused_allreduce_ok(x_shard.shape[0], x_shard.shape[1]):
+            from . import ops
+            return ops.q4_matmul_allreduce(x_shard, self.packed, self.scales, self.exchange.comm,
+                                           stream=self.stream)
         mm = self.matmul or _default_matmul()
         y = mm(x_shard, self.packed, self.scales)         # partial [n, N]
         if self.reduce_fp32:
@@ -129,10 +171,11 @@ def shard_shape(name: str, K: int, N: int, world: int):
     return K, hi - lo
 
 
-def megatron_linear(name: str, packed, scales, group=None, matmul=None):
-    """The TP wrapper of one Llama linear given this rank's shard."""
+def megatron_linear(name: str, packed, scales, group=None, matmul=None, exchange=None, stream=None):
+    """The TP wrapper of one Llama linear given this rank's shard (`exchange`:
+    the row-split linears fuse their all-reduce at decode)."""
     if MEGATRON_KIND[name] == "row":
-        return RowParallelQ4(packed, scales, group=group, matmul=matmul)
+        return RowParallelQ4(packed, scales, group=group, matmul=matmul, exchange=exchange, stream=stream)
     return ColumnParallelQ4(packed, scales, group=group, gather=(name == "lm_head"), matmul=matmul)
 
 
@@ -140,4 +183,5 @@ def split_x_for_rows(x, rank: int, world: int):
     """The K-slice of x a row-split rank consumes."""
     K = x.shape[1]
     lo, hi = shard_bounds(K, rank, world, GROUP)
-    return x[:, lo:hi].contiguous()
+    xs = x[:, lo:hi]
+    return xs.contiguous() if hasattr(xs, "contiguous") else np.ascontiguousarray(xs)

@@ -121,11 +121,57 @@ def repack_validation(L):
     assert L.relax_q4_repack(A, A + MB, 256, 64, 1, 64, P, P + MB, None) == 6      # valid: device check
 
 
+def allreduce_validation(L):
+    """relax_q4_matmul_allreduce (F1) and relax_tp_comm_bytes."""
+    nb = ctypes.c_size_t(0)
+    assert L.relax_tp_comm_bytes(0, 4096, ctypes.byref(nb)) == 1
+    assert L.relax_tp_comm_bytes(9, 4096, ctypes.byref(nb)) == 1
+    assert L.relax_tp_comm_bytes(2, 0, ctypes.byref(nb)) == 1
+    assert L.relax_tp_comm_bytes(2, 4096, None) == 1
+    assert L.relax_tp_comm_bytes(2, 4096, ctypes.byref(nb)) == 0
+    # epoch counters, then 2 parities x world x 2 tokens x N (epoch, fp32) words
+    assert nb.value == 1024 * 4 + 2 * 2 * 2 * 4096 * 8
+    B = A + 128 * MB
+
+    def comm(world=2, rank=0, bufs=None, nbytes=None):
+        c = ops.TpComm()
+        c.world, c.rank = world, rank
+        for p, b in enumerate(bufs if bufs is not None else [B + p * 4 * MB for p in range(world)]):
+            c.bufs[p] = b
+        L.relax_tp_comm_bytes(max(1, min(world, 8)), 256, ctypes.byref(nb))
+        c.buf_bytes = nb.value if nbytes is None else nbytes
+        return c
+
+    def ar(c, x=A, n=1, K=256, N=256, w=A + 8 * MB, s=A + 16 * MB, res=0, y=A + 24 * MB):
+        return L.relax_q4_matmul_allreduce(ctypes.byref(c) if c is not None else None, x, n, K, N, w, s, res, y,
+                                           None)
+    assert ar(None) == 1
+    assert ar(comm(world=0)) == 1
+    assert ar(comm(world=9, bufs=[B] * 8)) == 1
+    assert ar(comm(rank=2)) == 1
+    assert ar(comm(bufs=[B, 0])) == 1                   # a missing peer buffer
+    assert ar(comm(bufs=[B, B + 4 * MB + 8])) == 3       # misaligned peer buffer
+    assert ar(comm(nbytes=1024)) == 5                    # buffer too small for N
+    assert ar(comm(), n=-1) == 1
+    assert ar(comm(), K=100) == 2
+    assert ar(comm(), n=3) == 2                          # decode only (n <= 2)
+    assert ar(comm(), K=288) == 2                        # K % 256 != 0
+    assert ar(comm(), n=0, x=0, y=0) == 0                # no-op
+    assert ar(comm(), y=0) == 1
+    assert ar(comm(), x=A + 2) == 3
+    assert ar(comm(), y=A + 8 * MB) == 4                 # y over the weights
+    assert ar(comm(), y=B) == 4                          # y over this rank's exchange buffer
+    assert ar(comm(), res=A + 24 * MB + 16) == 4         # partial overlap with residual
+    assert ar(comm(), res=A + 24 * MB) == 6              # in-place residual is allowed
+    assert ar(comm()) == 6                               # valid: device check
+    assert ar(comm(world=1, bufs=[B])) == 6
+
+
 def main():
     assert os.environ.get("CUDA_VISIBLE_DEVICES", None) == "", "run with CUDA_VISIBLE_DEVICES=''"
     L = ops.lib()
     for f in (validation_codes, workspace_too_small, plan_invalid, fused_validation_codes, fused_plan_soundness,
-              repack_validation):
+              repack_validation, allreduce_validation):
         f(L)
         print("ok", f.__name__)
     print("ALL OK")

@@ -30,7 +30,7 @@ def header_symbols():
 
 def test_exports_every_declared_symbol(L):
     syms = header_symbols()
-    assert len(syms) == 15
+    assert len(syms) == 17
     assert sorted(ops.EXPORTS) == syms
     for s in syms:
         assert hasattr(L, s), s
