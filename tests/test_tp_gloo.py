@@ -162,3 +162,18 @@ def test_shard_bounds_errors():
     with pytest.raises(ValueError):
         tp.shard_bounds(96, 0, 2, align=32)   # 48 not a multiple of 32
     assert tp.shard_bounds(8192, 3, 8, 32) == (3072, 4096)
+
+
+def test_fused_allreduce_routing():
+    """Which row-split calls take the fused decode all-reduce (include/relax_q4.h
+    relax_q4_matmul_allreduce: n <= 2, K % 256 == 0): the Llama TP shards of o
+    and down, and the ones that fall back to matmul + NCCL."""
+    assert tp.fused_allreduce_ok(1, 1024) and tp.fused_allreduce_ok(2, 3584)      # 70B o / down at TP8
+    assert tp.fused_allreduce_ok(1, 512)                                           # 7B o at TP8
+    assert not tp.fused_allreduce_ok(1, 1376)                                      # 7B down at TP8 (11008 / 8)
+    assert not tp.fused_allreduce_ok(3, 1024) and not tp.fused_allreduce_ok(0, 1024)
+    K, N = tp.shard_shape("down", 28672, 8192, 8)
+    assert (K, N) == (3584, 8192) and tp.fused_allreduce_ok(1, K)
+    # without an exchange RowParallelQ4 never takes the fused path (CPU, gloo-testable)
+    lin = tp.RowParallelQ4(None, None, matmul=lambda x, pk, sc: x)
+    assert lin.exchange is None
