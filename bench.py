@@ -319,9 +319,9 @@ def run_ours(args, rank, world, local_rank):
         span = 3 if kind == "q" else 2 if kind == "gate" else 1
         groups.append(list(range(i, i + span)))
         i += span
-    # (a group is one launch only at decode, n <= 2; beyond that its members run
-    # one by one anyway, so the plain chain is used)
-    grouped = not args.serial and not args.no_pdl and n <= 2 and any(len(g) > 1 for g in groups)
+    # (a group is one launch at decode, n <= 2, and for small batches, n <= 8;
+    # beyond that its members run one by one anyway, so the plain chain is used)
+    grouped = not args.serial and not args.no_pdl and n <= 8 and any(len(g) > 1 for g in groups)
 
     def grouped_step():
         for g in groups:
@@ -512,8 +512,10 @@ def run_ours(args, rank, world, local_rank):
     launches = 0
     for g in (groups if grouped else [[j] for j in range(len(mats))]):
         kinds = [sched[f"{mats[j][1]}x{mats[j][2]}"]["variant"] for j in g]
-        if len(g) > 1 and all(k == "gemv" for k in kinds):
+        if len(g) > 1 and n <= 2:
             launches += -(-n // 2)                     # one grouped decode launch per token pair
+        elif len(g) > 1 and n <= 8:
+            launches += 1                              # one grouped small-batch launch
         else:
             launches += sum(per_kind[k]() for k in kinds)
     if args.kv > 0:

@@ -138,8 +138,10 @@ RELAX_API int relax_q4_matmul_ws(const void* x, int64_t n, int64_t K, int64_t N,
  * during the call only) holding device pointers.  For decode (n <= 2) the
  * members run as ONE launch of the streamed decode kernel, its CTAs split
  * among them in proportion to N[i] -- one dependent step of the stream
- * instead of `count` (horizontal fusion of independent operators); other n
- * run member by member through relax_q4_matmul.  Results equal `count`
+ * instead of `count` (horizontal fusion of independent operators); small
+ * batches (3 <= n <= 8, K % 256 == 0, K <= 16384, sum N[i] >= 2048) run as
+ * ONE launch of the small-batch kernel the same way; other n run member by
+ * member through relax_q4_matmul.  Results equal `count`
  * separate relax_q4_matmul calls within the tolerance (bitwise for the
  * pinned cases).  No workspace.  Errors as relax_q4_matmul, plus
  * RELAX_ERR_INVALID_ARG for count outside 1..4 and RELAX_ERR_ALIAS when an

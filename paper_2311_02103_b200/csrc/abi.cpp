@@ -527,6 +527,30 @@ int relax_q4_matmul_grouped(const void* x, int64_t n, int64_t K, int count, cons
         }
         return RELAX_OK;
     }
+    // small batches: one small-n launch for the whole group when the members
+    // together are wide enough for it (the rule of smalln_preferred applied to
+    // the group's total rows)
+    {
+        int64_t tot = 0;
+        for (int i = 0; i < count; ++i) tot += N[i];
+        if (rq4::smalln_preferred(n, K, tot) && rq4::smalln_mma_grouped_ok(n, K, count, N)) {
+            const int rc = rq4::check_device();
+            if (rc != RELAX_OK) return rc;
+            const uint16_t* sp[4];
+            uint16_t* yp[4];
+            for (int i = 0; i < count; ++i) {
+                sp[i] = static_cast<const uint16_t*>(scales[i]);
+                yp[i] = static_cast<uint16_t*>(y[i]);
+            }
+            const int e = rq4::launch_smalln_mma_grouped(static_cast<const uint16_t*>(x), n, K, count, N, packed_w, sp,
+                                                         yp, true, static_cast<cudaStream_t>(stream));
+            if (e != 0) {
+                cudaGetLastError();
+                return RELAX_ERR_CUDA;
+            }
+            return RELAX_OK;
+        }
+    }
     // otherwise each member through the ordinary dispatch (same results)
     for (int i = 0; i < count; ++i) {
         const int rc = rq4::matmul_impl(x, n, K, N[i], packed_w[i], scales[i], y[i], nullptr, 0, 0, 0, 0, 0u, stream);

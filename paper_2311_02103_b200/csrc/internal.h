@@ -116,6 +116,12 @@ bool smalln_mma_ok(int64_t n, int64_t K, int64_t N);
 int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                       const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream);
 int smalln_max_n();                 // largest n the automatic dispatch sends to it
+// Grouped small-batch launch: up to 4 matrices sharing x and K in one kernel
+// per 8 tokens (CTAs split in proportion to the matrices' 16-row blocks).
+bool smalln_mma_grouped_ok(int64_t n, int64_t K, int count, const int64_t* N);
+int launch_smalln_mma_grouped(const uint16_t* x, int64_t n, int64_t K, int count, const int64_t* N,
+                              const uint32_t* const* w, const uint16_t* const* s, uint16_t* const* y, bool pdl,
+                              cudaStream_t stream);
 // Decode attention over a symbolic KV length and the KV append (attention.cu).
 size_t attn_workspace_bytes(int64_t batch, int64_t Hq, int64_t Lmax);
 int launch_attention_decode(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* lens,

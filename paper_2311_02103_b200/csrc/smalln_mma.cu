@@ -39,6 +39,7 @@
 //   * PDL: the producer streams weights before griddepcontrol.wait; only the
 //     x loads and y stores wait for the previous kernel.
 #include <cstdio>
+#include <cstring>
 #include "internal.h"
 #include "relax_q4.h"
 #include "ptx.cuh"
@@ -58,13 +59,25 @@ constexpr uint32_t kSnStageBytes = kSnCodeBytes + kSnScaleBytes;  // 18 KB (mult
 // Two CTAs per SM must fit (this kernel and the next one under PDL).
 constexpr size_t kSnSmemCap = 113 * 1024;
 
+constexpr int kSnMaxGroup = 4;                       // matrices per grouped launch
+
 struct SnArgs {
     const uint16_t* x;     // [n][K] fp16
-    uint16_t* y;           // [n][N]
-    int64_t N;
     int K, G, n, NS, nkc;
-    int64_t nrb;           // 16-row blocks in N
     int rows_max;          // 16 * the most row blocks any CTA owns (partial-sum slots per warp)
+    // matrices of the launch (relax_q4_matmul_grouped: q/k/v, gate/up share x):
+    // matrix m takes CTAs [cta0[m], cta0[m+1]) and writes ygp[m] [n][Ngp[m]]
+    int nmat;
+    int cta0[kSnMaxGroup + 1];
+    uint16_t* ygp[kSnMaxGroup];
+    int64_t Ngp[kSnMaxGroup];
+    int64_t nrbgp[kSnMaxGroup];   // 16-row blocks of each matrix
+};
+
+// TMA descriptors of every matrix of the launch (kernel parameter space)
+struct alignas(64) SnMaps {
+    CUtensorMap w[kSnMaxGroup];   // codes: {32 words, N rows, K/256 chunks}, box {32, 16, 8}
+    CUtensorMap s[kSnMaxGroup];   // scales: {K/32, N}, box {64, 16}
 };
 
 __device__ __forceinline__ void mma16816_acc(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
@@ -91,8 +104,7 @@ __device__ __forceinline__ void group_mma(float (&d)[4], uint32_t wa, uint32_t w
 // W consumer warps; warp w owns groups [GPW w, GPW (w+1)) of every 64-group chunk.
 template <int W>
 __global__ void __launch_bounds__((W + 1) * 32, 2)
-q4_smalln_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap ms,
-                     const __grid_constant__ SnArgs a) {
+q4_smalln_mma_kernel(const __grid_constant__ SnMaps maps, const __grid_constant__ SnArgs a) {
     constexpr int kSnWarps = W;
     constexpr int GPW = kSnChunkG / W;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -104,8 +116,16 @@ q4_smalln_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_consta
     uint64_t* empty = full + a.NS;
     float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 256);
 
-    const int64_t rb0 = static_cast<int64_t>(blockIdx.x) * a.nrb / gridDim.x;
-    const int64_t rb1 = static_cast<int64_t>(blockIdx.x + 1) * a.nrb / gridDim.x;
+    // this CTA's matrix and its share of that matrix's row blocks
+    int m = 0;
+#pragma unroll 1
+    for (int i = 1; i < a.nmat; ++i) if (static_cast<int>(blockIdx.x) >= a.cta0[i]) m = i;
+    const int cb = static_cast<int>(blockIdx.x) - a.cta0[m];
+    const int nb = a.cta0[m + 1] - a.cta0[m];
+    const int64_t Nm = a.Ngp[m];
+    uint16_t* const ym = a.ygp[m];
+    const int64_t rb0 = static_cast<int64_t>(cb) * a.nrbgp[m] / nb;
+    const int64_t rb1 = static_cast<int64_t>(cb + 1) * a.nrbgp[m] / nb;
     const int nrb = static_cast<int>(rb1 - rb0);
     const int nst = nrb * a.nkc;
 
@@ -119,8 +139,10 @@ q4_smalln_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_consta
     if (warp == kSnWarps) {
         // ------------------------------------------------ producer (one thread)
         if (lane == 0) {
-            tma_prefetch_desc(&mw);
-            tma_prefetch_desc(&ms);
+            const CUtensorMap* mw = &maps.w[m];
+            const CUtensorMap* ms = &maps.s[m];
+            tma_prefetch_desc(mw);
+            tma_prefetch_desc(ms);
             const uint64_t pol = policy_evict_first();
             int slot = 0, rb = 0, kc = 0;
             uint32_t phase = 0;
@@ -129,8 +151,8 @@ q4_smalln_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_consta
                 uint8_t* stage = ring + static_cast<size_t>(slot) * kSnStageBytes;
                 const int32_t r = static_cast<int32_t>((rb0 + rb) * kSnRows);
                 mbar_arrive_expect_tx(&full[slot], kSnStageBytes);
-                tma_load_3d(stage, &mw, &full[slot], 0, r, kc * (kSnChunkK / 256), pol);
-                tma_load_2d(stage + kSnCodeBytes, &ms, &full[slot], kc * kSnChunkG, r, pol);
+                tma_load_3d(stage, mw, &full[slot], 0, r, kc * (kSnChunkK / 256), pol);
+                tma_load_2d(stage + kSnCodeBytes, ms, &full[slot], kc * kSnChunkG, r, pol);
                 if (++slot == a.NS) { slot = 0; phase ^= 1; }
                 if (++rb == nrb) { rb = 0; ++kc; }
             }
@@ -240,11 +262,11 @@ q4_smalln_mma_kernel(const __grid_constant__ CUtensorMap mw, const __grid_consta
         const int rl = o / a.n;
         const int tok = o - rl * a.n;
         const int64_t row = rb0 * kSnRows + rl;
-        if (row >= a.N) continue;
+        if (row >= Nm) continue;
         float sum = 0.f;
 #pragma unroll
         for (int c = 0; c < kSnWarps; ++c) sum += part[(static_cast<size_t>(c) * a.rows_max + rl) * kSnTok + tok];
-        a.y[static_cast<int64_t>(tok) * a.N + row] = __half_as_ushort(__float2half_rn(sum * 16777216.0f));
+        ym[static_cast<int64_t>(tok) * Nm + row] = __half_as_ushort(__float2half_rn(sum * 16777216.0f));
     }
 }
 
@@ -256,19 +278,40 @@ static int sn_warps() {
 
 struct SnConfig {
     int grid, NS, rows_max;
-    int64_t nrb;
+    int cta0[kSnMaxGroup + 1];
     size_t smem;
     bool ok;
 };
 
-static SnConfig sn_config(int64_t K, int64_t N) {
+// CTAs per matrix in proportion to its 16-row blocks (at least one each),
+// grid <= the SM count.
+static SnConfig sn_config_group(int64_t K, int count, const int64_t* N) {
     SnConfig c{};
     c.ok = false;
-    if (K % 256 != 0 || K <= 0 || N <= 0 || N >= (int64_t{1} << 30)) return c;
-    c.nrb = (N + kSnRows - 1) / kSnRows;
+    if (K % 256 != 0 || K <= 0 || count < 1 || count > kSnMaxGroup) return c;
+    int64_t tot = 0, nrb[kSnMaxGroup];
+    for (int i = 0; i < count; ++i) {
+        if (N[i] <= 0 || N[i] >= (int64_t{1} << 30)) return c;
+        nrb[i] = (N[i] + kSnRows - 1) / kSnRows;
+        tot += nrb[i];
+    }
+    if (tot < count) return c;
     const int64_t gmax = static_cast<int64_t>(num_sms()) * (knob_int("RELAX_Q4_SN_GRID_MULT", 1) == 2 ? 2 : 1);
-    c.grid = static_cast<int>(c.nrb < gmax ? c.nrb : gmax);
-    const int64_t nrb_max = (c.nrb + c.grid - 1) / c.grid;
+    const int grid = static_cast<int>(tot < gmax ? tot : gmax);
+    c.cta0[0] = 0;
+    int64_t acc = 0, nrb_max = 0;
+    for (int i = 0; i < count; ++i) {
+        acc += nrb[i];
+        int e = static_cast<int>(acc * grid / tot);
+        if (e < c.cta0[i] + 1) e = c.cta0[i] + 1;
+        if (i == count - 1 && e < grid) e = grid;
+        c.cta0[i + 1] = e;
+        const int nb = e - c.cta0[i];
+        if (nb > nrb[i]) return c;                                   // a CTA without rows
+        const int64_t r = (nrb[i] + nb - 1) / nb;
+        if (r > nrb_max) nrb_max = r;
+    }
+    c.grid = c.cta0[count];
     c.rows_max = static_cast<int>(nrb_max * kSnRows);
     const size_t part_bytes = static_cast<size_t>(nrb_max) * kSnRows * sn_warps() * kSnTok * 4;
     const size_t fixed = 1024 + 256 + part_bytes;
@@ -281,27 +324,38 @@ static SnConfig sn_config(int64_t K, int64_t N) {
 }
 
 bool smalln_mma_ok(int64_t n, int64_t K, int64_t N) {
-    return n >= 1 && sn_config(K, N).ok;
+    return n >= 1 && sn_config_group(K, 1, &N).ok;
 }
 
-int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                      const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
-    const SnConfig c = sn_config(K, N);
-    if (!c.ok || n < 1) return static_cast<int>(cudaErrorInvalidConfiguration);
-    // codes: {32 words, N rows, K/256 chunks of 128 B}, box {32, 16, 8}; scales: {K/32, N}, box {64, 16}
-    CUtensorMap mw, ms;
-    {
-        const uint64_t dims[3] = {32, static_cast<uint64_t>(N), static_cast<uint64_t>(K / 256)};
-        const uint64_t strides[2] = {static_cast<uint64_t>(K / 2), 128};
-        const uint32_t box[3] = {32, kSnRows, kSnChunkK / 256};
-        int rc = make_tensor_map(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, w, dims, strides, box,
-                                 CU_TENSOR_MAP_SWIZZLE_128B);
-        if (rc) return rc;
-        const uint64_t sdims[2] = {static_cast<uint64_t>(K / kGroup), static_cast<uint64_t>(N)};
-        const uint64_t sstrides[1] = {static_cast<uint64_t>(K / kGroup) * 2};
-        const uint32_t sbox[2] = {kSnChunkG, kSnRows};
-        rc = make_tensor_map(&ms, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, s, sdims, sstrides, sbox,
+bool smalln_mma_grouped_ok(int64_t n, int64_t K, int count, const int64_t* N) {
+    return n >= 1 && sn_config_group(K, count, N).ok;
+}
+
+static int sn_maps(SnMaps* maps, int i, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s) {
+    const uint64_t dims[3] = {32, static_cast<uint64_t>(N), static_cast<uint64_t>(K / 256)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(K / 2), 128};
+    const uint32_t box[3] = {32, kSnRows, kSnChunkK / 256};
+    int rc = make_tensor_map(&maps->w[i], CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, w, dims, strides, box,
                              CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    const uint64_t sdims[2] = {static_cast<uint64_t>(K / kGroup), static_cast<uint64_t>(N)};
+    const uint64_t sstrides[1] = {static_cast<uint64_t>(K / kGroup) * 2};
+    const uint32_t sbox[2] = {kSnChunkG, kSnRows};
+    return make_tensor_map(&maps->s[i], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, s, sdims, sstrides, sbox,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// `count` matrices sharing x and K in one launch per 8 tokens (count = 1: the
+// plain call).
+int launch_smalln_mma_grouped(const uint16_t* x, int64_t n, int64_t K, int count, const int64_t* N,
+                              const uint32_t* const* w, const uint16_t* const* s, uint16_t* const* y, bool pdl,
+                              cudaStream_t stream) {
+    const SnConfig c = sn_config_group(K, count, N);
+    if (!c.ok || n < 1) return static_cast<int>(cudaErrorInvalidConfiguration);
+    SnMaps maps;
+    memset(&maps, 0, sizeof maps);
+    for (int i = 0; i < count; ++i) {
+        const int rc = sn_maps(&maps, i, K, N[i], w[i], s[i]);
         if (rc) return rc;
     }
     const int W = sn_warps();
@@ -309,20 +363,24 @@ int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
     const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), static_cast<int>(kSnSmemCap));
     if (e != cudaSuccess) return static_cast<int>(e);
     if (knob_int("RELAX_Q4_GS_PRINT", 0))
-        fprintf(stderr, "smalln_mma K=%lld N=%lld n=%lld NS=%d grid=%d smem=%zu\n", (long long)K, (long long)N,
-                (long long)n, c.NS, c.grid, c.smem);
+        fprintf(stderr, "smalln_mma K=%lld N0=%lld count=%d n=%lld NS=%d grid=%d smem=%zu\n", (long long)K,
+                (long long)N[0], count, (long long)n, c.NS, c.grid, c.smem);
     for (int64_t t0 = 0; t0 < n; t0 += kSnTok) {          // 8 tokens (the MMA's N) per launch
-        SnArgs a;
+        SnArgs a{};
         a.x = x + t0 * K;
-        a.y = y + t0 * N;
-        a.N = N;
         a.K = static_cast<int>(K);
         a.G = static_cast<int>(K / kGroup);
         a.n = static_cast<int>(n - t0 < kSnTok ? n - t0 : kSnTok);
         a.NS = c.NS;
         a.nkc = static_cast<int>((K + kSnChunkK - 1) / kSnChunkK);
-        a.nrb = c.nrb;
         a.rows_max = c.rows_max;
+        a.nmat = count;
+        for (int i = 0; i <= count; ++i) a.cta0[i] = c.cta0[i];
+        for (int i = 0; i < count; ++i) {
+            a.ygp[i] = y[i] + t0 * N[i];
+            a.Ngp[i] = N[i];
+            a.nrbgp[i] = (N[i] + kSnRows - 1) / kSnRows;
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(c.grid);
         cfg.blockDim = dim3((W + 1) * 32);
@@ -333,10 +391,15 @@ int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
         attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        const int rc = static_cast<int>(cudaLaunchKernelEx(&cfg, kern, mw, ms, a));
+        const int rc = static_cast<int>(cudaLaunchKernelEx(&cfg, kern, maps, a));
         if (rc) return rc;
     }
     return 0;
+}
+
+int launch_smalln_mma(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
+                      const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
+    return launch_smalln_mma_grouped(x, n, K, 1, &N, &w, &s, &y, pdl, stream);
 }
 
 // Largest n the automatic dispatch gives this kernel (measured

@@ -21,7 +21,7 @@ GROUPS = {
 
 
 @pytest.mark.parametrize("name", list(GROUPS))
-@pytest.mark.parametrize("n", [1, 2, 3, 17])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 17])
 def test_grouped_members_match_oracle(name, n):
     mats = GROUPS[name]
     K = mats[0][0]
@@ -37,6 +37,22 @@ def test_grouped_members_match_oracle(name, n):
         assert_within_tol(host_bits(y)[:, cols], r, f"grouped {name} member {i} n={n}")
 
 
+def test_grouped_smalln_equals_single_calls():
+    """3 <= n <= 8: one small-batch launch for the group; each member equals
+    the member's own relax_q4_matmul (the same kernel over the same rows,
+    another CTA split) bit for bit."""
+    K = 4096
+    for mats in (GROUPS["qkv7b"], GROUPS["gate_up7b"], GROUPS["qkv70b_gqa"][:1] + [(4096, 1024), (4096, 1024)]):
+        host = [inputs.realistic_weights(7400 + i, K, N) for i, (_, N) in enumerate(mats)]
+        devw = [dev_weights(p, s) for p, s in host]
+        for n in (3, 8):
+            x = dev_x(inputs.activations(7500 + n, n, K))
+            ys = ops.q4_matmul_grouped(x, devw)
+            for (pk, sc), y in zip(devw, ys):
+                single = ops.q4_matmul_ex(x, pk, sc, variant=ops.VARIANT_SMALLN)
+                assert np.array_equal(host_bits(y), host_bits(single))
+
+
 def test_grouped_pinned_cases_bitwise():
     """One-hot rows extract W and all-7 members give exact zeros, as for single calls."""
     K = 512
@@ -44,7 +60,7 @@ def test_grouped_pinned_cases_bitwise():
     host = [inputs.stress_weights(7200 + i, K, N) for i, (_, N) in enumerate(mats)]
     host[1] = (np.full_like(host[1][0], 0x77777777), host[1][1])
     devw = [dev_weights(p, s) for p, s in host]
-    for n, ks in ((1, [5]), (2, [0, 511])):
+    for n, ks in ((1, [5]), (2, [0, 511]), (4, [0, 7, 300, 511])):
         x = np.zeros((n, K), dtype=np.uint16)
         for i, k in enumerate(ks):
             x[i, k] = 0x3C00
