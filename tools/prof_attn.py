@@ -21,11 +21,18 @@ ws = torch.empty(ops.attn_decode_workspace(b, hq, L), dtype=torch.uint8, device=
 for _ in range(reps):
     ops.attn_decode(q, k, v, lens, out=out, ws=ws)
 torch.cuda.synchronize()
+# 20 calls captured in a CUDA graph (device time, no host dispatch in it)
+st = torch.cuda.Stream()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g, stream=st):
+    for _ in range(20):
+        ops.attn_decode(q, k, v, lens, out=out, ws=ws, stream=st)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for _ in range(20):
-    ops.attn_decode(q, k, v, lens, out=out, ws=ws)
-e1.record()
+with torch.cuda.stream(st):
+    g.replay()
+    e0.record(st)
+    g.replay()
+    e1.record(st)
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 1e3 / 20
 byts = 2 * b * hkv * L * 128 * 2
