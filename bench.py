@@ -333,7 +333,21 @@ def run_ours(args, rank, world, local_rank):
                 ops.q4_matmul_grouped(xs[mats[g[0]][1]], [weights[j] for j in g], ys=[ys[j] for j in g],
                                       stream=stream)
 
-    step = grouped_step if grouped else serial_step
+    # --chain: the whole layer set as ONE persistent launch (relax_q4_chain_run):
+    # the same linears and weights, every op after the first of its group waiting
+    # for all earlier ops (the layer's dependency chain)
+    chain = None
+    if args.chain:
+        if n != 1 or tp_mode or args.block != "none":
+            raise SystemExit("--chain runs the n = 1 layer set on one GPU")
+        first_of_group = {g[0] for g in groups} if not args.serial else set(range(len(mats)))
+        chain = ops.DecodeChain([(xs[K], *weights[j], ys[j], j in first_of_group)
+                                 for j, (name, K, N) in enumerate(mats)])
+
+    def chain_step():
+        chain.run(stream=stream)
+
+    step = chain_step if chain is not None else grouped_step if grouped else serial_step
     out_last = lambda: ys[-1]          # noqa: E731  the step's result (logits)
     tp_allreduce = None
     block_io = None
@@ -500,17 +514,22 @@ def run_ours(args, rank, world, local_rank):
              + (f"-megatron-tp{tp_world}" if tp_mode else "")
              + (f"-block-{args.block}" if args.block != "none" else "")
              + (f"-attn-kv{args.kv}" if args.kv > 0 else "")
-             + ("-grouped-qkv-gateup" if grouped else ""))
+             + ("-chain" if chain is not None else "-grouped-qkv-gateup" if grouped else ""))
     roof["traffic"] = traffic_per_launch(label, n)
-    roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
-    roof["kernel"] = ("q4_decode_stream_kernel (streamed decode GEMV)"
-                      if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" else "tc_q4_kernel")
-    roof["per"] = "average over all launches of the step (every launch is this kernel family)"
+    if chain is not None:
+        roof["algorithmic_bytes_per_launch"] = int(bytes_step)
+        roof["kernel"] = "q4_decode_chain_kernel (the whole layer set in one persistent launch)"
+        roof["per"] = "one launch per step"
+    else:
+        roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
+        roof["kernel"] = ("q4_decode_stream_kernel (streamed decode GEMV)"
+                          if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" else "tc_q4_kernel")
+        roof["per"] = "average over all launches of the step (every launch is this kernel family)"
     if tp_mode:
         roof["per"] += "; per GPU: each rank streams its own shards"
     per_kind = {"tc": lambda: 1, "smalln": lambda: -(-n // 8), "gemv": lambda: -(-n // 2)}
     launches = 0
-    for g in (groups if grouped else [[j] for j in range(len(mats))]):
+    for g in ([] if chain is not None else groups if grouped else [[j] for j in range(len(mats))]):
         kinds = [sched[f"{mats[j][1]}x{mats[j][2]}"]["variant"] for j in g]
         if len(g) > 1 and n <= 2:
             launches += -(-n // 2)                     # one grouped decode launch per token pair
@@ -518,6 +537,8 @@ def run_ours(args, rank, world, local_rank):
             launches += 1                              # one grouped small-batch launch
         else:
             launches += sum(per_kind[k]() for k in kinds)
+    if chain is not None:
+        launches = 1
     if args.kv > 0:
         launches += 3 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))   # append, partial, combine
     res = {
@@ -679,6 +700,8 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="tensor parallelism over the ranks even at N = 1 (one NCCL rank: exercises the "
                          "collectives of the TP step on one GPU); the default for N > 1")
+    ap.add_argument("--chain", action="store_true",
+                    help="n = 1: the whole layer set as one persistent launch (relax_q4_chain_run)")
     ap.add_argument("--nccl-allreduce", action="store_true",
                     help="TP decode: sum the row-parallel partials with an NCCL all_reduce instead of the fused "
                          "kernel epilogue (relax_q4_matmul_allreduce)")

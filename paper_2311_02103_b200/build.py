@@ -31,9 +31,9 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "librelax_q4.so")
 
 SOURCES = ["abi.cpp", "device.cpp", "gemv.cu", "gemv_stream.cu", "smalln_mma.cu", "gemm_tc.cu", "gemm_tc_persist.cu", "fused.cu", "repack.cu", "attention.cu"]
-HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh", "fusion.cuh", "knobs.h"]
+HEADERS = ["internal.h", "ptx.cuh", "q4_unpack.cuh", "fusion.cuh", "knobs.h", "decode_math.cuh"]
 EXP_DIR = os.path.join(ROOT, "experiments", "csrc")
-EXP_SOURCES = ["gemv_mma.cu", "gemv_row.cu"]
+EXP_SOURCES = ["gemv_mma.cu", "gemv_row.cu", "decode_chain.cu"]
 BUILD_EXP = os.path.join(ROOT, "build_exp")
 LIB_EXP = os.path.join(BUILD_EXP, "librelax_q4_exp.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -3,7 +3,11 @@
 // P:432-433), the upper-bound workspace plan, and the
 // launches.  No exceptions cross this boundary; nothing here allocates.
 #include <cmath>
+#include <vector>
 #include "relax_q4.h"
+#ifdef RQ4_EXPERIMENTS
+#include "relax_q4_debug.h"
+#endif
 
 #include <cstdlib>
 #include <cstring>
@@ -558,6 +562,61 @@ int relax_q4_matmul_grouped(const void* x, int64_t n, int64_t K, int count, cons
     }
     return RELAX_OK;
 }
+
+#ifdef RQ4_EXPERIMENTS
+// the persistent decode chain (experiments build; include/relax_q4_debug.h)
+int relax_q4_chain_workspace(int count, size_t* ws_bytes) {
+    if (!ws_bytes || count < 1 || count > rq4::chain_max_ops()) return RELAX_ERR_INVALID_ARG;
+    *ws_bytes = rq4::chain_workspace_bytes(count);
+    return RELAX_OK;
+}
+
+int relax_q4_chain_init(const relax_q4_chain_op* ops, int count, void* ws, size_t ws_bytes) {
+    if (!ops || count < 1 || count > rq4::chain_max_ops() || !ws) return RELAX_ERR_INVALID_ARG;
+    std::vector<rq4::ChainOpHost> h(static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+        const relax_q4_chain_op& o = ops[i];
+        if (!o.x || !o.packed_w || !o.scales || !o.y || o.K <= 0 || o.N <= 0 || o.reserved != 0)
+            return RELAX_ERR_INVALID_ARG;
+        if (!rq4::chain_op_ok(o.K, o.N)) return RELAX_ERR_UNSUPPORTED_SHAPE;
+        if (!rq4::aligned16(o.x) || !rq4::aligned16(o.packed_w) || !rq4::aligned16(o.scales) || !rq4::aligned16(o.y))
+            return RELAX_ERR_MISALIGNED;
+        const size_t xb = static_cast<size_t>(o.K) * 2, yb = static_cast<size_t>(o.N) * 2;
+        const size_t wb = static_cast<size_t>(o.N) * o.K / 2, sb = static_cast<size_t>(o.N) * (o.K / rq4::kGroup) * 2;
+        if (rq4::overlap(o.y, yb, o.x, xb) || rq4::overlap(o.y, yb, o.packed_w, wb) ||
+            rq4::overlap(o.y, yb, o.scales, sb) || rq4::overlap(o.y, yb, ws, ws_bytes))
+            return RELAX_ERR_ALIAS;
+        h[i].x = static_cast<const uint16_t*>(o.x);
+        h[i].w = o.packed_w;
+        h[i].s = static_cast<const uint16_t*>(o.scales);
+        h[i].y = static_cast<uint16_t*>(o.y);
+        h[i].K = o.K;
+        h[i].N = o.N;
+        h[i].after = o.after;
+    }
+    if (!rq4::aligned16(ws)) return RELAX_ERR_MISALIGNED;
+    if (ws_bytes < rq4::chain_workspace_bytes(count)) return RELAX_ERR_WORKSPACE;
+    const int rc = rq4::check_device();
+    if (rc != RELAX_OK) return rc;
+    if (rq4::chain_init(h.data(), count, ws) != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
+int relax_q4_chain_run(void* ws, void* stream) {
+    if (!ws) return RELAX_ERR_INVALID_ARG;
+    const int rc = rq4::check_device();
+    if (rc != RELAX_OK) return rc;
+    if (rq4::launch_chain(ws, true, static_cast<cudaStream_t>(stream)) != 0) {
+        cudaGetLastError();
+        return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+
+#endif
 
 int relax_tp_comm_bytes(int32_t world, int64_t N_max, size_t* bytes) {
     if (!bytes || world < 1 || world > RELAX_TP_MAX_WORLD || N_max <= 0) return RELAX_ERR_INVALID_ARG;

@@ -122,6 +122,22 @@ bool smalln_mma_grouped_ok(int64_t n, int64_t K, int count, const int64_t* N);
 int launch_smalln_mma_grouped(const uint16_t* x, int64_t n, int64_t K, int count, const int64_t* N,
                               const uint32_t* const* w, const uint16_t* const* s, uint16_t* const* y, bool pdl,
                               cudaStream_t stream);
+#ifdef RQ4_EXPERIMENTS
+// A chain of n = 1 GEMVs in one persistent launch (experiments/csrc/decode_chain.cu).
+struct ChainOpHost {
+    const uint16_t* x;
+    const uint32_t* w;
+    const uint16_t* s;
+    uint16_t* y;
+    int64_t K, N;
+    int after;          // wait for every earlier op before reading x
+};
+bool chain_op_ok(int64_t K, int64_t N);
+int chain_max_ops();
+size_t chain_workspace_bytes(int count);
+int chain_init(const ChainOpHost* ops, int count, void* ws);     // synchronous (writes the op table)
+int launch_chain(void* ws, bool pdl, cudaStream_t stream);
+#endif
 // Decode attention over a symbolic KV length and the KV append (attention.cu).
 size_t attn_workspace_bytes(int64_t batch, int64_t Hq, int64_t Lmax);
 int launch_attention_decode(const uint16_t* q, const uint16_t* k, const uint16_t* v, const int32_t* lens,

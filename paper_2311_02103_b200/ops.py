@@ -43,6 +43,8 @@ EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "rel
            "relax_plan_workspace_fused", "relax_q4_matmul_fused", "relax_q4_repack",
            "relax_attn_decode_workspace", "relax_attn_decode", "relax_kv_append", "relax_q4_matmul_grouped",
            "relax_tp_comm_bytes", "relax_q4_matmul_allreduce")
+# the persistent decode chain: experiments build only (include/relax_q4_debug.h)
+CHAIN_EXPORTS = ("relax_q4_chain_workspace", "relax_q4_chain_init", "relax_q4_chain_run")
 
 # fused neighbours (include/relax_q4.h RELAX_OP_*)
 OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL = 1, 2, 4
@@ -61,6 +63,13 @@ class TpComm(ctypes.Structure):
     """struct relax_tp_comm: bufs[p] = rank p's exchange buffer mapped on this device."""
     _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("bufs", ctypes.c_void_p * TP_MAX_WORLD), ("buf_bytes", ctypes.c_size_t)]
+
+
+class ChainOp(ctypes.Structure):
+    """struct relax_q4_chain_op."""
+    _fields_ = [("x", ctypes.c_void_p), ("packed_w", ctypes.c_void_p), ("scales", ctypes.c_void_p),
+                ("y", ctypes.c_void_p), ("K", ctypes.c_int64), ("N", ctypes.c_int64), ("after", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class RelaxError(RuntimeError):
@@ -118,6 +127,13 @@ def lib() -> ctypes.CDLL:
         L.relax_attn_decode.restype = I
         L.relax_kv_append.argtypes = [P, P, P, I64, I64, I64, I64, P, P, P]
         L.relax_kv_append.restype = I
+        if hasattr(L, "relax_q4_chain_run"):
+            L.relax_q4_chain_workspace.argtypes = [I, ctypes.POINTER(SZ)]
+            L.relax_q4_chain_workspace.restype = I
+            L.relax_q4_chain_init.argtypes = [ctypes.POINTER(ChainOp), I, P, SZ]
+            L.relax_q4_chain_init.restype = I
+            L.relax_q4_chain_run.argtypes = [P, P]
+            L.relax_q4_chain_run.restype = I
         L.relax_tp_comm_bytes.argtypes = [ctypes.c_int32, I64, ctypes.POINTER(SZ)]
         L.relax_tp_comm_bytes.restype = I
         L.relax_q4_matmul_allreduce.argtypes = [ctypes.POINTER(TpComm), P, I64, I64, I64, P, P, P, P, P]
@@ -258,6 +274,45 @@ def q4_matmul_grouped(x, weights, ys=None, stream=None):
     rc = lib().relax_q4_matmul_grouped(_ptr(x), x.shape[0], x.shape[1], cnt, Ns, Ws, Ss, Ys, _stream_ptr(stream))
     _check(rc, "relax_q4_matmul_grouped")
     return outs
+
+
+def has_chain() -> bool:
+    """Whether the loaded library is the experiments build with the decode chain."""
+    return hasattr(lib(), "relax_q4_chain_run")
+
+
+class DecodeChain:
+    """relax_q4_chain_* (experiments build only; RELAX_Q4_LIB=build_exp/...): a
+    fixed sequence of n = 1 matmuls run as ONE persistent launch.  ops: list of (x, packed_w, scales, y, after) with x fp16 [1, K] (or
+    [K]), y fp16 [1, N]; `after` = the op reads what an earlier op wrote (it
+    waits for every earlier op).  The tensors must stay alive and in place: the
+    chain keeps their pointers."""
+
+    def __init__(self, ops, device=None):
+        import torch
+        if not has_chain():
+            raise RelaxError(1, "relax_q4_chain_init (not in this library: build --experiments and set RELAX_Q4_LIB)")
+        dev = _device_of_call()
+        arr = (ChainOp * len(ops))()
+        self._keep = []
+        for i, (x, pw, sc, y, after) in enumerate(ops):
+            N, K = pw.shape[0], pw.shape[1] * 8
+            _check_tensor(x, f"ops[{i}].x", torch.float16, dev=dev)
+            _check_tensor(pw, f"ops[{i}].packed_w", (torch.int32, torch.uint32), dev=dev)
+            _check_tensor(sc, f"ops[{i}].scales", torch.float16, (N, K // 32), dev=dev)
+            _check_tensor(y, f"ops[{i}].y", torch.float16, dev=dev)
+            if x.numel() != K or y.numel() != N:
+                raise ValueError(f"ops[{i}]: x has {x.numel()} elements (K = {K}), y {y.numel()} (N = {N})")
+            arr[i] = ChainOp(_ptr(x), _ptr(pw), _ptr(sc), _ptr(y), K, N, 1 if after else 0, 0)
+            self._keep.append((x, pw, sc, y))
+        nb = ctypes.c_size_t(0)
+        _check(lib().relax_q4_chain_workspace(len(ops), ctypes.byref(nb)), "relax_q4_chain_workspace")
+        self.ws = torch.empty(int(nb.value), dtype=torch.uint8, device=dev)
+        _check(lib().relax_q4_chain_init(arr, len(ops), _ptr(self.ws), int(nb.value)), "relax_q4_chain_init")
+        self.count = len(ops)
+
+    def run(self, stream=None):
+        _check(lib().relax_q4_chain_run(_ptr(self.ws), _stream_ptr(stream)), "relax_q4_chain_run")
 
 
 def tp_comm_bytes(world: int, N_max: int) -> int:

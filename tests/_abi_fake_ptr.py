@@ -167,6 +167,37 @@ def allreduce_validation(L):
     assert ar(comm(world=1, bufs=[B])) == 6
 
 
+def chain_validation(L):
+    """relax_q4_chain_* (the persistent decode chain)."""
+    nb = ctypes.c_size_t(0)
+    assert L.relax_q4_chain_workspace(0, ctypes.byref(nb)) == 1
+    assert L.relax_q4_chain_workspace(3, None) == 1
+    assert L.relax_q4_chain_workspace(3, ctypes.byref(nb)) == 0 and nb.value > 0
+    W = A + 256 * MB
+
+    def op(x=A, w=A + 8 * MB, s=A + 16 * MB, y=A + 24 * MB, K=4096, N=4096, after=0, reserved=0):
+        return ops.ChainOp(x, w, s, y, K, N, after, reserved)
+
+    def init(oplist, ws=W, wsb=None):
+        arr = (ops.ChainOp * len(oplist))(*oplist)
+        return L.relax_q4_chain_init(arr, len(oplist), ws, nb.value if wsb is None else wsb)
+    L.relax_q4_chain_workspace(2, ctypes.byref(nb))
+    assert L.relax_q4_chain_init(None, 2, W, nb.value) == 1
+    assert init([op(), op(x=0)]) == 1
+    assert init([op(), op(reserved=1)]) == 1
+    assert init([op(), op(K=0)]) == 1
+    assert init([op(), op(K=4128)]) == 2                 # K % 256 != 0
+    assert init([op(), op(K=32768)]) == 2                # more than 30 K-column warps
+    assert init([op(), op(x=A + 2)]) == 3
+    assert init([op(), op(y=A + 8 * MB)]) == 4           # y over the weights
+    assert init([op(), op(y=A)]) == 4                    # y over its own x
+    assert init([op(), op()], wsb=16) == 5
+    assert init([op(), op()], ws=0) == 1
+    assert init([op(), op(x=A + 24 * MB, y=A + 32 * MB, after=1)]) == 6   # x = the previous y: valid
+    assert L.relax_q4_chain_run(None, None) == 1
+    assert L.relax_q4_chain_run(W, None) == 6
+
+
 def main():
     assert os.environ.get("CUDA_VISIBLE_DEVICES", None) == "", "run with CUDA_VISIBLE_DEVICES=''"
     L = ops.lib()
@@ -174,6 +205,9 @@ def main():
               repack_validation, allreduce_validation):
         f(L)
         print("ok", f.__name__)
+    if hasattr(L, "relax_q4_chain_run"):            # the experiments build (RELAX_Q4_LIB)
+        chain_validation(L)
+        print("ok chain_validation")
     print("ALL OK")
 
 
