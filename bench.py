@@ -509,24 +509,6 @@ def run_ours(args, rank, world, local_rank):
     else:
         roof = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(gbs / peaks["hbm_gbs"], 4), "peak_src": f"{peaks['src']} hbm copy"}
-    label = (args.workload + ("-fused-qkv-gateup" if fused else "")
-             + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else "")
-             + (f"-megatron-tp{tp_world}" if tp_mode else "")
-             + (f"-block-{args.block}" if args.block != "none" else "")
-             + (f"-attn-kv{args.kv}" if args.kv > 0 else "")
-             + ("-chain" if chain is not None else "-grouped-qkv-gateup" if grouped else ""))
-    roof["traffic"] = traffic_per_launch(label, n)
-    if chain is not None:
-        roof["algorithmic_bytes_per_launch"] = int(bytes_step)
-        roof["kernel"] = "q4_decode_chain_kernel (the whole layer set in one persistent launch)"
-        roof["per"] = "one launch per step"
-    else:
-        roof["algorithmic_bytes_per_launch"] = int(bytes_step / len(mats))
-        roof["kernel"] = ("q4_decode_stream_kernel (streamed decode GEMV)"
-                          if sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"] == "gemv" else "tc_q4_kernel")
-        roof["per"] = "average over all launches of the step (every launch is this kernel family)"
-    if tp_mode:
-        roof["per"] += "; per GPU: each rank streams its own shards"
     per_kind = {"tc": lambda: 1, "smalln": lambda: -(-n // 8), "gemv": lambda: -(-n // 2)}
     launches = 0
     for g in ([] if chain is not None else groups if grouped else [[j] for j in range(len(mats))]):
@@ -541,6 +523,27 @@ def run_ours(args, rank, world, local_rank):
         launches = 1
     if args.kv > 0:
         launches += 3 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))   # append, partial, combine
+    label = (args.workload + ("-fused-qkv-gateup" if fused else "")
+             + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else "")
+             + (f"-megatron-tp{tp_world}" if tp_mode else "")
+             + (f"-block-{args.block}" if args.block != "none" else "")
+             + (f"-attn-kv{args.kv}" if args.kv > 0 else "")
+             + ("-chain" if chain is not None else "-grouped-qkv-gateup" if grouped else ""))
+    roof["traffic"] = traffic_per_launch(label, n)
+    if chain is not None:
+        roof["algorithmic_bytes_per_launch"] = int(bytes_step)
+        roof["kernel"] = "q4_decode_chain_kernel (the whole layer set in one persistent launch)"
+        roof["per"] = "one launch per step"
+    else:
+        # per launch of the linears (a grouped q/k/v or gate/up launch counts once)
+        lin_launches = launches - (3 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv")) if args.kv > 0 else 0)
+        roof["algorithmic_bytes_per_launch"] = int(bytes_step / max(lin_launches, 1))
+        kind0 = sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"]
+        roof["kernel"] = {"gemv": "q4_decode_stream_kernel (streamed decode GEMV)",
+                          "smalln": "q4_smalln_mma_kernel (small-batch warp-MMA)"}.get(kind0, "tc_q4_kernel")
+        roof["per"] = "average over all launches of the step (every launch is this kernel family)"
+    if tp_mode:
+        roof["per"] += "; per GPU: each rank streams its own shards"
     res = {
         "metric": METRIC,
         "value": round(tok_s, 2),

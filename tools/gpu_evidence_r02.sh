@@ -28,15 +28,22 @@ b 7b_prefill_n128 --workload llama2-7b-prefill --n 128 --no-cpu-baseline
 b 7b_prefill_n512 --workload llama2-7b-prefill --n 512 --no-cpu-baseline
 b 7b_prefill_n4096 --workload llama2-7b-prefill --n 4096 --steps 5 --no-cpu-baseline
 b 13b_prefill_n512 --workload llama2-13b-prefill --n 512 --no-cpu-baseline
+b 7b_decode_serial --serial --no-cpu-baseline
 b 70b_megatron_tp1 --workload llama2-70b-decode --tp --no-cpu-baseline
+b 70b_megatron_tp1_nccl --workload llama2-70b-decode --tp --nccl-allreduce --no-cpu-baseline
+b 7b_megatron_tp1 --tp --no-cpu-baseline
+b 7b_megatron_tp1_nccl --tp --nccl-allreduce --no-cpu-baseline
+for p in 2 4 8; do b 70b_fused_shard$p --workload llama2-70b-decode --fused --tp-shard $p --no-cpu-baseline; done
 timeout 600 python bench.py --impl reference > $O/reference.json 2> $O/reference.err; echo "reference rc=$? $(cut -c1-200 $O/reference.json)"
 if [ "${NCU:-1}" = "1" ]; then
-  for spec in "7b:" "7bfused:--fused" "7bn8:--n 8"; do
-    tag=${spec%%:*}; fl=${spec#*:}
+  for spec in "7b:llama2-7b-decode-grouped-qkv-gateup:n1:" "7bfused:llama2-7b-decode-fused-qkv-gateup:n1:--fused" \
+              "7bn8:llama2-7b-decode-grouped-qkv-gateup:n8:--n 8" "7bserial:llama2-7b-decode:n1:--serial"; do
+    tag=${spec%%:*}; rest=${spec#*:}; key=${rest%:*}; fl=${rest##*:}
     timeout 600 python bench.py $fl --steps 2 --warmup 3 --no-cpu-baseline > $O/ll_plain_$tag.log 2>&1 && \
-    timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 800 -c 300 --csv \
+    timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -s 400 -c 300 --csv \
         --log-file $O/launches_$tag.csv python bench.py $fl --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_ll_$tag.log 2>&1
     echo "launch list $tag rc=$?"
+    python tools/launch_summary.py $O/launches_$tag.csv $O/launches_${tag}_summary.csv "$key" > $O/launches_${tag}_shares.txt 2>&1
   done
   p() { tag=$1; kre=$2; shift 2; timeout 120 python tools/prof_one.py "$@" 5 > /dev/null 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:$kre -s 2 -c 1 -o $O/prof_$tag python tools/prof_one.py "$@" 5 > $O/ncu_$tag.log 2>&1; echo "ncu $tag rc=$?"; }
   p decode_4096x11008_n1 decode_stream 4096 11008 1 auto
@@ -44,4 +51,5 @@ if [ "${NCU:-1}" = "1" ]; then
   p smalln_4096x11008_n8 smalln 4096 11008 8 auto
   p tc_4096x11008_n512 tc_q4 4096 11008 512 auto
   p persist_4096x32000_n4096 persist 4096 32000 4096 auto
+  timeout 60 python tools/prof_attn.py 1 32 32 4096 3 > /dev/null 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_partial -s 2 -c 1 -o $O/prof_attn_b1_h32_L4096 python tools/prof_attn.py 1 32 32 4096 3 > $O/ncu_attn.log 2>&1; echo "ncu attn rc=$?"
 fi
