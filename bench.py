@@ -751,8 +751,18 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         if world == 1 and "MASTER_ADDR" not in os.environ:
-            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()), RANK="0", WORLD_SIZE="1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            # a single self-launched rank picks its own port; a port taken
+            # between the probe and the bind (EADDRINUSE) is retried with another
+            for attempt in range(5):
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()), RANK="0", WORLD_SIZE="1")
+                try:
+                    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+                    break
+                except dist.DistNetworkError:
+                    if attempt == 4:
+                        raise
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
