@@ -308,6 +308,14 @@ RELAX_API int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int
  *                    k..k+7 of output column j, low nibble first -- the
  *                    per-column packing of GPTQ-style checkpoints),
  *                    src_scales fp16 [K/G][N]
+ *   RELAX_LAYOUT_NK3 3-bit codes ("3-bit" Llama-2-7B on the iPhone;
+ *                    DESIGN.md reading 20): src_packed uint32 [N][3 K/32],
+ *                    the 32 codes of group g of column j at bits 3 i .. 3 i + 2
+ *                    of words 3 g .. 3 g + 2 (96 bits, little-endian), zero
+ *                    point 3: W(k, j) = fp16_RNE((q3 - 3) * s(k/G, j)); stored
+ *                    natively as q4 = q3 + 4 (bit-exact, 4.5 instead of 3.5
+ *                    bits per weight in HBM);
+ *                    src_scales fp16 [N][K/G]
  *   group G in {32, 64, 128}; W(k, j) = fp16_RNE((q - 7) * s(k/G, j)).
  * Outputs: packed_w uint32 [N][K/8], scales fp16 [N][K/32] (device, caller-
  * owned, must not overlap the inputs).  Asynchronous on `stream`.
@@ -317,6 +325,7 @@ RELAX_API int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int
  * N == 0 is a no-op. */
 #define RELAX_LAYOUT_NK 0
 #define RELAX_LAYOUT_KN 1
+#define RELAX_LAYOUT_NK3 2
 RELAX_API int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t K, int64_t N,
                               int layout, int group, uint32_t* packed_w, void* scales, void* stream);
 

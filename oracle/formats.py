@@ -19,7 +19,7 @@ its dequantized weight, written out plainly:
   W(k, j) = fp16_RNE((q(k, j) - 7) * s(k/G, j)),  G in {32, 64, 128}
 
 and the native format is G = 32, layout "nk".  3-bit weights (the
-iPhone runs Llama-2-7B "in 3-bit"; reading 24):
+iPhone runs Llama-2-7B "in 3-bit"; reading 20):
 
   layout "nk3":           packed[j][3 g .. 3 g + 2] holds the 32 codes of
                           group g of column j, code i at bits 3 i .. 3 i + 2

@@ -708,7 +708,8 @@ int relax_q4_dequant(const uint32_t* packed_w, const void* scales, int64_t K, in
 int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t K, int64_t N, int layout,
                     int group, uint32_t* packed_w, void* scales, void* stream) {
     if (K <= 0 || N < 0) return RELAX_ERR_INVALID_ARG;
-    if (layout != RELAX_LAYOUT_NK && layout != RELAX_LAYOUT_KN) return RELAX_ERR_INVALID_ARG;
+    if (layout != RELAX_LAYOUT_NK && layout != RELAX_LAYOUT_KN && layout != RELAX_LAYOUT_NK3)
+        return RELAX_ERR_INVALID_ARG;
     if (group != 32 && group != 64 && group != 128) return RELAX_ERR_UNSUPPORTED_SHAPE;
     if (K % group != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
     if (N == 0) return RELAX_OK;
@@ -717,10 +718,11 @@ int relax_q4_repack(const uint32_t* src_packed, const void* src_scales, int64_t 
         !rq4::aligned16(scales))
         return RELAX_ERR_MISALIGNED;
     const size_t wb = static_cast<size_t>(N) * K / 2;
+    const size_t wb_in = layout == RELAX_LAYOUT_NK3 ? static_cast<size_t>(N) * (K / rq4::kGroup) * 12 : wb;
     const size_t sb_out = static_cast<size_t>(N) * (K / rq4::kGroup) * 2;
     const size_t sb_in = static_cast<size_t>(N) * (K / group) * 2;
-    if (rq4::overlap(packed_w, wb, src_packed, wb) || rq4::overlap(packed_w, wb, src_scales, sb_in) ||
-        rq4::overlap(scales, sb_out, src_packed, wb) || rq4::overlap(scales, sb_out, src_scales, sb_in) ||
+    if (rq4::overlap(packed_w, wb, src_packed, wb_in) || rq4::overlap(packed_w, wb, src_scales, sb_in) ||
+        rq4::overlap(scales, sb_out, src_packed, wb_in) || rq4::overlap(scales, sb_out, src_scales, sb_in) ||
         rq4::overlap(packed_w, wb, scales, sb_out))
         return RELAX_ERR_ALIAS;
     const int rc = rq4::check_device();

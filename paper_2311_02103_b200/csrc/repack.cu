@@ -4,6 +4,7 @@
 //
 // Source formats (include/relax_q4.h RELAX_LAYOUT_*, readings 19-20):
 //   NK: packed [N][K/8], scales [N][K/G]      KN: packed [K/8][N], scales [K/G][N]
+//   NK3 (3-bit, zero point 3): packed [N][3 K/32] (32 codes per 96 bits), scales [N][K/G]
 // with G in {32, 64, 128}; a word always holds the codes of 8 consecutive k of
 // one output column, low nibble first.  Native: NK with G = 32.  The codes
 // move unchanged and every 32-group takes the scale of the G-group holding
@@ -53,6 +54,34 @@ __global__ void __launch_bounds__(256) expand_rows_kernel(const uint16_t* __rest
     }
 }
 
+// 3-bit source (RELAX_LAYOUT_NK3): per (row, 32-group) three words hold the
+// codes at bits 3 i .. 3 i + 2 of their 96 bits; the native word w (codes
+// 8 w .. 8 w + 7) gets q4 = q3 + 4 (q4 - 7 == q3 - 3: the same W).
+__global__ void __launch_bounds__(256) repack_q3_kernel(const uint32_t* __restrict__ in, int64_t groups,
+                                                        uint32_t* __restrict__ out) {
+    for (int64_t gi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; gi < groups;
+         gi += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t lo = static_cast<uint64_t>(in[3 * gi]) | (static_cast<uint64_t>(in[3 * gi + 1]) << 32);
+        const uint32_t hi = in[3 * gi + 2];
+        uint32_t o[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int bit = 3 * (8 * w + i);
+                uint32_t q;
+                if (bit + 3 <= 64) q = static_cast<uint32_t>(lo >> bit) & 7u;
+                else if (bit >= 64) q = (hi >> (bit - 64)) & 7u;
+                else q = (static_cast<uint32_t>(lo >> bit) | (hi << (64 - bit))) & 7u;   // straddles words 1 and 2
+                v |= (q + 4u) << (4 * i);
+            }
+            o[w] = v;
+        }
+        reinterpret_cast<uint4*>(out)[gi] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 template <typename T>
 static int launch_transpose(const T* in, int64_t R, int64_t C, int rep, T* out, cudaStream_t st) {
     const dim3 grid(static_cast<unsigned>((C + kTile - 1) / kTile), static_cast<unsigned>((R + kTile - 1) / kTile));
@@ -64,6 +93,20 @@ int launch_repack(const uint32_t* src_w, const uint16_t* src_s, int64_t K, int64
                   uint32_t* w, uint16_t* s, cudaStream_t st) {
     const int rep = group / kGroup;
     int e;
+    if (layout == 2) {                                   // 3-bit NK
+        const int64_t groups = N * (K / kGroup);
+        int64_t blocks = (groups + 255) / 256;
+        const int64_t bmax = 8 * static_cast<int64_t>(num_sms());
+        if (blocks > bmax) blocks = bmax;
+        repack_q3_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(src_w, groups, w);
+        e = static_cast<int>(cudaGetLastError());
+        if (e) return e;
+        const int64_t total = N * (K / kGroup);
+        int64_t sblocks = (total + 255) / 256;
+        if (sblocks > bmax) sblocks = bmax;
+        expand_rows_kernel<<<static_cast<unsigned>(sblocks), 256, 0, st>>>(src_s, N, K / group, rep, s);
+        return static_cast<int>(cudaGetLastError());
+    }
     if (layout == 0) {
         e = static_cast<int>(cudaMemcpyAsync(w, src_w, static_cast<size_t>(N) * (K / 8) * 4, cudaMemcpyDeviceToDevice, st));
         if (e) return e;

@@ -453,21 +453,21 @@ def kv_append(k_new, v_new, pos, k_cache, v_cache, stream=None):
     _check(rc, "relax_kv_append")
 
 
-LAYOUT_NK, LAYOUT_KN = 0, 1
+LAYOUT_NK, LAYOUT_KN, LAYOUT_NK3 = 0, 1, 2
 
 
 def q4_repack(src_packed, src_scales, K: int, N: int, layout: str = "kn", group: int = 32,
               packed_w=None, scales=None, stream=None):
-    """relax_q4_repack: convert a weight stored as `layout` ("nk" / "kn") with
+    """relax_q4_repack: convert a weight stored as `layout` ("nk" / "kn" / "nk3" = 3-bit) with
     group size `group` into the native packed_w [N, K/8] (int32) and scales
     [N, K/32] (fp16); bit-exact (include/relax_q4.h)."""
     import torch
-    lay = {"nk": LAYOUT_NK, "kn": LAYOUT_KN}[layout]
+    lay = {"nk": LAYOUT_NK, "kn": LAYOUT_KN, "nk3": LAYOUT_NK3}[layout]
     dev = _device_of_call()
     if K % group != 0 or group not in (32, 64, 128):
         raise ValueError(f"group {group} must be 32, 64 or 128 and divide K = {K}")
-    want_p = (N, K // 8) if lay == LAYOUT_NK else (K // 8, N)
-    want_s = (N, K // group) if lay == LAYOUT_NK else (K // group, N)
+    want_p = {LAYOUT_NK: (N, K // 8), LAYOUT_KN: (K // 8, N), LAYOUT_NK3: (N, K // 32 * 3)}[lay]
+    want_s = (K // group, N) if lay == LAYOUT_KN else (N, K // group)
     _check_tensor(src_packed, "src_packed", (torch.int32, torch.uint32), want_p, dev=dev)
     _check_tensor(src_scales, "src_scales", torch.float16, want_s, dev=dev)
     if packed_w is None:

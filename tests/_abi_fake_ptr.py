@@ -111,7 +111,8 @@ def fused_plan_soundness(L):
 
 def repack_validation(L):
     P = A + 64 * MB
-    assert L.relax_q4_repack(A, A + MB, 256, 64, 2, 32, P, P + MB, None) == 1      # unknown layout
+    assert L.relax_q4_repack(A, A + MB, 256, 64, 3, 32, P, P + MB, None) == 1      # unknown layout
+    assert L.relax_q4_repack(A, A + MB, 256, 64, 2, 32, P, P + MB, None) == 6      # 3-bit NK: valid
     assert L.relax_q4_repack(A, A + MB, 256, 64, 1, 48, P, P + MB, None) == 2      # group not 32/64/128
     assert L.relax_q4_repack(A, A + MB, 320, 64, 1, 128, P, P + MB, None) == 2     # K % G != 0
     assert L.relax_q4_repack(A, A + MB, 256, 64, 1, 64, 0, P + MB, None) == 1

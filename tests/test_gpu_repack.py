@@ -44,3 +44,27 @@ def test_repack_bit_exact_and_matmul(layout, group, K, N):
         cols = np.arange(0, N, max(1, N // 40))
         r = oracle.matmul_cols_f64(x, want_p, want_s, K, cols)
         assert_within_tol(y[:, cols], r, f"repacked {layout} G={group} {K}x{N} n={n}")
+
+
+@pytest.mark.parametrize("group", [32, 128])
+@pytest.mark.parametrize("K,N", [(256, 24), (4096, 1000), (11008, 300)])
+def test_repack_q3_bit_exact_and_matmul(group, K, N):
+    """3-bit source (layout "nk3", reading 20): random words (every 96-bit
+    pattern is a valid code triple) -> native words equal the oracle's
+    to_native bit for bit, and the matmul on them matches the oracle of the
+    3-bit weight."""
+    rng = np.random.default_rng(K + N + group)
+    src_p = rng.integers(0, 2 ** 32, size=(N, K // 32 * 3), dtype=np.uint64).astype(np.uint32)
+    src_s = rng.uniform(2.0 ** -10, 2.0 ** -5, size=(N, K // group)).astype(np.float16).view(np.uint16)
+    want_p, want_s = fm.to_native(src_p, src_s, K, N, "nk3", group)
+    pw, sc = ops.q4_repack(torch.from_numpy(src_p.view(np.int32)).cuda(), torch.from_numpy(src_s.view(np.float16)).cuda(),
+                           K, N, layout="nk3", group=group)
+    torch.cuda.synchronize()
+    assert np.array_equal(pw.cpu().numpy().view(np.uint32), want_p)
+    assert np.array_equal(host_bits(sc), want_s)
+    W3 = fm.dequant3(src_p, src_s, K, N, group).view(np.float16).astype(np.float64)   # [N][K]
+    for n in (1, 64):
+        x = inputs.activations(n + K + 3, n, K)
+        y = host_bits(ops.q4_matmul(dev_x(x), pw, sc, ws=ops.workspace(n, K, N)))
+        r = x.view(np.float16).astype(np.float64) @ W3.T
+        assert_within_tol(y, r, f"repacked nk3 G={group} {K}x{N} n={n}")

@@ -52,7 +52,7 @@ def test_format_matches_native_oracle(layout, group):
     assert np.array_equal(W, oracle.dequant(nat_p, nat_s, K, N))
 
 
-# ---- 3-bit ("nk3", reading 24) -------------------------------------
+# ---- 3-bit ("nk3", reading 20) -------------------------------------
 # Hand-worked group: codes c_i = i mod 8.  Word 0 = codes 0..7 in bits 0..23
 # (0b111_110_101_100_011_010_001_000 = 0xFAC688), code 8 = 0 in bits 24..26,
 # code 9 = 1 sets bit 27, code 10 = 2 = 0b010 puts its middle bit at bit 31
