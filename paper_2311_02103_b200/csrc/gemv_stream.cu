@@ -50,6 +50,7 @@ struct GsArgs {
     int rows_cta_max;
     uint32_t trace_seq;    // 0 = no trace, else launch sequence number
     int prefetch;          // stages the producer issues before griddepcontrol.wait
+    int l2_prefetch;       // bytes of codes beyond the ring pulled into L2 at the start (0: none)
     int trigger;           // where the CTA signals launch_dependents (0 start, 1 after x, 2 after stage 0)
     // fused neighbours (include/relax_q4.h RELAX_OP_*)
     uint32_t ops;
@@ -361,6 +362,25 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
             const uint64_t pol = policy_evict_first();
             const uint8_t* wsrc = w_base + row0 * cb_row;
             const uint8_t* ssrc = s_base + row0 * sb_row;
+#ifdef RQ4_EXPERIMENTS
+            if (a.l2_prefetch > 0) {
+                // experiments build: the rows beyond what the ring holds, pulled
+                // into L2 at the start so HBM keeps streaming across the kernel
+                // boundary -- measured slower (7B 1167 -> 967 tok/s at 192 KB
+                // per CTA, profiles/r02/l2pf/)
+                const int ring_rows = a.NS * a.RS;
+                if (rows > ring_rows) {
+                    uint64_t cbytes = static_cast<uint64_t>(rows - ring_rows) * cb_row;
+                    uint64_t sbytes = static_cast<uint64_t>(rows - ring_rows) * sb_row;
+                    const uint64_t cap = static_cast<uint64_t>(a.l2_prefetch);
+                    if (cbytes > cap) { sbytes = sbytes * cap / cbytes & ~15ull; cbytes = cap; }
+                    const uint8_t* cp = wsrc + static_cast<size_t>(ring_rows) * cb_row;
+                    for (uint64_t o = 0; o < cbytes; o += 32768)
+                        bulk_prefetch_l2(cp + o, static_cast<uint32_t>(cbytes - o < 32768 ? cbytes - o : 32768));
+                    if (sbytes > 0) bulk_prefetch_l2(ssrc + static_cast<size_t>(ring_rows) * sb_row, static_cast<uint32_t>(sbytes));
+                }
+            }
+#endif
             int slot = 0;
             uint32_t phase = 0;
             int issued = 0;
@@ -531,6 +551,9 @@ static bool gs_trace() { return RQ4_TRACE && knob_int("RELAX_Q4_TRACE", 0) == 1;
 static int gs_prefetch() { static const int v = knob_int("RELAX_Q4_GS_PREFETCH", -1); return v < 0 ? (1 << 30) : v; }
 // where each CTA signals griddepcontrol.launch_dependents (0: at its start)
 static int gs_trigger() { static const int v = knob_int("RELAX_Q4_GS_TRIGGER", 0); return v; }
+// bytes of codes per CTA beyond the ring prefetched into L2 at kernel start
+// (experiments build only; measured slower)
+static int gs_l2_prefetch() { static const int v = knob_int("RELAX_Q4_GS_L2PF_KB", 0); return v > 0 ? v * 1024 : 0; }
 // 2 = integer dot products (default); 1 = FHFMA with the factored
 // zero point, 0 = exact centering (experiments build)
 static int gs_zpf() { static const int v = knob_int("RELAX_Q4_GEMV_ZPF", 2); return v; }
@@ -666,6 +689,7 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.rows_cta_max = c.rows_cta_max;
         a.prefetch = gs_prefetch();
         a.trigger = gs_trigger();
+        a.l2_prefetch = gs_l2_prefetch();
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
         a.tp_world = 0;
         a.tp_rank = 0;
@@ -760,6 +784,7 @@ int launch_gemv_stream_grouped(const uint16_t* x, int64_t n, int64_t K, int coun
         a.rows_cta_max = c.rows_cta_max;
         a.prefetch = gs_prefetch();
         a.trigger = gs_trigger();
+        a.l2_prefetch = gs_l2_prefetch();
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
         const int rc = cnt == 1 ? launch_gs_z<1, 2>(a, c, pdl, stream) : launch_gs_z<2, 2>(a, c, pdl, stream);
         if (rc != 0) return rc;

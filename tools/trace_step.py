@@ -30,6 +30,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--grouped", action="store_true", help="q/k/v and gate/up as grouped launches (the bench default)")
     a = ap.parse_args()
     L = ops.lib()
     L.relax_debug_trace_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t,
@@ -46,9 +47,20 @@ def main():
     st = torch.cuda.Stream()
     flags = ops.FLAG_NO_PDL if a.no_pdl else 0
 
+    groups, i = [], 0
+    while i < len(mats):
+        kind = mats[i][0].split(".")[-1]
+        span = (3 if kind == "q" else 2 if kind == "gate" else 1) if a.grouped else 1
+        groups.append(list(range(i, i + span)))
+        i += span
+
     def step():
-        for (nm, K, N), (pk, sc), y in zip(mats, ws, ys):
-            ops.q4_matmul_ex(xs[K], pk, sc, y=y, flags=flags, stream=st)
+        for g in groups:
+            if len(g) == 1:
+                j = g[0]
+                ops.q4_matmul_ex(xs[mats[j][1]], *ws[j], y=ys[j], flags=flags, stream=st)
+            else:
+                ops.q4_matmul_grouped(xs[mats[g[0]][1]], [ws[j] for j in g], ys=[ys[j] for j in g], stream=st)
     with torch.cuda.stream(st):
         step()
     torch.cuda.synchronize()
@@ -72,7 +84,9 @@ def main():
     prev_end = None
     for i, s in enumerate(seqs):
         q = r[r["seq"] == s]
-        nm, K, N = mats[i % len(mats)]
+        g = groups[i % len(groups)]
+        K = mats[g[0]][1]
+        N = sum(mats[j][2] for j in g)
         us = lambda v: (v - T0) / 1e3  # noqa: E731
         line = (f"{s:>4} {K:>5}x{N:<6} {len(q):>4} | {us(q['t0'].min()):7.2f} {us(q['t0'].max()):7.2f} | "
                 f"{np.median(q['tw'] - q['t0']) / 1e3:9.2f} {np.median(q['tf'] - q['t0']) / 1e3:9.2f} | "
