@@ -160,8 +160,8 @@ def block_step(args, mats, weights, n, dev, stream):
     W_head . RMSNorm(h).  Without --kv the attention is a fixed fp16 tensor `a`
     standing in for its output; with --kv L (fused block, n = 1) it is the
     library's decode attention: the new token's k, v (slices
-    of the qkv output) appended at position L - 1 of the layer's fp16 KV cache
-    (relax_kv_append) and q attending over the L cached keys
+    of the qkv output) stored at position L - 1 of the layer's fp16 KV cache by
+    the qkv kernel itself (RELAX_OP_KV_APPEND epilogue) and q attending over the L cached keys
     (relax_attn_decode) -- the whole decode step, attention over a symbolic KV
     length included (RoPE is not applied: it does not change what is read or
     computed per byte).  --block fused runs each linear
@@ -219,14 +219,14 @@ def block_step(args, mats, weights, n, dev, stream):
             kind = name.split(".")[-1]
             if args.block == "fused":
                 if kind in ("qkv", "lm_head"):
+                    # with the KV cache the new token's k, v go to their cache
+                    # position in the same kernel (RELAX_OP_KV_APPEND epilogue)
+                    kva = (kv["k"][li], kv["v"][li], kv["pos"], hq * 128) if kind == "qkv" and kv is not None else None
                     ops.q4_matmul_fused(h, pk, sc, y=outs[name], rms_weight=gamma, rms_eps=eps, ws=wss[name],
-                                        stream=stream)
+                                        kv_append=kva, stream=stream)
                     if kind == "qkv" and kv is not None:
                         y = outs[name]
                         qv = y[:, :hq * 128].view(1, hq, 128)
-                        kn = y[:, hq * 128:(hq + hkv) * 128].view(1, hkv, 128)
-                        vn = y[:, (hq + hkv) * 128:].view(1, hkv, 128)
-                        ops.kv_append(kn, vn, kv["pos"], kv["k"][li], kv["v"][li], stream=stream)
                         ops.attn_decode(qv, kv["k"][li], kv["v"][li], kv["lens"], out=kv["out"], ws=kv["ws"],
                                         stream=stream)
                         li += 1
@@ -522,7 +522,7 @@ def run_ours(args, rank, world, local_rank):
     if chain is not None:
         launches = 1
     if args.kv > 0:
-        launches += 3 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))   # append, partial, combine
+        launches += 2 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv"))   # attention partial + combine
     label = (args.workload + ("-fused-qkv-gateup" if fused else "")
              + (f"-tp{args.tp_shard}-rank0-shard" if args.tp_shard > 1 else "")
              + (f"-megatron-tp{tp_world}" if tp_mode else "")
@@ -536,7 +536,7 @@ def run_ours(args, rank, world, local_rank):
         roof["per"] = "one launch per step"
     else:
         # per launch of the linears (a grouped q/k/v or gate/up launch counts once)
-        lin_launches = launches - (3 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv")) if args.kv > 0 else 0)
+        lin_launches = launches - (2 * sum(1 for nm, _, _ in mats if nm.endswith(".qkv")) if args.kv > 0 else 0)
         roof["algorithmic_bytes_per_launch"] = int(bytes_step / max(lin_launches, 1))
         kind0 = sched[f"{shapes[0][0]}x{shapes[0][1]}"]["variant"]
         roof["kernel"] = {"gemv": "q4_decode_stream_kernel (streamed decode GEMV)",

@@ -234,12 +234,23 @@ RELAX_API int relax_q4_matmul_ex(const void* x, int64_t n, int64_t K, int64_t N,
  *       so y has N/2 columns.
  *   RELAX_OP_RESIDUAL   (epilogue, residual add), applied last:
  *       y[t][j] = fp16_RNE(v + residual[t][j]),  v = the fp16 output so far.
+ *   RELAX_OP_KV_APPEND  (epilogue of the fused q/k/v projection at decode, the
+ *       consumer relax_kv_append fused into its producer): y is
+ *       written as usual and, in addition, its rows kv_row0 + h*128 + d
+ *       (h < kv_heads: the new token's keys) and kv_row0 + (kv_heads + h)*128
+ *       + d (its values) are stored at k_cache / v_cache[t][h][kv_pos[t]][d]
+ *       for token t (= sequence t; caches as relax_attn_decode; positions
+ *       outside [0, kv_len_max) store nothing).  Decode only: n <= 2 and a
+ *       shape the streamed decode kernel holds (else RELAX_ERR_UNSUPPORTED_SHAPE);
+ *       not with SILU_MUL.
  *
- * Combinations are allowed; the order is prologue, matmul, SiLU-mul, residual.
+ * Combinations are allowed; the order is prologue, matmul, SiLU-mul, residual,
+ * KV append.
  */
 #define RELAX_OP_RMSNORM_X 1u
 #define RELAX_OP_SILU_MUL 2u
 #define RELAX_OP_RESIDUAL 4u
+#define RELAX_OP_KV_APPEND 8u
 
 typedef struct relax_q4_fusion {
     uint32_t ops;             /* RELAX_OP_* bitmask (0 = plain matmul) */
@@ -249,6 +260,13 @@ typedef struct relax_q4_fusion {
                                  kernel waits on the previous kernel of the stream (PDL) */
     const void* residual;     /* RESIDUAL: device fp16 [n][N_out], 16-byte aligned; may be
                                  exactly y (in-place add) but not partially overlap it */
+    /* KV_APPEND (ignored otherwise; zero them) */
+    void* k_cache;            /* device fp16 [n][kv_heads][kv_len_max][128], 16-byte aligned */
+    void* v_cache;            /* likewise */
+    const int32_t* kv_pos;    /* device int32 [n]: the position written for each token */
+    int64_t kv_len_max;
+    int32_t kv_heads;
+    int32_t kv_row0;          /* first key row of y; kv_row0 + 2*kv_heads*128 <= N */
 } relax_q4_fusion;
 
 /* Workspace plan of relax_q4_matmul_fused for n <= n_max: the plain plan plus

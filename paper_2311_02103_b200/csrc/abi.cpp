@@ -312,7 +312,7 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
 // Fused neighbours (relax_q4_matmul_fused; include/relax_q4.h).  The plain
 // plan picks the variant; RMSNORM_X on the tensor-core path writes the
 // normalised x into the workspace after the plan's own bytes.
-static constexpr uint32_t kOpsAll = RELAX_OP_RMSNORM_X | RELAX_OP_SILU_MUL | RELAX_OP_RESIDUAL;
+static constexpr uint32_t kOpsAll = RELAX_OP_RMSNORM_X | RELAX_OP_SILU_MUL | RELAX_OP_RESIDUAL | RELAX_OP_KV_APPEND;
 
 static size_t align16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
 
@@ -326,6 +326,7 @@ static int fused_shape_check(int64_t K, int64_t N, uint32_t ops) {
     if (ops & ~kOpsAll) return RELAX_ERR_INVALID_ARG;
     if (ops != 0 && K % kTcWStageK != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
     if ((ops & RELAX_OP_SILU_MUL) && (N % 2) != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
+    if ((ops & RELAX_OP_KV_APPEND) && (ops & RELAX_OP_SILU_MUL)) return RELAX_ERR_INVALID_ARG;
     return RELAX_OK;
 }
 
@@ -341,8 +342,15 @@ static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint
     if ((ops & RELAX_OP_RMSNORM_X) && (!fz->rms_weight || !(fz->rms_eps >= 0.f) || !std::isfinite(fz->rms_eps)))
         return RELAX_ERR_INVALID_ARG;
     if ((ops & RELAX_OP_RESIDUAL) && !fz->residual) return RELAX_ERR_INVALID_ARG;
+    const bool kva = (ops & RELAX_OP_KV_APPEND) != 0;
+    if (kva && (!fz->k_cache || !fz->v_cache || !fz->kv_pos || fz->kv_len_max <= 0 || fz->kv_heads <= 0 ||
+                fz->kv_row0 < 0 || static_cast<int64_t>(fz->kv_row0) + 2 * 128 * static_cast<int64_t>(fz->kv_heads) > N))
+        return RELAX_ERR_INVALID_ARG;
+    if (kva && n > 2) return RELAX_ERR_UNSUPPORTED_SHAPE;         // decode only
     if (n == 0) return RELAX_OK;
     if (!x || !packed_w || !scales || !y) return RELAX_ERR_INVALID_ARG;
+    if (kva && (!aligned16(fz->k_cache) || !aligned16(fz->v_cache) || (reinterpret_cast<uintptr_t>(fz->kv_pos) & 3u)))
+        return RELAX_ERR_MISALIGNED;
     if (ws_bytes > 0 && !ws) return RELAX_ERR_INVALID_ARG;
     const void* gamma = (ops & RELAX_OP_RMSNORM_X) ? fz->rms_weight : nullptr;
     const void* res = (ops & RELAX_OP_RESIDUAL) ? fz->residual : nullptr;
@@ -359,6 +367,13 @@ static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint
         overlap(ws, ws_bytes, gamma, gb) || overlap(ws, ws_bytes, res, res ? yb : 0) ||
         (res && res != y && overlap(y, yb, res, yb)))
         return RELAX_ERR_ALIAS;
+    if (kva) {
+        const size_t cb = static_cast<size_t>(n) * fz->kv_heads * fz->kv_len_max * 128 * 2;
+        if (overlap(fz->k_cache, cb, y, yb) || overlap(fz->v_cache, cb, y, yb) || overlap(fz->k_cache, cb, x, xb) ||
+            overlap(fz->v_cache, cb, x, xb) || overlap(fz->k_cache, cb, fz->v_cache, cb) ||
+            overlap(fz->k_cache, cb, packed_w, wb) || overlap(fz->v_cache, cb, packed_w, wb))
+            return RELAX_ERR_ALIAS;
+    }
     Plan plan;
     rc = make_plan(n, K, N, kVariantAuto, 0, 0, &plan, false);
     if (rc == RELAX_OK && plan.ws_bytes > 0 && ws_bytes < plan.ws_bytes) {
@@ -373,6 +388,7 @@ static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint
         rc = make_plan(n, K, N, kVariantTc, 0, 0, &plan, false);
         if (rc != RELAX_OK) return rc;
     }
+    if (kva && plan.variant != kVariantGemv) return RELAX_ERR_UNSUPPORTED_SHAPE;   // the decode kernel's epilogue only
     const bool tc_norm = plan.variant == kVariantTc && (ops & RELAX_OP_RMSNORM_X);
     const size_t xn_off = fused_xn_offset(plan.ws_bytes);
     const size_t need = tc_norm ? xn_off + xb : plan.ws_bytes;
@@ -385,6 +401,14 @@ static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint
     fu.eps = (ops & RELAX_OP_RMSNORM_X) ? fz->rms_eps : 0.f;
     fu.gamma = static_cast<const uint16_t*>(gamma);
     fu.res = static_cast<const uint16_t*>(res);
+    if (kva) {
+        fu.kc = static_cast<uint16_t*>(fz->k_cache);
+        fu.vc = static_cast<uint16_t*>(fz->v_cache);
+        fu.kv_pos = fz->kv_pos;
+        fu.kv_lmax = fz->kv_len_max;
+        fu.kv_heads = fz->kv_heads;
+        fu.kv_row0 = fz->kv_row0;
+    }
     int e;
     if (plan.variant == kVariantGemv) {
         e = launch_gemv_stream(static_cast<const uint16_t*>(x), n, K, N, packed_w,

@@ -66,6 +66,12 @@ struct GsArgs {
     const uint8_t* sgp[kGsMaxGroup];
     uint16_t* ygp[kGsMaxGroup];
     int64_t Ngp[kGsMaxGroup];
+    // RELAX_OP_KV_APPEND: rows kv_row0 .. are also stored into the caches
+    uint16_t* kc;
+    uint16_t* vc;
+    const int32_t* kv_pos;
+    int64_t kv_lmax;
+    int kv_heads, kv_row0;
     // kOpTpAllReduce (relax_q4_matmul_allreduce): rank tp_rank of tp_world,
     // tp_bufs[p] = rank p's exchange buffer mapped on this device
     int tp_world, tp_rank;
@@ -523,8 +529,24 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
             for (int c = 0; c < a.WK; ++c) sum += part[(static_cast<size_t>(rl) * a.WK + c) * NT + t];
             const int64_t idx = static_cast<int64_t>(t) * Nout + row0 + rl;
             const bool pre = o == static_cast<int>(threadIdx.x) && warp < nwc;
-            y_base[idx] = residual_add(__half_as_ushort(__float2half_rn(sum * rescale)), ops,
-                                    (ops & RELAX_OP_RESIDUAL) ? (pre ? res_pre : a.res[idx]) : uint16_t(0));
+            const uint16_t v = residual_add(__half_as_ushort(__float2half_rn(sum * rescale)), ops,
+                                            (ops & RELAX_OP_RESIDUAL) ? (pre ? res_pre : a.res[idx]) : uint16_t(0));
+            y_base[idx] = v;
+            if (FU && (ops & RELAX_OP_KV_APPEND)) {
+                // the new token's key / value rows, also stored at its cache position
+                const int64_t kr = row0 + rl - a.kv_row0;
+                const int64_t span = static_cast<int64_t>(a.kv_heads) * 128;
+                if (kr >= 0 && kr < 2 * span) {
+                    const int p = a.kv_pos[t];
+                    if (p >= 0 && p < a.kv_lmax) {
+                        const bool isv = kr >= span;
+                        const int64_t hr = isv ? kr - span : kr;
+                        const int64_t hd = hr >> 7, d = hr & 127;
+                        uint16_t* cache = isv ? a.vc : a.kc;
+                        cache[((static_cast<int64_t>(t) * a.kv_heads + hd) * a.kv_lmax + p) * 128 + d] = v;
+                    }
+                }
+            }
         }
     }
 #if RQ4_TRACE
@@ -682,6 +704,17 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.ops = fu.ops;
         a.eps = fu.eps;
         a.gamma = fu.gamma;
+        a.kc = fu.kc;
+        a.vc = fu.vc;
+        a.kv_pos = fu.kv_pos ? fu.kv_pos + t0 : nullptr;
+        a.kv_lmax = fu.kv_lmax;
+        a.kv_heads = fu.kv_heads;
+        a.kv_row0 = fu.kv_row0;
+        if (fu.kc) {
+            const int64_t per_tok = static_cast<int64_t>(fu.kv_heads) * fu.kv_lmax * 128;
+            a.kc = fu.kc + t0 * per_tok;
+            a.vc = fu.vc + t0 * per_tok;
+        }
         a.res = fu.res ? fu.res + t0 * Nout : nullptr;
         a.Nout = Nout;
         a.nmat = 1;

@@ -67,6 +67,11 @@ struct Fusion {
     const uint16_t* gamma = nullptr;   // RMSNORM_X, fp16 [K]
     const uint16_t* res = nullptr;     // RESIDUAL, fp16 [n][N_out]
     const TpComm* tp = nullptr;        // kOpTpAllReduce: the exchange buffers
+    uint16_t* kc = nullptr;            // KV_APPEND: caches [n][H][Lmax][128], positions, shape
+    uint16_t* vc = nullptr;
+    const int32_t* kv_pos = nullptr;
+    int64_t kv_lmax = 0;
+    int kv_heads = 0, kv_row0 = 0;
 };
 
 enum Variant : int { kVariantAuto = 0, kVariantGemv = 1, kVariantTc = 2, kVariantSmallN = 3 };

@@ -47,13 +47,15 @@ EXPORTS = ("relax_plan_workspace", "relax_q4_matmul", "relax_q4_matmul_ws", "rel
 CHAIN_EXPORTS = ("relax_q4_chain_workspace", "relax_q4_chain_init", "relax_q4_chain_run")
 
 # fused neighbours (include/relax_q4.h RELAX_OP_*)
-OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL = 1, 2, 4
+OP_RMSNORM_X, OP_SILU_MUL, OP_RESIDUAL, OP_KV_APPEND = 1, 2, 4, 8
 
 
 class Fusion(ctypes.Structure):
     """struct relax_q4_fusion."""
     _fields_ = [("ops", ctypes.c_uint32), ("rms_eps", ctypes.c_float),
-                ("rms_weight", ctypes.c_void_p), ("residual", ctypes.c_void_p)]
+                ("rms_weight", ctypes.c_void_p), ("residual", ctypes.c_void_p),
+                ("k_cache", ctypes.c_void_p), ("v_cache", ctypes.c_void_p), ("kv_pos", ctypes.c_void_p),
+                ("kv_len_max", ctypes.c_int64), ("kv_heads", ctypes.c_int32), ("kv_row0", ctypes.c_int32)]
 
 
 TP_MAX_WORLD = 8
@@ -385,14 +387,16 @@ def plan_workspace_fused(n_max: int, K: int, N: int, ops: int) -> int:
 
 
 def q4_matmul_fused(x, packed_w, scales, y=None, rms_weight=None, rms_eps: float = 1e-5, silu_mul: bool = False,
-                    residual=None, ws=None, stream=None):
+                    residual=None, kv_append=None, ws=None, stream=None):
     """relax_q4_matmul_fused: optional RMSNorm prologue on x (rms_weight = gamma [K]),
-    SiLU-mul epilogue over interleaved (gate, up) rows (y has N/2 columns) and a
-    residual add; see include/relax_q4.h for the exact fp16 semantics."""
+    SiLU-mul epilogue over interleaved (gate, up) rows (y has N/2 columns), a
+    residual add, and (decode) the KV append: kv_append = (k_cache, v_cache,
+    pos, row0) stores y's rows row0 .. row0 + 2 H 128 (keys, then values) at
+    cache position pos[t]; see include/relax_q4.h for the exact semantics."""
     import torch
     n, K, N = _shapes(x, packed_w, scales)
     ops = (OP_RMSNORM_X if rms_weight is not None else 0) | (OP_SILU_MUL if silu_mul else 0) | \
-          (OP_RESIDUAL if residual is not None else 0)
+          (OP_RESIDUAL if residual is not None else 0) | (OP_KV_APPEND if kv_append is not None else 0)
     n_out = N // 2 if silu_mul else N
     y = _out(y, n, n_out, x)
     if rms_weight is not None:
@@ -400,6 +404,15 @@ def q4_matmul_fused(x, packed_w, scales, y=None, rms_weight=None, rms_eps: float
     if residual is not None:
         _check_tensor(residual, "residual", torch.float16, (n, n_out), dev=x.device)
     fz = Fusion(ops, float(rms_eps), _ptr(rms_weight) or None, _ptr(residual) or None)
+    if kv_append is not None:
+        kc, vc, pos, row0 = kv_append
+        if kc.dim() != 4 or kc.shape[0] != n or kc.shape[3] != 128:
+            raise ValueError(f"k_cache: shape {tuple(kc.shape)}, expected [n, H, L_max, 128]")
+        _check_tensor(kc, "k_cache", torch.float16, dev=x.device)
+        _check_tensor(vc, "v_cache", torch.float16, tuple(kc.shape), dev=x.device)
+        _check_tensor(pos, "pos", torch.int32, (n,), dev=x.device)
+        fz.k_cache, fz.v_cache, fz.kv_pos = _ptr(kc), _ptr(vc), _ptr(pos)
+        fz.kv_len_max, fz.kv_heads, fz.kv_row0 = kc.shape[2], kc.shape[1], int(row0)
     nb = _ws_bytes(ws, x.device)
     rc = lib().relax_q4_matmul_fused(_ptr(x), n, K, N, _ptr(packed_w), _ptr(scales), _ptr(y), ctypes.byref(fz),
                                      _ptr(ws), nb, _stream_ptr(stream))

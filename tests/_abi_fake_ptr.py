@@ -80,7 +80,7 @@ def fcall(L, ops_=0, eps=1e-5, gamma=A + 32 * MB, res=0, x=A, n=1, K=256, N=256,
 
 def fused_validation_codes(L):
     R, S, Q = ops.OP_RMSNORM_X, ops.OP_SILU_MUL, ops.OP_RESIDUAL
-    assert fcall(L, ops_=8) == 1                                  # unknown op bit
+    assert fcall(L, ops_=16) == 1                                 # unknown op bit
     assert fcall(L, ops_=R, K=96) == 2                            # fused ops need K % 256 == 0
     assert fcall(L, ops_=S, N=255) == 2                           # SiLU-mul pairs need N even
     assert fcall(L, ops_=R, gamma=0) == 1                         # RMSNorm without gamma
@@ -98,6 +98,29 @@ def fused_validation_codes(L):
     # a SiLU-mul decode call on a row pair layout too wide for the streamed
     # kernel takes the tensor path (needs no workspace without RMSNorm)
     assert fcall(L, ops_=S, n=1, K=16384, N=2 * 128256, w=A + 64 * MB, s=A + 4096 * MB, y=A + 8192 * MB) == 6
+
+
+def kv_append_validation(L):
+    """RELAX_OP_KV_APPEND (the KV append fused into the q/k/v epilogue)."""
+    KV = ops.OP_KV_APPEND
+    C = A + 512 * MB
+
+    def kcall(n=1, K=256, N=1024, kc=C, vc=C + 64 * MB, pos=C + 128 * MB, lmax=64, heads=2, row0=256, o=0):
+        fz = ops.Fusion(KV | o, 1e-5, (A + 32 * MB) if o & ops.OP_RMSNORM_X else None, None)
+        fz.k_cache, fz.v_cache, fz.kv_pos = kc, vc, pos
+        fz.kv_len_max, fz.kv_heads, fz.kv_row0 = lmax, heads, row0
+        return L.relax_q4_matmul_fused(A, n, K, N, A + 8 * MB, A + 16 * MB, A + 24 * MB, ctypes.byref(fz), 0, 0,
+                                       None)
+    assert kcall() == 6                                           # valid: device check
+    assert kcall(o=ops.OP_RMSNORM_X) == 6
+    assert kcall(kc=0) == 1 and kcall(pos=0) == 1 and kcall(heads=0) == 1 and kcall(lmax=0) == 1
+    assert kcall(row0=-1) == 1
+    assert kcall(row0=600) == 1                                   # rows past N
+    assert kcall(o=ops.OP_SILU_MUL) == 1                          # not with SiLU-mul
+    assert kcall(n=3) == 2                                        # decode only
+    assert kcall(kc=C + 8) == 3 and kcall(pos=C + 128 * MB + 2) == 3
+    assert kcall(kc=A + 24 * MB) == 4                             # cache over y
+    assert kcall(vc=C) == 4                                       # v cache over k cache
 
 
 def fused_plan_soundness(L):
@@ -203,7 +226,7 @@ def main():
     assert os.environ.get("CUDA_VISIBLE_DEVICES", None) == "", "run with CUDA_VISIBLE_DEVICES=''"
     L = ops.lib()
     for f in (validation_codes, workspace_too_small, plan_invalid, fused_validation_codes, fused_plan_soundness,
-              repack_validation, allreduce_validation):
+              repack_validation, allreduce_validation, kv_append_validation):
         f(L)
         print("ok", f.__name__)
     if hasattr(L, "relax_q4_chain_run"):            # the experiments build (RELAX_Q4_LIB)

@@ -78,3 +78,38 @@ def test_kv_append_then_attend_in_graph():
     got = host_bits(out)
     for b in range(batch):
         assert_within_tol(got[b], want[b], f"append+attend b={b}")
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_kv_append_fused_into_qkv_epilogue(n):
+    """RELAX_OP_KV_APPEND: the fused q/k/v projection (RMSNorm prologue) stores
+    its key / value rows at each token's cache position while writing y:
+    y is bit-identical to the same call without the op, the cache rows at the
+    positions equal y's key / value slices bit for bit, nothing else in the
+    caches changes, and out-of-range positions store nothing."""
+    from paper_2311_02103_b200 import inputs
+    from tests._util import dev_weights, dev_x
+    hq, hkv, K, lmax = 8, 2, 512, 300
+    N = (hq + 2 * hkv) * 128
+    pk, sc = inputs.realistic_weights(6100 + n, K, N)
+    w = dev_weights(pk, sc)
+    x = dev_x(inputs.activations(6200 + n, n, K))
+    gamma = torch.from_numpy(np.random.default_rng(1).uniform(0.5, 1.5, K).astype(np.float16)).cuda()
+    rng = np.random.default_rng(7)
+    k0 = rng.standard_normal((n, hkv, lmax, 128)).astype(np.float16)
+    v0 = rng.standard_normal((n, hkv, lmax, 128)).astype(np.float16)
+    for pos in ([299, 17][:n], [0, -1][:n], [lmax, 5][:n]):
+        kc, vc = torch.from_numpy(k0.copy()).cuda(), torch.from_numpy(v0.copy()).cuda()
+        pt = torch.tensor(pos, dtype=torch.int32, device="cuda")
+        y = ops.q4_matmul_fused(x, *w, rms_weight=gamma, kv_append=(kc, vc, pt, hq * 128))
+        y_ref = ops.q4_matmul_fused(x, *w, rms_weight=gamma)
+        torch.cuda.synchronize()
+        yb = host_bits(y)
+        assert np.array_equal(yb, host_bits(y_ref))
+        kb, vb = host_bits(kc), host_bits(vc)
+        kw, vw = k0.view(np.uint16).copy(), v0.view(np.uint16).copy()
+        for t, p in enumerate(pos):
+            if 0 <= p < lmax:
+                kw[t, :, p, :] = yb[t, hq * 128:(hq + hkv) * 128].reshape(hkv, 128)
+                vw[t, :, p, :] = yb[t, (hq + hkv) * 128:].reshape(hkv, 128)
+        assert np.array_equal(kb, kw) and np.array_equal(vb, vw), pos
