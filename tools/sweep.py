@@ -74,7 +74,9 @@ def main():
                     continue
                 if var == "smalln" and n > 32:
                     continue
-                base, _, sp = var.partition(":")        # "tc:S" forces split-K S (cluster reduction)
+                base, _, sp = var.partition(":")        # "tc:S" forces split-K S (cluster reduction), "tc:S:BN" the tile
+                sp, _, bnv = sp.partition(":")
+                bn = int(bnv) if bnv else 0
                 vflags = flags
                 if base.endswith("-np"):                # one tile per CTA (no persistent kernel)
                     base = base[:-3]
@@ -84,14 +86,15 @@ def main():
                      "smalln": ops.VARIANT_SMALLN}[base]
                 # a rotation long enough to stream >= 4 L2 of weights per replay
                 fns = [lambda p=p, s=s: ops.q4_matmul_ex(x, p, s, y=y, ws=ws, variant=v, flags=vflags,
-                                                         split_k=split, stream=stream) for p, s in copies]
+                                                         split_k=split, bn=bn, stream=stream) for p, s in copies]
                 try:
                     ms = time_calls(fns, a.reps, stream)
                 except Exception as e:  # noqa: BLE001
                     print(json.dumps({"K": K, "N": N, "n": n, "variant": var, "error": str(e)}), flush=True)
                     continue
                 by = wb + 2 * n * K + 2 * n * N
-                rec = {"K": K, "N": N, "n": n, "variant": var, "split": split, "sched": ops.query_schedule(n, K, N),
+                rec = {"K": K, "N": N, "n": n, "variant": var, "split": split, "bn": bn,
+                       "sched": ops.query_schedule(n, K, N),
                        "us": round(ms * 1e3, 3), "GBps": round(by / (ms * 1e-3) / 1e9, 1),
                        "TFLOPS": round(2 * n * K * N / (ms * 1e-3) / 1e12, 2), "R": R, "pdl": not a.no_pdl}
                 print(json.dumps(rec), flush=True)
