@@ -603,17 +603,20 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_sample(workload, n, nthreads=None, which=None):
+def oracle_sample(workload, n, nthreads=None, which=None, budget_s=None):
     """Time the oracle (oracle.matmul_f64, full outputs) on a bounded sample of
-    one step's workload: layer 0's linears at n tokens -- all seven, or only
-    linear `which` (the reference arm rotates through them, one per step).
-    Returns (extrapolated tok/s, measured sample seconds, info): the sample's
-    multiply-accumulates are a known fraction of the layer set's, so
+    one step's workload.  which = i: only linear i of layer 0 (the reference arm
+    rotates through them, one per step).  which = None: the layer set's linears
+    in order until `budget_s` seconds of oracle time have run (default 10 s;
+    for the 7B decode set on 16 cores that is the whole set, measured, not
+    extrapolated).  Returns (tok/s, measured sample seconds, info): a partial
+    sample is extrapolated by multiply-accumulate count,
     t_step = t_sample * MAC(set) / MAC(sample)."""
     import oracle
     model, mats = layer_set(workload)
     layer0 = [(nm, K, N) for nm, K, N in mats if nm.startswith("L0.")]
-    sample = layer0 if which is None else [layer0[which % len(layer0)]]
+    sample = mats if which is None else [layer0[which % len(layer0)]]
+    budget = 10.0 if budget_s is None else budget_s
     # all host cores the process may run on (torchrun sets OMP_NUM_THREADS=1)
     cores = nthreads or len(os.sched_getaffinity(0))
     gen = {}
@@ -621,19 +624,28 @@ def oracle_sample(workload, n, nthreads=None, which=None):
         if (K, N) not in gen:
             gen[(K, N)] = inputs.stress_weights(5 + K + N, K, N)
     xs = {K: inputs.activations(7 + n + K, n, K) for _, K, _ in sample}
+    done = []
     t0 = time.perf_counter()
     for nm, K, N in sample:
         pk, sc = gen[(K, N)]
         oracle.matmul_f64(xs[K], pk, sc, K, N, nthreads=cores)
+        done.append((nm, K, N))
+        if which is None and time.perf_counter() - t0 > budget:
+            break
     t_sample = time.perf_counter() - t0
-    mac_sample = sum(n * K * N for _, K, N in sample)
+    mac_sample = sum(n * K * N for _, K, N in done)
     mac_step = sum(n * K * N for _, K, N in mats)
     t_step = t_sample * mac_step / mac_sample
-    what = "layer 0's 7 linears" if which is None else "one linear of layer 0 per step (rotating q..down)"
+    if which is not None:
+        what = "one linear of layer 0 per step (rotating q..down)"
+    elif len(done) == len(mats):
+        what = f"the whole {len(mats)}-linear layer set (measured, no extrapolation)"
+    else:
+        what = f"the first {len(done)} of the {len(mats)} linears of the layer set (a {budget:.0f} s budget)"
+    tail = "" if len(done) == len(mats) else (f"; extrapolated by multiply-accumulate count to the "
+                                              f"{len(mats)}-linear layer set")
     return n / t_step, t_sample, {"cores": cores,
-                                  "sample": f"oracle (fp64, {cores} threads) on {what} at n={n}, full outputs; "
-                                            f"extrapolated by multiply-accumulate count to the "
-                                            f"{len(mats)}-linear layer set"}
+                                  "sample": f"oracle (fp64, {cores} threads) on {what} at n={n}, full outputs{tail}"}
 
 
 def run_reference(args):
