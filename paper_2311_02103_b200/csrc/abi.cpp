@@ -84,8 +84,8 @@ static int choose_bn(int64_t n, int64_t N) {
 // measured far slower than the model (cluster placement), so s > 1 requires
 // tiles * s <= 148.  The model only ranks schedules; results never depend on
 // it (every BN/split meets the same tolerance).
-static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out, bool* persist_out,
-                            bool allow_persist) {
+static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out, int* persist_out,
+                            bool allow_persist, bool allow_sk) {
     const int64_t tm = (N + kTcBM - 1) / kTcBM;
     const int64_t sms = num_sms();
     double best = 1e300;
@@ -96,7 +96,7 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
     if (allow_persist && (force_pbn == 128 || force_pbn == 256)) {
         *bn_out = force_pbn;
         *s_out = 1;
-        *persist_out = true;
+        *persist_out = 1;
         return;
     }
     if (allow_persist && tm * ((n + 255) / 256) >= min_per_sm * sms) {
@@ -126,9 +126,32 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
             if (t < best * 0.999) { best = t; bb = bn; bs = s; bp = false; }
         }
     }
+    int bpk = bp ? 1 : 0;
+    // Stream-K on the persistent kernel (gemm_tc_persist.cu): the (tile,
+    // 256-k stage) units spread evenly over the clusters, cut tiles reduced
+    // through the workspace -- for grids that whole tiles quantise badly
+    // (4096 x 11008 at n = 512: 172 tiles on 148 SMs).  Offered with a 10%
+    // margin over the model's best (the model is rough; the fixup costs a
+    // partial-tile write and read per cut tile).
+    // Measured slower wherever the model offers it (4096 x 11008 n = 512: 68.8 vs
+    // 51.0 us; profiles/r02/streamk_ab_r02.txt): the fixup's partial-tile
+    // reads are latency-bound and nearly every tile is cut.  Experiments
+    // build only (RELAX_Q4_STREAMK=1); the product keeps the schedules above.
+#ifdef RQ4_EXPERIMENTS
+    static const int sk_knob = knob_int("RELAX_Q4_STREAMK", 0);
+#else
+    const int sk_knob = 0;
+#endif
+    const int64_t tiles1 = tm * ((n + 255) / 256);                 // single-CTA BN = 256 tiles
+    const int64_t pair_tiles = ((tm + 1) / 2) * ((n + 255) / 256);
+    if (allow_persist && allow_sk && sk_knob && n >= 256 && pair_tiles * 2 <= static_cast<int64_t>(kTicketBytes / 4)) {
+        const int64_t per_cta = (tiles1 * kt + sms - 1) / sms;
+        const double t = static_cast<double>(per_cta) * kPersistStepUs + kPersistFixedUs + 2.0;
+        if (t < best * 0.9) { bb = 256; bs = 1; bpk = 2; }
+    }
     *bn_out = bb;
     *s_out = bs;
-    *persist_out = bp;
+    *persist_out = bpk;
 }
 
 // Split-K factor for small n (<= 64, HBM-bound): aim for about two CTAs per
@@ -152,7 +175,7 @@ static int choose_split(int64_t n, int64_t tiles, int kt, int bn) {
 }
 
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split, int force_bn,
-              Plan* out, bool force_ws, bool no_persist) {
+              Plan* out, bool force_ws, bool no_persist, bool allow_sk) {
     if (n < 0 || K <= 0 || N <= 0) return RELAX_ERR_INVALID_ARG;
     if (K % kGroup != 0) return RELAX_ERR_UNSUPPORTED_SHAPE;
     Plan p;
@@ -189,9 +212,9 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
                 return RELAX_ERR_INVALID_ARG;
             p.bn = force_bn;
         } else if (n > 64 && force_split <= 0) {
-            bool persist = false;
-            choose_tc_large(n, N, kt, &p.bn, &auto_split, &persist, !no_persist && persist_enabled());
-            p.persist = persist ? 1 : 0;
+            int persist = 0;
+            choose_tc_large(n, N, kt, &p.bn, &auto_split, &persist, !no_persist && persist_enabled(), allow_sk);
+            p.persist = persist;
         } else {
             p.bn = choose_bn(n, N);
         }
@@ -213,6 +236,7 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
         // the split fits a portable cluster (<= 8), else in the workspace.
         p.cluster = (s > 1 && s <= 8 && !force_ws) ? 1 : 0;
         p.ws_bytes = p.cluster ? 0 : tc_workspace_bytes(n, N, p.bn, s);
+        if (p.persist == 2) p.ws_bytes = persist_sk_ws_bytes(p.bn);
     } else {
         return RELAX_ERR_INVALID_ARG;
     }
@@ -280,10 +304,12 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
     const bool force_ws = (flags & RELAX_FLAG_SPLIT_WORKSPACE) != 0;
     const bool no_persist = (flags & RELAX_FLAG_TILE_PER_CTA) != 0;
     int rc = make_plan(n, K, N, variant, split_k, bn, &plan, force_ws, no_persist);
+    if (rc == RELAX_OK && plan.persist == 2 && ws_bytes < plan.ws_bytes)         // stream-K needs its workspace
+        rc = make_plan(n, K, N, variant, split_k, bn, &plan, force_ws, no_persist, false);
     if (rc == RELAX_OK && plan.ws_bytes > 0 && ws_bytes == 0 && !force_ws && split_k == 0) {
         // no workspace given: fall back to the largest cluster-reduced split
         int s = plan.split < 8 ? plan.split : 8;
-        rc = make_plan(n, K, N, variant, s, bn, &plan, false, no_persist);
+        rc = make_plan(n, K, N, variant, s, bn, &plan, false, no_persist, false);
     }
     if (rc != RELAX_OK) return rc;
     if (plan.ws_bytes > ws_bytes) return RELAX_ERR_WORKSPACE;
@@ -375,17 +401,17 @@ static int fused_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint
             return RELAX_ERR_ALIAS;
     }
     Plan plan;
-    rc = make_plan(n, K, N, kVariantAuto, 0, 0, &plan, false);
+    rc = make_plan(n, K, N, kVariantAuto, 0, 0, &plan, false, false, false);
     if (rc == RELAX_OK && plan.ws_bytes > 0 && ws_bytes < plan.ws_bytes) {
         const int sp = plan.split < 8 ? plan.split : 8;
-        rc = make_plan(n, K, N, kVariantAuto, sp, 0, &plan, false);
+        rc = make_plan(n, K, N, kVariantAuto, sp, 0, &plan, false, false, false);
     }
     if (rc != RELAX_OK) return rc;
     if (plan.variant == kVariantSmallN ||
         (plan.variant == kVariantGemv && !gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1))) {
         // the fused neighbours live in the streamed decode kernel and the
         // tensor-core kernel only: a shape the former cannot hold takes the latter
-        rc = make_plan(n, K, N, kVariantTc, 0, 0, &plan, false);
+        rc = make_plan(n, K, N, kVariantTc, 0, 0, &plan, false, false, false);
         if (rc != RELAX_OK) return rc;
     }
     if (kva && plan.variant != kVariantGemv) return RELAX_ERR_UNSUPPORTED_SHAPE;   // the decode kernel's epilogue only
@@ -447,13 +473,13 @@ int relax_plan_workspace_fused(int64_t n_max, int64_t K, int64_t N, uint32_t ops
     size_t best = 0;
     for (int64_t n = 1; n <= hi; ++n) {
         rq4::Plan p;
-        rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false);
+        rc = rq4::make_plan(n, K, N, rq4::kVariantAuto, 0, 0, &p, false, false, false);
         if (rc != RELAX_OK) return rc;
         // a GEMV plan the streamed decode kernel cannot hold runs on the TC path (fused_impl)
         if (p.variant == rq4::kVariantSmallN ||
             (p.variant == rq4::kVariantGemv &&
              !rq4::gemv_stream_ok(n >= 2 ? 2 : 1, K, N, (ops & RELAX_OP_SILU_MUL) ? 2 : 1))) {
-            rc = rq4::make_plan(n, K, N, rq4::kVariantTc, 0, 0, &p, false);
+            rc = rq4::make_plan(n, K, N, rq4::kVariantTc, 0, 0, &p, false, false, false);
             if (rc != RELAX_OK) return rc;
         }
         size_t need = p.ws_bytes;

@@ -65,7 +65,48 @@ struct TpArgs {
     uint16_t* y;
     int kt;                   // 256-k W stages per tile (= K / 256)
     int64_t m_tiles, tiles;   // m-tile pairs, and pair tiles = m_tiles * ceil(n / 256), pairs fastest
+    // stream-K (sk = 1): the units (pair tile, 256-k stage), tiles * kt of
+    // them, split into one contiguous range per cluster; a tile whose range is
+    // cut between clusters is reduced through the workspace by the last
+    // cluster to finish it (fp32 partials, fixed cluster order)
+    int sk;
+    int64_t units;
+    float* part;              // [cluster][rank][slot 0/1][128 rows][BN] fp32
+    uint32_t* tick;           // [pair tile][rank], zero before and after every call
 };
+
+// The work of one cluster: whole pair tiles p = cluster + i * clusters
+// (sk = 0), or the stages [kb0, kb1) of the pair tiles its unit range covers
+// (sk = 1).  Every warp role walks the same sequence.
+struct Seg {
+    int64_t p;
+    int kb0, kb1;
+};
+struct SegIter {
+    int64_t cur, end, step;
+    int kt, sk;
+    __device__ SegIter(const TpArgs& a, int64_t cid, int64_t nclu) : kt(a.kt), sk(a.sk) {
+        if (a.sk) { cur = cid * a.units / nclu; end = (cid + 1) * a.units / nclu; step = 0; }
+        else { cur = cid; end = a.tiles; step = nclu; }
+    }
+    __device__ bool next(Seg& g) {
+        if (cur >= end) return false;
+        if (!sk) { g.p = cur; g.kb0 = 0; g.kb1 = kt; cur += step; return true; }
+        g.p = cur / kt;
+        g.kb0 = static_cast<int>(cur - g.p * kt);
+        const int64_t left = end - cur;
+        g.kb1 = static_cast<int>(left < kt - g.kb0 ? g.kb0 + left : kt);
+        cur += g.kb1 - g.kb0;
+        return true;
+    }
+};
+// stream-K bookkeeping: first unit of cluster c, the cluster owning unit u,
+// and the partial slot cluster c uses for tile p (0: its range starts in the
+// tile, 1: the tile is the last of its range)
+__device__ __forceinline__ int64_t sk_start(const TpArgs& a, int64_t c, int64_t nclu) { return c * a.units / nclu; }
+__device__ __forceinline__ int64_t sk_owner(const TpArgs& a, int64_t u, int64_t nclu) {
+    return ((u + 1) * nclu + a.units - 1) / a.units - 1;
+}
 
 __device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -157,9 +198,11 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
             const uint64_t pol = policy_evict_last();           // W tiles are re-read by later token tiles
             int slot = 0;
             uint32_t ph = 0;
-            for (int64_t p = cid; p < a.tiles; p += nclu) {
-                const int32_t m0 = static_cast<int32_t>((2 * (p % a.m_tiles) + rank) * kTcBM);
-                for (int i = 0; i < a.kt; ++i) {
+            SegIter it(a, cid, nclu);
+            Seg g;
+            while (it.next(g)) {
+                const int32_t m0 = static_cast<int32_t>((2 * (g.p % a.m_tiles) + rank) * kTcBM);
+                for (int i = g.kb0; i < g.kb1; ++i) {
                     mbar_wait(&w_empty[slot], ph ^ 1);
                     mbar_arrive_expect_tx(&w_full[slot], kPCodes + kPScales);
                     tma_load_2d(codes_sm + slot * kPCodes, &tm_w, &w_full[slot], i * (kTcWStageK / 2), m0, pol);
@@ -175,9 +218,11 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
             const uint64_t pol = policy_evict_last();
             int slot = 0;
             uint32_t ph = 0;
-            for (int64_t p = cid; p < a.tiles; p += nclu) {
-                const int32_t n0 = static_cast<int32_t>((p / a.m_tiles) * kPBN + rank * (kPBN / 2));
-                for (int j = 0; j < nsub; ++j) {
+            SegIter it(a, cid, nclu);
+            Seg g;
+            while (it.next(g)) {
+                const int32_t n0 = static_cast<int32_t>((g.p / a.m_tiles) * kPBN + rank * (kPBN / 2));
+                for (int j = g.kb0 * 4; j < g.kb1 * 4; ++j) {
                     mbar_wait(&x_empty[slot], ph ^ 1);                // both CTAs released the slot
                     mbar_arrive_expect_tx(&x_full[slot], kPXStageBytes);     // own half + the peer's half
                     tma_load_2d_mc(x_sm + slot * kPXStageBytes + rank * (kPXStageBytes / 2), &tm_x, &x_full[slot],
@@ -193,12 +238,15 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
             int as = 0, xs = 0;
             uint32_t aph = 0, xph = 0;
             int it = 0;
-            for (int64_t p = cid; p < a.tiles; p += nclu, ++it) {
+            SegIter si(a, cid, nclu);
+            Seg g;
+            for (; si.next(g); ++it) {
                 const int b = it & 1;
                 mbar_wait(&acc_empty[b], ((it >> 1) & 1) ^ 1);        // the epilogue drained it
                 tc_fence_after();
                 const uint32_t d = tmem_base + static_cast<uint32_t>(b * kPBN);
-                for (int j = 0; j < nsub; ++j) {
+                const int j0 = g.kb0 * 4;
+                for (int j = j0; j < g.kb1 * 4; ++j) {
                     mbar_wait(&a_full[as], aph);
                     mbar_wait(&x_full[xs], xph);
                     tc_fence_after();
@@ -207,7 +255,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
 #pragma unroll
                     for (int kk = 0; kk < kTcXStageK / 16; ++kk)
                         tc_mma_ss(d, adesc + static_cast<uint64_t>(kk * 2), bdesc + static_cast<uint64_t>(kk * 2),
-                                  idesc, (j | kk) != 0 ? 1u : 0u);
+                                  idesc, (j != j0 || kk != 0) ? 1u : 0u);
                     tc_commit(&a_empty[as]);
                     tc_commit_mc(&x_empty[xs], 0x3);                  // release the slot in both CTAs
                     if (++as == kPASlots) { as = 0; aph ^= 1; }
@@ -226,8 +274,10 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
         const uint32_t rbase = static_cast<uint32_t>((m >> 3) * 1024 + (m & 7) * 128);
         int ws = 0, as = h;
         uint32_t wph = 0, aph = 0;
-        for (int64_t p = cid; p < a.tiles; p += nclu) {
-            for (int i = 0; i < a.kt; ++i) {
+        SegIter si(a, cid, nclu);
+        Seg g;
+        while (si.next(g)) {
+            for (int i = g.kb0; i < g.kb1; ++i) {
                 mbar_wait(&w_full[ws], wph);
                 const uint8_t* crow = codes_sm + ws * kPCodes + m * 128;
                 const uint32_t* srow = reinterpret_cast<const uint32_t*>(scales_sm + ws * kPScales + m * 16);
@@ -275,34 +325,100 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int it = 0;
         bool waited = false;
-        for (int64_t p = cid; p < a.tiles; p += nclu, ++it) {
+        __shared__ uint32_t sk_tick;
+        SegIter si(a, cid, nclu);
+        Seg g;
+        for (; si.next(g); ++it) {
+            const int64_t p = g.p;
             const int b = it & 1;
             const int64_t row = (2 * (p % a.m_tiles) + rank) * kTcBM + m;
             const int64_t n0 = (p / a.m_tiles) * kPBN;
             mbar_wait(&acc_full[b], (it >> 1) & 1);
             tc_fence_after();
-            if (!waited) { pdl_wait(); waited = true; }           // y may still be read by the previous kernel
+            if (!waited) { pdl_wait(); waited = true; }           // y / workspace may still be used by the previous kernel
             const uint32_t col0 = tmem_base + lane_base + static_cast<uint32_t>(b * kPBN);
             const bool row_ok = row < a.N;
-            uint32_t v0[16], v1[16];
-            tmem_ld_32x32b_x16(col0, v0);
-            tc_wait_ld();
+            if (!a.sk || (g.kb0 == 0 && g.kb1 == a.kt)) {
+                // the whole k range of the tile: fp16 stores straight from TMEM
+                uint32_t v0[16], v1[16];
+                tmem_ld_32x32b_x16(col0, v0);
+                tc_wait_ld();
 #pragma unroll 1
-            for (int c0 = 0; c0 < kPBN; c0 += 32) {
-                tmem_ld_32x32b_x16(col0 + c0 + 16, v1);
+                for (int c0 = 0; c0 < kPBN; c0 += 32) {
+                    tmem_ld_32x32b_x16(col0 + c0 + 16, v1);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t tok = n0 + c0 + i;
-                    if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v0[i])));
-                }
-                tc_wait_ld();
-                if (c0 + 32 < kPBN) tmem_ld_32x32b_x16(col0 + c0 + 32, v0);
+                    for (int i = 0; i < 16; ++i) {
+                        const int64_t tok = n0 + c0 + i;
+                        if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v0[i])));
+                    }
+                    tc_wait_ld();
+                    if (c0 + 32 < kPBN) tmem_ld_32x32b_x16(col0 + c0 + 32, v0);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int64_t tok = n0 + c0 + 16 + i;
-                    if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v1[i])));
+                    for (int i = 0; i < 16; ++i) {
+                        const int64_t tok = n0 + c0 + 16 + i;
+                        if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v1[i])));
+                    }
+                    tc_wait_ld();
                 }
-                tc_wait_ld();
+            } else {
+                // stream-K: a part of the tile's k range.  Write this cluster's fp32
+                // partial, take a ticket; the cluster that completes the tile sums
+                // every cluster's partial in cluster order and stores y.
+                const int64_t slot = sk_start(a, cid, nclu) >= p * a.kt ? 0 : 1;
+                float* mine = a.part + ((((cid * 2 + rank) * 2 + slot) * kTcBM) + m) * kPBN;
+#pragma unroll 1
+                for (int c0 = 0; c0 < kPBN; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(col0 + c0, v);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        *reinterpret_cast<float4*>(mine + c0 + i) =
+                            make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                        __uint_as_float(v[i + 3]));
+                }
+                asm volatile("bar.sync 5, 128;" ::: "memory");        // the 4 epilogue warps wrote their rows
+                if (warp == 12 && lane == 0) {
+                    __threadfence();
+                    sk_tick = atomicAdd(&a.tick[p * 2 + rank], 1u);
+                }
+                asm volatile("bar.sync 5, 128;" ::: "memory");
+                const int64_t ca = sk_owner(a, p * a.kt, nclu), cb = sk_owner(a, (p + 1) * a.kt - 1, nclu);
+                if (static_cast<int64_t>(sk_tick) == cb - ca) {
+                    __threadfence();                              // the other clusters' partials are visible
+#pragma unroll 1
+                    for (int c0 = 0; c0 < kPBN; c0 += 16) {
+                        uint32_t v[16];
+                        tmem_ld_32x32b_x16(col0 + c0, v);
+                        tc_wait_ld();
+                        float acc[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+                        for (int64_t cc = ca; cc <= cb; ++cc) {
+                            float val[16];
+                            if (cc == cid) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) val[i] = __uint_as_float(v[i]);
+                            } else {
+                                const int64_t sl = sk_start(a, cc, nclu) >= p * a.kt ? 0 : 1;
+                                const float* src = a.part + ((((cc * 2 + rank) * 2 + sl) * kTcBM) + m) * kPBN + c0;
+#pragma unroll
+                                for (int i = 0; i < 16; i += 4) {
+                                    const float4 f = __ldcg(reinterpret_cast<const float4*>(src + i));
+                                    val[i] = f.x; val[i + 1] = f.y; val[i + 2] = f.z; val[i + 3] = f.w;
+                                }
+                            }
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) acc[i] = cc == ca ? val[i] : acc[i] + val[i];
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int64_t tok = n0 + c0 + i;
+                            if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(acc[i]));
+                        }
+                    }
+                    if (warp == 12 && lane == 0) a.tick[p * 2 + rank] = 0u;   // zero again for the next call
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -318,9 +434,15 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     if (warp == 3) tmem_dealloc<C::kTmemCols>(tmem_base);
 }
 
+// Workspace of the stream-K schedule: the ticket region (zero before and after
+// every call) and one fp32 partial tile per (cluster, rank, slot).
+size_t persist_sk_ws_bytes(int bn) {
+    return kTicketBytes + static_cast<size_t>(num_sms() / 2) * 2 * 2 * kTcBM * bn * 4;
+}
+
 template <int BN>
 static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                                const uint16_t* s, uint16_t* y, bool pdl, cudaStream_t stream) {
+                                const uint16_t* s, uint16_t* y, bool sk, void* ws, bool pdl, cudaStream_t stream) {
     using C = PCfg<BN>;
     CUtensorMap mw, ms, mx;
     int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
@@ -341,8 +463,15 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
     a.m_tiles = ((N + kTcBM - 1) / kTcBM + 1) / 2;             // m-tile PAIRS (an odd last one is zero-filled)
     a.tiles = a.m_tiles * ((n + BN - 1) / BN);                  // pair tiles
     const int64_t clusters = num_sms() / 2;
+    a.sk = sk ? 1 : 0;
+    a.units = a.tiles * a.kt;
+    a.tick = static_cast<uint32_t*>(ws);
+    a.part = sk ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes) : nullptr;
+    if (sk && (!ws || a.tiles * 2 > static_cast<int64_t>(kTicketBytes / 4))) return static_cast<int>(cudaErrorInvalidValue);
+    // stream-K keeps every cluster busy (units >= clusters); whole tiles use at most one cluster per tile
+    const int64_t grid_clusters = sk ? (a.units < clusters ? a.units : clusters) : (a.tiles < clusters ? a.tiles : clusters);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(2 * (a.tiles < clusters ? a.tiles : clusters)));
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * grid_clusters));
     cfg.blockDim = dim3(kPThreads);
     cfg.dynamicSmemBytes = C::kSmemBytes;
     cfg.stream = stream;
@@ -359,14 +488,14 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
 }
 
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, int bn, bool pdl, cudaStream_t stream) {
+                      uint16_t* y, int bn, bool sk, void* ws, bool pdl, cudaStream_t stream) {
     if (K % kTcWStageK != 0 || n <= 0) return static_cast<int>(cudaErrorInvalidValue);
 #ifdef RQ4_EXPERIMENTS
     // BN = 128 tiles: measured slower than both BN = 256 and one tile per CTA at
     // every n (the A transform is re-done per 128 tokens; profiles/r02/sweep_persist_bn_r02.txt)
-    if (bn == 128) return launch_tc_persist_bn<128>(x, n, K, N, w, s, y, pdl, stream);
+    if (bn == 128) return launch_tc_persist_bn<128>(x, n, K, N, w, s, y, sk, ws, pdl, stream);
 #endif
-    if (bn == 256) return launch_tc_persist_bn<256>(x, n, K, N, w, s, y, pdl, stream);
+    if (bn == 256) return launch_tc_persist_bn<256>(x, n, K, N, w, s, y, sk, ws, pdl, stream);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 

@@ -82,7 +82,8 @@ struct Plan {
     int bn = 0;          // TC: token tile (MMA N)
     int split = 1;       // TC: split-K factor
     int cluster = 0;     // TC: split-K reduced in a thread-block cluster (DSMEM), no workspace
-    int persist = 0;     // TC: persistent kernel, double-buffered accumulator (BN = 128 / 256, no split)
+    int persist = 0;     // TC: persistent kernel, double-buffered accumulator (BN = 128 / 256, no split);
+                         // 2 = its stream-K schedule (k ranges split over clusters, workspace reduction)
     int grid = 0;
     size_t ws_bytes = 0; // workspace bytes this plan needs
 };
@@ -90,7 +91,7 @@ struct Plan {
 // Host-pure dispatch (a1): variant, tiles, split-K and workspace for (n,K,N).
 // `force_variant` / `force_split` / `force_bn` override (0 = choose).
 int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_split,
-              int force_bn, Plan* out, bool force_ws, bool no_persist = false);
+              int force_bn, Plan* out, bool force_ws, bool no_persist = false, bool allow_sk = true);
 size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split);
 int gemv_max_n();                   // GEMV/TC threshold (env RELAX_Q4_GEMV_MAX_N)
 bool gemv_fits(int nt, int64_t K);
@@ -171,8 +172,11 @@ bool gemv_row_ok(int64_t K);
 int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
                 uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
                 CUtensorMapSwizzle sw);
+// sk: the stream-K schedule (Plan::persist == 2), reduced through `ws`
+// (persist_sk_ws_bytes; its ticket region zero before and after the call).
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, int bn, bool pdl, cudaStream_t stream);
+                      uint16_t* y, int bn, bool sk, void* ws, bool pdl, cudaStream_t stream);
+size_t persist_sk_ws_bytes(int bn);
 int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                     const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
                     CUtensorMapSwizzle sw);

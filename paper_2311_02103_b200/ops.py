@@ -176,6 +176,8 @@ def query_schedule(n: int, K: int, N: int) -> dict:
     d = {"variant": name, "tile": t.value, "split_k": s.value, "ws_bytes": int(ws.value)}
     if pe.value:
         d["persistent"] = True
+    if pe.value == 2:
+        d["stream_k"] = True
     return d
 
 
