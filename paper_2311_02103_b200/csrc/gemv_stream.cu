@@ -49,6 +49,7 @@ struct GsArgs {
     uint32_t stage_bytes;  // RS * (K/2 + K/16)
     int rows_cta_max;
     uint32_t trace_seq;    // 0 = no trace, else launch sequence number
+    int trace_xload;       // trace: stamp t_first after the x loads (1) or after the conversion (0)
     int prefetch;          // stages the producer issues before griddepcontrol.wait
     int l2_prefetch;       // bytes of codes beyond the ring pulled into L2 at the start (0: none)
     int trigger;           // where the CTA signals launch_dependents (0 start, 1 after x, 2 after stage 0)
@@ -432,6 +433,14 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
             for (int q = 0; q < 4; ++q)
                 xr[t][q] = gv ? reinterpret_cast<const uint4*>(a.x + static_cast<int64_t>(t) * a.K + g * 32)[q]
                               : make_uint4(0u, 0u, 0u, 0u);
+#if RQ4_TRACE
+        // experiments: RELAX_Q4_TRACE_XLOAD=1 stamps t_first when the x loads have
+        // landed (before the fixed-point conversion) instead of after it
+        if (a.trace_seq && a.trace_xload && warp == 0 && lane == 0) {
+            asm volatile("" ::"r"(xr[0][0].x), "r"(xr[0][3].w));
+            tr_first = gtime() + ((xr[0][0].x ^ xr[0][3].w) == 0x9E3779B9u ? 1u : 0u);
+        }
+#endif
         if (ops & RELAX_OP_RMSNORM_X) rmsnorm_prologue<NT>(xr, gm, a, lane, kw, h, nwc, rms_red);
         // zero-point chains: the per-group FHFMA chains with every code = 7
         // (exactly what row_dot computes for an all-7 group)
@@ -460,7 +469,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
                 res_pre = a.res[static_cast<int64_t>(t) * Nout + col];
             }
         }
-        if (RQ4_TRACE && a.trace_seq && warp == 0 && lane == 0) tr_first = gtime();   // x in registers
+        if (RQ4_TRACE && a.trace_seq && !a.trace_xload && warp == 0 && lane == 0) tr_first = gtime();   // x in registers
         if (a.trigger == 1) pdl_launch_dependents();
         const int rsel = reduce_row_of_lane<RPW>(lane);
         const bool writer = (lane & (32 / RPW - 1)) == 0;
@@ -724,6 +733,7 @@ int launch_gemv_stream(const uint16_t* x, int64_t n, int64_t K, int64_t N, const
         a.trigger = gs_trigger();
         a.l2_prefetch = gs_l2_prefetch();
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
+        a.trace_xload = knob_int("RELAX_Q4_TRACE_XLOAD", 0);
         a.tp_world = 0;
         a.tp_rank = 0;
         for (int p = 0; p < kTpMaxWorld; ++p) a.tp_bufs[p] = nullptr;
@@ -819,6 +829,7 @@ int launch_gemv_stream_grouped(const uint16_t* x, int64_t n, int64_t K, int coun
         a.trigger = gs_trigger();
         a.l2_prefetch = gs_l2_prefetch();
         a.trace_seq = gs_trace() ? ++g_launch_seq : 0u;
+        a.trace_xload = knob_int("RELAX_Q4_TRACE_XLOAD", 0);
         const int rc = cnt == 1 ? launch_gs_z<1, 2>(a, c, pdl, stream) : launch_gs_z<2, 2>(a, c, pdl, stream);
         if (rc != 0) return rc;
     }
