@@ -511,6 +511,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
         }
     }
     __syncthreads();
+#if RQ4_TRACE
+    __shared__ uint64_t tr_epi;                           // every stage consumed: the epilogue starts
+    if (a.trace_seq && threadIdx.x == 0) tr_epi = gtime();
+#endif
     // fixed-order sum over the WK K-columns; fp32 -> fp16 RNE
     const float rescale = ZPF == 1 ? 16777216.0f : 1.0f;     // exact power-of-two rescale
     if (FU && (ops & kOpTpAllReduce)) {
@@ -562,11 +566,13 @@ __global__ void __launch_bounds__(MAXT, (MAXT <= 544 ? 2 : 1)) q4_decode_stream_
     if (a.trace_seq) {
         __syncthreads();
         if (threadIdx.x == 0) {
+            const uint64_t t_end = gtime();               // before the record's own global atomic
             const uint32_t i = atomicAdd(&g_trace_n, 1u);
             if (i < kTraceMax) {
                 TraceRec r;
-                r.seq = a.trace_seq; r.cta = blockIdx.x; r.smid = smid(); r.pad = 0;
-                r.t0 = t_start; r.t_wait = tr_wait; r.t_first = tr_first; r.t_end = gtime();
+                r.seq = a.trace_seq; r.cta = blockIdx.x; r.smid = smid();
+                r.pad = static_cast<uint32_t>(tr_epi - t_start);   // ns from start to the epilogue
+                r.t0 = t_start; r.t_wait = tr_wait; r.t_first = tr_first; r.t_end = t_end;
                 g_trace[i] = r;
             }
         }

@@ -80,7 +80,7 @@ def main():
     seqs = sorted(set(r["seq"].tolist()))
     T0 = r["t0"].min()
     print(f"{'seq':>4} {'shape':>12} {'ctas':>4} | {'start min/max':>15} | {'wait_rel':>9} {'first_rel':>9} | "
-          f"{'end min/max':>15} | {'x->end':>7}  (us, rel. to step start)")
+          f"{'end min/max':>15} | {'x->end':>7} {'first->epi':>10} {'epi':>6}  (us, rel. to step start)")
     prev_end = None
     for i, s in enumerate(seqs):
         q = r[r["seq"] == s]
@@ -91,6 +91,7 @@ def main():
         line = (f"{s:>4} {K:>5}x{N:<6} {len(q):>4} | {us(q['t0'].min()):7.2f} {us(q['t0'].max()):7.2f} | "
                 f"{np.median(q['tw'] - q['t0']) / 1e3:9.2f} {np.median(q['tf'] - q['t0']) / 1e3:9.2f} | "
                 f"{us(q['te'].min()):7.2f} {us(q['te'].max()):7.2f} | {np.median(q['te'] - q['tw']) / 1e3:7.2f}"
+                f" {np.median(q['t0'] + q['pad'] - q['tf']) / 1e3:10.2f} {np.median(q['te'] - q['t0'] - q['pad']) / 1e3:6.2f}"
                 f"  sm/cta {len(set(q['smid'].tolist()))}/{np.bincount(q['smid']).max()}")
         print(line)
         prev_end = q["te"].max()
