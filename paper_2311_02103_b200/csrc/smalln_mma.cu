@@ -61,6 +61,16 @@ constexpr size_t kSnSmemCap = 113 * 1024;
 
 constexpr int kSnMaxGroup = 4;                       // matrices per grouped launch
 
+#if RQ4_TRACE
+// per-CTA timeline (experiments build, RELAX_Q4_TRACE=1): start, after
+// griddepcontrol.wait, first stage's operands ready (x fragments + dz), epilogue
+// start, end (globaltimer ns)
+constexpr int kSnTraceMax = 1 << 16;
+struct SnTraceRec { uint32_t seq, cta, pad0, pad1; uint64_t t0, t_wait, t_first, t_epi, t_end; };
+__device__ SnTraceRec g_sn_trace[kSnTraceMax];
+__device__ uint32_t g_sn_trace_n;
+#endif
+
 struct SnArgs {
     const uint16_t* x;     // [n][K] fp16
     int K, G, n, NS, nkc;
@@ -72,6 +82,7 @@ struct SnArgs {
     uint16_t* ygp[kSnMaxGroup];
     int64_t Ngp[kSnMaxGroup];
     int64_t nrbgp[kSnMaxGroup];   // 16-row blocks of each matrix
+    uint32_t trace_seq;           // experiments build: 0 = no trace, else the launch's sequence number
 };
 
 // TMA descriptors of every matrix of the launch (kernel parameter space)
@@ -124,6 +135,10 @@ q4_smalln_mma_kernel(const __grid_constant__ SnMaps maps, const __grid_constant_
     const int nb = a.cta0[m + 1] - a.cta0[m];
     const int64_t Nm = a.Ngp[m];
     uint16_t* const ym = a.ygp[m];
+#if RQ4_TRACE
+    const uint64_t sn_t0 = a.trace_seq ? globaltimer() : 0;
+    __shared__ uint64_t sn_tw, sn_tf;
+#endif
     const int64_t rb0 = static_cast<int64_t>(cb) * a.nrbgp[m] / nb;
     const int64_t rb1 = static_cast<int64_t>(cb + 1) * a.nrbgp[m] / nb;
     const int nrb = static_cast<int>(rb1 - rb0);
@@ -162,6 +177,9 @@ q4_smalln_mma_kernel(const __grid_constant__ SnMaps maps, const __grid_constant_
         const int g = lane >> 2, t = lane & 3;
         const int w = warp;
         pdl_wait();
+#if RQ4_TRACE
+        if (a.trace_seq && threadIdx.x == 0) sn_tw = globaltimer();
+#endif
         const __half2 sixteenth = __float2half2_rn(0.0625f);
         const uint4 sevens = make_uint4(0x00070007u, 0x00700070u, 0u, 0u);
         uint4 bf[GPW];      // B fragments of the warp's groups of the current chunk (token g)
@@ -196,6 +214,9 @@ q4_smalln_mma_kernel(const __grid_constant__ SnMaps maps, const __grid_constant_
                     dz[j][1] = d[1];
                 }
             }
+#if RQ4_TRACE
+            if (a.trace_seq && threadIdx.x == 0 && st == 0) sn_tf = globaltimer();
+#endif
             if (rb == 0 && kc + 1 < a.nkc && g < a.n) {
                 // the next chunk's x is read at the next chunk boundary: pull it into
                 // L1 now, so that load does not stall all warps on an L2 round trip
@@ -256,6 +277,9 @@ q4_smalln_mma_kernel(const __grid_constant__ SnMaps maps, const __grid_constant_
         }
     }
     __syncthreads();
+#if RQ4_TRACE
+    const uint64_t sn_te0 = (a.trace_seq && threadIdx.x == 0) ? globaltimer() : 0;
+#endif
     // fixed-order sum over the 8 warps; y = fp16_RNE(2^24 * acc)
     const int rows = nrb * kSnRows;
     for (int o = threadIdx.x; o < rows * a.n; o += blockDim.x) {
@@ -268,6 +292,21 @@ q4_smalln_mma_kernel(const __grid_constant__ SnMaps maps, const __grid_constant_
         for (int c = 0; c < kSnWarps; ++c) sum += part[(static_cast<size_t>(c) * a.rows_max + rl) * kSnTok + tok];
         ym[static_cast<int64_t>(tok) * Nm + row] = __half_as_ushort(__float2half_rn(sum * 16777216.0f));
     }
+#if RQ4_TRACE
+    if (a.trace_seq) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint64_t te = globaltimer();
+            const uint32_t i = atomicAdd(&g_sn_trace_n, 1u);
+            if (i < kSnTraceMax) {
+                SnTraceRec r;
+                r.seq = a.trace_seq; r.cta = blockIdx.x; r.pad0 = 0; r.pad1 = 0;
+                r.t0 = sn_t0; r.t_wait = sn_tw; r.t_first = sn_tf; r.t_epi = sn_te0; r.t_end = te;
+                g_sn_trace[i] = r;
+            }
+        }
+    }
+#endif
 }
 
 // consumer warps (8; 16 in the experiments build with RELAX_Q4_SN_WARPS=16)
@@ -375,6 +414,10 @@ int launch_smalln_mma_grouped(const uint16_t* x, int64_t n, int64_t K, int count
         a.nkc = static_cast<int>((K + kSnChunkK - 1) / kSnChunkK);
         a.rows_max = c.rows_max;
         a.nmat = count;
+#if RQ4_TRACE
+        static uint32_t sn_seq = 0;
+        a.trace_seq = knob_int("RELAX_Q4_TRACE", 0) == 1 ? ++sn_seq : 0u;
+#endif
         for (int i = 0; i <= count; ++i) a.cta0[i] = c.cta0[i];
         for (int i = 0; i < count; ++i) {
             a.ygp[i] = y[i] + t0 * N[i];
@@ -410,3 +453,19 @@ int smalln_max_n() {
 }
 
 }  // namespace rq4
+
+#if RQ4_TRACE
+extern "C" RELAX_API int relax_debug_sntrace_read(void* host, size_t max_records, size_t* n_records, int reset) {
+    uint32_t n = 0;
+    if (cudaMemcpyFromSymbol(&n, rq4::g_sn_trace_n, sizeof n) != cudaSuccess) return RELAX_ERR_CUDA;
+    if (n > static_cast<uint32_t>(rq4::kSnTraceMax)) n = rq4::kSnTraceMax;
+    const size_t m = n < max_records ? n : max_records;
+    if (m && cudaMemcpyFromSymbol(host, rq4::g_sn_trace, m * sizeof(rq4::SnTraceRec)) != cudaSuccess) return RELAX_ERR_CUDA;
+    if (n_records) *n_records = m;
+    if (reset) {
+        const uint32_t z = 0;
+        if (cudaMemcpyToSymbol(rq4::g_sn_trace_n, &z, sizeof z) != cudaSuccess) return RELAX_ERR_CUDA;
+    }
+    return RELAX_OK;
+}
+#endif
