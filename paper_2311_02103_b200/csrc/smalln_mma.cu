@@ -58,6 +58,15 @@ constexpr uint32_t kSnScaleBytes = kSnRows * kSnChunkG * 2;     // 2 KB
 constexpr uint32_t kSnStageBytes = kSnCodeBytes + kSnScaleBytes;  // 18 KB (multiple of 1 KB)
 // Two CTAs per SM must fit (this kernel and the next one under PDL).
 constexpr size_t kSnSmemCap = 113 * 1024;
+constexpr size_t kSnSmemMax = 220 * 1024;           // the attribute (experiments may raise the cap; static smem aside)
+// experiments build: RELAX_Q4_SN_SMEM_KB raises the shared-memory cap (one CTA per SM above ~114 KB)
+static size_t sn_smem_cap() {
+    static const size_t v = [] {
+        const int kb = knob_int("RELAX_Q4_SN_SMEM_KB", 113);
+        return static_cast<size_t>(kb >= 64 && kb <= 220 ? kb : 113) * 1024;
+    }();
+    return v;
+}
 
 constexpr int kSnMaxGroup = 4;                       // matrices per grouped launch
 
@@ -354,9 +363,10 @@ static SnConfig sn_config_group(int64_t K, int count, const int64_t* N) {
     c.rows_max = static_cast<int>(nrb_max * kSnRows);
     const size_t part_bytes = static_cast<size_t>(nrb_max) * kSnRows * sn_warps() * kSnTok * 4;
     const size_t fixed = 1024 + 256 + part_bytes;
-    if (fixed + 3 * static_cast<size_t>(kSnStageBytes) > kSnSmemCap) return c;
-    const int ns = static_cast<int>((kSnSmemCap - fixed) / kSnStageBytes);
-    c.NS = ns > 8 ? 8 : ns;
+    const size_t cap = sn_smem_cap();
+    if (fixed + 3 * static_cast<size_t>(kSnStageBytes) > cap) return c;
+    const int ns = static_cast<int>((cap - fixed) / kSnStageBytes);
+    c.NS = ns > 12 ? 12 : ns;
     c.smem = fixed + static_cast<size_t>(c.NS) * kSnStageBytes;
     c.ok = true;
     return c;
@@ -399,7 +409,7 @@ int launch_smalln_mma_grouped(const uint16_t* x, int64_t n, int64_t K, int count
     }
     const int W = sn_warps();
     auto kern = W == 16 ? q4_smalln_mma_kernel<16> : q4_smalln_mma_kernel<8>;
-    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), static_cast<int>(kSnSmemCap));
+    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(kern), static_cast<int>(kSnSmemMax));
     if (e != cudaSuccess) return static_cast<int>(e);
     if (knob_int("RELAX_Q4_GS_PRINT", 0))
         fprintf(stderr, "smalln_mma K=%lld N0=%lld count=%d n=%lld NS=%d grid=%d smem=%zu\n", (long long)K,
