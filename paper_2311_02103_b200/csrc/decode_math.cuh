@@ -66,9 +66,6 @@ __device__ __forceinline__ int dp2a_hi(uint32_t a16x2, uint32_t b8x4, int c) {
     asm("dp2a.hi.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a16x2), "r"(b8x4), "r"(c));
     return d;
 }
-__device__ __forceinline__ uint32_t pack16(int lo, int hi) {
-    return (static_cast<uint32_t>(lo) & 0xFFFFu) | (static_cast<uint32_t>(hi) << 16);
-}
 
 // x (4 uint4 = 32 fp16 of one group) -> int16 pairs in the dp2a order
 // (x0,x2) (x4,x6) (x1,x3) (x5,x7) per 8 k, 7 * sum x_int, and 2^-e.
