@@ -779,9 +779,12 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             v, t_s, info = oracle_sample(args.workload, args.n)
+            v1, t1, info1 = oracle_sample(args.workload, args.n, nthreads=1, which=0)
             res["cpu_baseline"] = {"value": round(v, 6), "unit": "tok/s", "cores": info["cores"],
                                    "kind": "oracle", "sample": info["sample"], "sample_s": round(t_s, 3),
-                                   "cpu_model": cpu_model()}
+                                   "cpu_model": cpu_model(),
+                                   "single_thread": {"value": round(v1, 6), "unit": "tok/s", "sample": info1["sample"],
+                                                     "sample_s": round(t1, 3)}}
         print(json.dumps(res))
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
