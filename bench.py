@@ -368,8 +368,14 @@ def run_ours(args, rank, world, local_rank):
         # SURVEY §8(f) F1) unless --nccl-allreduce
         row_N = [N for name, K, N in mats if tpm.MEGATRON_KIND[name.split(".")[-1]] == "row"
                  and tpm.fused_allreduce_ok(n, K)]
-        exchange = tpm.TpExchange(max(row_N)) if row_N and not args.nccl_allreduce else None
-        tp_allreduce = "fused-epilogue" if exchange is not None else "nccl"
+        exchange, tp_allreduce = None, "nccl"
+        if row_N and not args.nccl_allreduce:
+            try:
+                exchange = tpm.TpExchange(max(row_N))
+                tp_allreduce = "fused-epilogue"
+            except Exception as e:  # noqa: BLE001  no peer mapping on this box: the NCCL all_reduce (GPU) instead
+                print(f"bench: fused all-reduce unavailable ({type(e).__name__}: {e}); using NCCL", file=sys.stderr)
+                tp_allreduce = "nccl (fused exchange unavailable)"
         lin = [tpm.megatron_linear(name.split(".")[-1], pk, sc, matmul=mm_for(K, N), exchange=exchange,
                                    stream=stream)
                for (name, K, N), (pk, sc) in zip(mats, weights)]
