@@ -375,7 +375,11 @@ def run_ours(args, rank, world, local_rank):
                 tp_allreduce = "fused-epilogue"
             except Exception as e:  # noqa: BLE001  no peer mapping on this box: the NCCL all_reduce (GPU) instead
                 print(f"bench: fused all-reduce unavailable ({type(e).__name__}: {e}); using NCCL", file=sys.stderr)
-                tp_allreduce = "nccl (fused exchange unavailable)"
+            # every rank must take the same path
+            ok = torch.tensor([1 if exchange is not None else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                exchange, tp_allreduce = None, "nccl (fused exchange unavailable)"
         lin = [tpm.megatron_linear(name.split(".")[-1], pk, sc, matmul=mm_for(K, N), exchange=exchange,
                                    stream=stream)
                for (name, K, N), (pk, sc) in zip(mats, weights)]
