@@ -9,6 +9,7 @@
 #include "relax_q4_debug.h"
 #endif
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -278,7 +279,21 @@ static int check_device() {
         std::lock_guard<std::mutex> lk(mu);
         cc[dev] = c;
     }
-    return c == 100 ? RELAX_OK : RELAX_ERR_DEVICE;
+    if (c != 100) return RELAX_ERR_DEVICE;
+    // The tensor maps are encoded with the driver API (cuTensorMapEncodeTiled),
+    // which needs the device's context current in the CALLING thread; a host
+    // thread whose runtime calls so far did not bind it (seen after other
+    // threads had driven the device) got CUDA_ERROR_INVALID_CONTEXT.  Bind the
+    // primary context once per (thread, device).
+    thread_local int bound_dev = -1;
+    if (bound_dev != dev) {
+        if (cudaSetDevice(dev) != cudaSuccess) {
+            cudaGetLastError();
+            return RELAX_ERR_DEVICE;
+        }
+        bound_dev = dev;
+    }
+    return RELAX_OK;
 }
 
 static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uint32_t* packed_w,
@@ -328,6 +343,12 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
         e = launch_tc(static_cast<const uint16_t*>(x), n, K, N, packed_w,
                       static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), plan, ws, pdl, st);
     if (e != 0) {
+#ifdef RQ4_EXPERIMENTS
+        if (knob_int("RELAX_Q4_PRINT_ERR", 0))
+            fprintf(stderr, "rq4: matmul n=%lld K=%lld N=%lld variant=%d bn=%d split=%d persist=%d: error %d (%s)\n",
+                    (long long)n, (long long)K, (long long)N, plan.variant, plan.bn, plan.split, plan.persist, e,
+                    cudaGetErrorString(static_cast<cudaError_t>(e)));
+#endif
         cudaGetLastError();
         return RELAX_ERR_CUDA;
     }

@@ -627,6 +627,12 @@ int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void
     CUresult r = enc(m, dt, static_cast<cuuint32_t>(rank), const_cast<void*>(base), d, st, bx, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+#ifdef RQ4_EXPERIMENTS
+    if (r != CUDA_SUCCESS && knob_int("RELAX_Q4_PRINT_ERR", 0))
+        fprintf(stderr, "rq4: cuTensorMapEncodeTiled -> %d (rank %d base %p dims %llu %llu box %u %u align64 %d)\n",
+                static_cast<int>(r), rank, base, (unsigned long long)d[0], (unsigned long long)d[1], bx[0], bx[1],
+                static_cast<int>((reinterpret_cast<uintptr_t>(m) & 63u) == 0));
+#endif
     return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
 }
 
@@ -686,9 +692,15 @@ static int launch_tc_k(const CUtensorMap& mw, const CUtensorMap& ms, const uint1
     CUtensorMap mx;
     int rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, a.K, a.n, a.K * 2, kTcXStageK, BN,
                          CU_TENSOR_MAP_SWIZZLE_128B);
+#ifdef RQ4_EXPERIMENTS
+    if (rc && knob_int("RELAX_Q4_PRINT_ERR", 0)) fprintf(stderr, "rq4: x map failed %d\n", rc);
+#endif
     if (rc) return rc;
     const cudaError_t ae = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_kernel<BN, FU>),
                                                static_cast<int>(Cfg::kSmemBytes), true);
+#ifdef RQ4_EXPERIMENTS
+    if (ae && knob_int("RELAX_Q4_PRINT_ERR", 0)) fprintf(stderr, "rq4: attrs failed %d\n", static_cast<int>(ae));
+#endif
     if (ae != cudaSuccess) return static_cast<int>(ae);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>((a.N + kTcBM - 1) / kTcBM),
@@ -716,7 +728,14 @@ static int launch_tc_k(const CUtensorMap& mw, const CUtensorMap& ms, const uint1
                          CU_TENSOR_MAP_SWIZZLE_NONE);
         if (rc) return rc;
     }
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN, FU>, mw, ms, mx, my, a));
+    const int lr = static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_kernel<BN, FU>, mw, ms, mx, my, a));
+#ifdef RQ4_EXPERIMENTS
+    if (lr && knob_int("RELAX_Q4_PRINT_ERR", 0))
+        fprintf(stderr, "rq4: tc launch BN=%d grid=(%u,%u,%u) cluster=%d smem=%u stream=%p: %d\n", BN, cfg.gridDim.x,
+                cfg.gridDim.y, cfg.gridDim.z, a.cluster, static_cast<unsigned>(cfg.dynamicSmemBytes),
+                static_cast<void*>(stream), lr);
+#endif
+    return lr;
 }
 
 template <int BN>
