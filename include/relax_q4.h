@@ -303,9 +303,9 @@ RELAX_API int relax_q4_matmul_fused(const void* x, int64_t n, int64_t K, int64_t
  * bytes needed; persistent: 1 when the TC schedule is the persistent
  * double-buffered-accumulator kernel, 2 for its stream-K schedule (the k
  * ranges of the tiles spread evenly over the CTA pairs, cut tiles reduced
- * through the workspace; only when the caller's workspace holds it, else the
- * call falls back to another schedule).  Errors: RELAX_ERR_INVALID_ARG,
- * RELAX_ERR_UNSUPPORTED_SHAPE. */
+ * through the workspace; experiments build only, and only when the caller's
+ * workspace holds it, else the call falls back to another schedule).
+ * Errors: RELAX_ERR_INVALID_ARG, RELAX_ERR_UNSUPPORTED_SHAPE. */
 RELAX_API int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile,
                          int* split_k, size_t* ws_bytes, int* persistent);
 

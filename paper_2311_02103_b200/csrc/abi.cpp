@@ -128,27 +128,34 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
         }
     }
     int bpk = bp ? 1 : 0;
-    // Stream-K on the persistent kernel (gemm_tc_persist.cu): the (tile,
-    // 256-k stage) units spread evenly over the clusters, cut tiles reduced
-    // through the workspace -- for grids that whole tiles quantise badly
-    // (4096 x 11008 at n = 512: 172 tiles on 148 SMs).  Offered with a 10%
-    // margin over the model's best (the model is rough; the fixup costs a
-    // partial-tile write and read per cut tile).
-    // Measured slower wherever the model offers it (4096 x 11008 n = 512: 68.8 vs
-    // 51.0 us; profiles/r02/streamk_ab_r02.txt): the fixup's partial-tile
-    // reads are latency-bound and nearly every tile is cut.  Experiments
-    // build only (RELAX_Q4_STREAMK=1); the product keeps the schedules above.
+    // Stream-K on the persistent kernel (gemm_tc_persist.cu) for grids that
+    // whole tiles quantise badly (4096 x 11008 at n = 512: 86 pair tiles on 74
+    // CTA pairs): the full waves run as whole tiles, the W rest tiles are cut
+    // into (tile, 256-k stage) units spread evenly over all pairs and run
+    // FIRST, so the fixup of a cut tile (partials through the workspace) runs
+    // in the epilogue while the MMA streams a whole tile.  Model: a pair's
+    // stages x the persistent step + fill/drain (+ the exposed fixup of a
+    // grid without whole tiles).
+    // Measured slower than the whole-tile schedules on most 7B/70B shapes
+    // (profiles/r02/streamk_ab_r02.txt: the fixup traffic of 128-KB fp32
+    // partials per cut tile competes with the MMA operand stream in L2), so
+    // the product never offers it; experiments build: RELAX_Q4_STREAMK=1.
 #ifdef RQ4_EXPERIMENTS
     static const int sk_knob = knob_int("RELAX_Q4_STREAMK", 0);
 #else
     const int sk_knob = 0;
 #endif
-    const int64_t tiles1 = tm * ((n + 255) / 256);                 // single-CTA BN = 256 tiles
+    const int64_t clusters = sms / 2;
     const int64_t pair_tiles = ((tm + 1) / 2) * ((n + 255) / 256);
     if (allow_persist && allow_sk && sk_knob && n >= 256 && pair_tiles * 2 <= static_cast<int64_t>(kTicketBytes / 4)) {
-        const int64_t per_cta = (tiles1 * kt + sms - 1) / sms;
-        const double t = static_cast<double>(per_cta) * kPersistStepUs + kPersistFixedUs + 2.0;
-        if (t < best * 0.9) { bb = 256; bs = 1; bpk = 2; }
+        const int64_t full = pair_tiles / clusters, rest = pair_tiles - full * clusters;
+        if (rest > 0 && (full > 0 || sk_knob == 2)) {
+            // (a rest with fewer units than clusters takes one full wave with it, gemm_tc_persist.cu)
+            const int64_t cut = rest * kt < clusters && full > 0 ? rest + clusters : rest;
+            const int64_t stages = (pair_tiles - cut) / clusters * kt + (cut * kt + clusters - 1) / clusters;
+            const double t = static_cast<double>(stages) * kPersistStepUs + kPersistFixedUs + (full ? 1.0 : 3.0);
+            if (t < best * 0.9) { bb = 256; bs = 1; bpk = 2; }
+        }
     }
     *bn_out = bb;
     *s_out = bs;

@@ -840,7 +840,7 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
         a.cnt = static_cast<uint32_t*>(ws);
         a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes);
     }
-    if (plan.persist && a.ops == 0) return launch_tc_persist(x, n, K, N, w, s, y, plan.bn, plan.persist == 2, ws, pdl, stream);
+    if (plan.persist && a.ops == 0) return launch_tc_persist(x, n, K, N, w, s, y, plan.bn, plan.persist, ws, pdl, stream);
     switch (plan.bn) {
         case 16: return launch_tc_bn<16>(mw, ms, x, a, pdl, stream);
         case 32: return launch_tc_bn<32>(mw, ms, x, a, pdl, stream);

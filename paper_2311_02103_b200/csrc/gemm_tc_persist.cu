@@ -30,6 +30,7 @@
 // griddepcontrol.wait; x loads and y stores wait.
 #include <cstdio>
 #include "internal.h"
+#include "knobs.h"
 #include "relax_q4.h"
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
@@ -65,47 +66,84 @@ struct TpArgs {
     uint16_t* y;
     int kt;                   // 256-k W stages per tile (= K / 256)
     int64_t m_tiles, tiles;   // m-tile pairs, and pair tiles = m_tiles * ceil(n / 256), pairs fastest
-    // stream-K (sk = 1): the units (pair tile, 256-k stage), tiles * kt of
-    // them, split into one contiguous range per cluster; a tile whose range is
-    // cut between clusters is reduced through the workspace by the last
-    // cluster to finish it (fp32 partials, fixed cluster order)
+    // stream-K (sk = 1): the pair tiles [sk_tile0, tiles) are cut into units
+    // (pair tile, 256-k stage), units = (tiles - sk_tile0) * kt of them, split
+    // into one contiguous range per cluster; a tile whose range is cut between
+    // clusters is reduced through the workspace by the last cluster to finish
+    // it (fp32 partials, fixed cluster order).  The whole tiles [0, sk_tile0)
+    // (a multiple of the cluster count: the full waves) go round-robin, AFTER
+    // each cluster's units, so the fixups of the cut tiles run in the
+    // epilogue while the MMA streams a whole tile (sk_tile0 = 0: pure stream-K).
     int sk;
-    int64_t units;
-    float* part;              // [cluster][rank][slot 0/1][128 rows][BN] fp32
+    int64_t units, sk_tile0;
+    float* part;              // [cluster][rank][slot 0/1][BN/4][128 rows][4] fp32
     uint32_t* tick;           // [pair tile][rank], zero before and after every call
+    int trace;                // experiments build: per-CTA segment timeline
 };
+
+// Experiments build (RELAX_Q4_TRACE=1): per CTA {smid, segments, t_setup,
+// per segment (<= kPtSegs) {p, t_acc_full, t_partial_written, t_all_partials,
+// t_done}, t_end} in globaltimer ns (relax_debug_ptrace_read)
+constexpr int kPtSegs = 8;
+constexpr int kPtWords = 3 + kPtSegs * 5 + 1;
+#if RQ4_TRACE
+__device__ uint64_t g_ptrace[512 * kPtWords];
+#define PT_STAMP(w, v) do { if (a.trace && lane == 0 && warp == 12) g_ptrace[blockIdx.x * kPtWords + (w)] = (v); } while (0)
+#else
+#define PT_STAMP(w, v) do { } while (0)
+#endif
 
 // The work of one cluster: whole pair tiles p = cluster + i * clusters
 // (sk = 0), or the stages [kb0, kb1) of the pair tiles its unit range covers
-// (sk = 1).  Every warp role walks the same sequence.
+// followed by its whole tiles (sk = 1).  Every warp role walks the same sequence.
 struct Seg {
     int64_t p;
     int kb0, kb1;
 };
 struct SegIter {
-    int64_t cur, end, step;
+    int64_t cur, end, step, dp, dpend;
     int kt, sk;
     __device__ SegIter(const TpArgs& a, int64_t cid, int64_t nclu) : kt(a.kt), sk(a.sk) {
-        if (a.sk) { cur = cid * a.units / nclu; end = (cid + 1) * a.units / nclu; step = 0; }
-        else { cur = cid; end = a.tiles; step = nclu; }
+        if (a.sk) {
+            const int64_t base = a.sk_tile0 * a.kt;
+            cur = base + cid * a.units / nclu;
+            end = base + (cid + 1) * a.units / nclu;
+            dp = cid; dpend = a.sk_tile0; step = nclu;
+        } else { cur = cid; end = a.tiles; step = nclu; dp = dpend = 0; }
     }
     __device__ bool next(Seg& g) {
-        if (cur >= end) return false;
-        if (!sk) { g.p = cur; g.kb0 = 0; g.kb1 = kt; cur += step; return true; }
-        g.p = cur / kt;
-        g.kb0 = static_cast<int>(cur - g.p * kt);
-        const int64_t left = end - cur;
-        g.kb1 = static_cast<int>(left < kt - g.kb0 ? g.kb0 + left : kt);
-        cur += g.kb1 - g.kb0;
+        if (!sk) {
+            if (cur >= end) return false;
+            g.p = cur; g.kb0 = 0; g.kb1 = kt; cur += step; return true;
+        }
+        if (cur < end) {
+            g.p = cur / kt;
+            g.kb0 = static_cast<int>(cur - g.p * kt);
+            const int64_t left = end - cur;
+            g.kb1 = static_cast<int>(left < kt - g.kb0 ? g.kb0 + left : kt);
+            cur += g.kb1 - g.kb0;
+            return true;
+        }
+        if (dp >= dpend) return false;
+        g.p = dp; g.kb0 = 0; g.kb1 = kt; dp += step;
         return true;
     }
 };
-// stream-K bookkeeping: first unit of cluster c, the cluster owning unit u,
-// and the partial slot cluster c uses for tile p (0: its range starts in the
-// tile, 1: the tile is the last of its range)
-__device__ __forceinline__ int64_t sk_start(const TpArgs& a, int64_t c, int64_t nclu) { return c * a.units / nclu; }
+// stream-K bookkeeping (global unit u = pair tile * kt + stage): first unit of
+// cluster c, the cluster owning unit u, and the partial slot cluster c uses
+// for tile p (0: its range starts in the tile, 1: the tile is the last of its range)
+__device__ __forceinline__ int64_t sk_start(const TpArgs& a, int64_t c, int64_t nclu) {
+    return a.sk_tile0 * a.kt + c * a.units / nclu;
+}
 __device__ __forceinline__ int64_t sk_owner(const TpArgs& a, int64_t u, int64_t nclu) {
-    return ((u + 1) * nclu + a.units - 1) / a.units - 1;
+    return ((u - a.sk_tile0 * a.kt + 1) * nclu + a.units - 1) / a.units - 1;
+}
+// the fixup loads the partials of up to this many clusters at once
+constexpr int kSkMaxP = 8;
+// fp32 partial of (cluster, rank, slot): float4 j of row m at [j][m], so a
+// warp's 32 rows of one float4 column are 512 contiguous bytes
+__device__ __forceinline__ float4* sk_part(const TpArgs& a, int64_t c, uint32_t rank, int64_t slot, int bn) {
+    return reinterpret_cast<float4*>(a.part + ((c * 2 + rank) * 2 + slot) * kTcBM * bn);
 }
 
 __device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -159,7 +197,6 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
 
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
-    const int nsub = a.kt * (kTcWStageK / kTcXStageK);      // 64-k sub-blocks per tile
     // CTA pairs (clusters of 2) share each token tile: pair p covers m-tiles
     // 2 (p % m_pairs) + {0, 1} of token tile p / m_pairs; each CTA loads half
     // of every x stage and multicasts it to both, halving the L2 -> SM traffic
@@ -325,20 +362,109 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int it = 0;
         bool waited = false;
-        __shared__ uint32_t sk_tick;
         SegIter si(a, cid, nclu);
         Seg g;
+#ifdef RQ4_EXPERIMENTS
+        // stream-K: the cut tiles whose partial this cluster has written and
+        // whose slice it still has to sum (a cluster's cut tiles come first in
+        // its sequence, at most kSkPending of them, and are summed only once
+        // all their partials are written, so no partial waits behind a sum)
+        constexpr int kSkPending = 4;
+        int64_t pend[kSkPending];
+        int npend = 0;
+        int pend_it[kSkPending];
+        // Sum column slice k of cut tile p over the P partials of clusters
+        // ca..cb in cluster order and store it (fp16 RNE).
+        auto sk_fixup = [&](const int64_t p, const int tr) {
+            const int64_t row = (2 * (p % a.m_tiles) + rank) * kTcBM + m;
+            const int64_t n0 = (p / a.m_tiles) * kPBN;
+            const bool row_ok = row < a.N;
+            const int64_t ca = sk_owner(a, p * a.kt, nclu), cb = sk_owner(a, (p + 1) * a.kt - 1, nclu);
+            const int P = static_cast<int>(cb - ca + 1);
+            const int k = static_cast<int>(cid - ca);
+            uint32_t* tick = &a.tick[p * 2 + rank];
+            if (warp == 12 && lane == 0) {
+                const uint64_t t0 = globaltimer();
+                while (ld_acquire_gpu_u32(tick) < static_cast<uint32_t>(P)) {
+                    __nanosleep(64);
+                    if (globaltimer() - t0 > 10000000000ull) __trap();   // a partial never came: fail loudly
+                }
+            }
+            asm volatile("bar.sync 5, 128;" ::: "memory");
+            if (tr < kPtSegs) PT_STAMP(6 + tr * 5, globaltimer());
+            // column slice k: float4 columns [j0, j1) of the tile
+            const int nj = kPBN / 4;
+            const int j0 = k * nj / P, j1 = (k + 1) * nj / P;
+            // source c = 0 is cluster ca (slot 1 if the tile is the second of
+            // its range); every later contributor's range starts in the tile (slot 0)
+            const float4* src0 = sk_part(a, ca, rank, sk_start(a, ca, nclu) >= p * a.kt ? 0 : 1, kPBN) + m;
+            const float4* src1 = sk_part(a, ca + 1, rank, 0, kPBN) + m;
+            constexpr int64_t kSrcStride = 4 * kTcBM * kPBN / 4;     // float4s between clusters' slot-0 partials
+            // (column j, source c) pairs in order, kSkMaxP loads in flight
+            // per batch; each column summed over c = 0..P-1 in order
+            const int L = (j1 - j0) * P;
+            int jl = j0, cl = 0;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+            for (int q0 = 0; q0 < L; q0 += kSkMaxP) {
+                float4 f[kSkMaxP];
+                int jq = jl, cq = cl;
+#pragma unroll
+                for (int t = 0; t < kSkMaxP; ++t) {
+                    if (q0 + t < L) {
+                        const float4* src = cq == 0 ? src0 : src1 + (cq - 1) * kSrcStride;
+                        f[t] = __ldcg(src + jq * kTcBM);
+                        if (++cq == P) { cq = 0; ++jq; }
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < kSkMaxP; ++t) {
+                    if (q0 + t < L) {
+                        if (cl == 0) acc = f[t];
+                        else { acc.x += f[t].x; acc.y += f[t].y; acc.z += f[t].z; acc.w += f[t].w; }
+                        if (cl == P - 1) {
+                            const float o[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const int64_t tok = n0 + 4 * jl + i;
+                                if (row_ok && tok < a.n)
+                                    a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(o[i]));
+                            }
+                        }
+                        if (++cl == P) { cl = 0; ++jl; }
+                    }
+                }
+            }
+            asm volatile("bar.sync 5, 128;" ::: "memory");           // every row of the slice read
+            if (tr < kPtSegs) PT_STAMP(7 + tr * 5, globaltimer());
+            if (warp == 12 && lane == 0) {
+                // the last of the P clusters to finish its slice zeroes the counter for the next call
+                if (atomicAdd(tick, 1u) == static_cast<uint32_t>(2 * P - 1)) *tick = 0u;
+            }
+        };
+#endif
+        PT_STAMP(2, globaltimer());
         for (; si.next(g); ++it) {
             const int64_t p = g.p;
             const int b = it & 1;
+#ifdef RQ4_EXPERIMENTS
+            const bool whole = !a.sk || (g.kb0 == 0 && g.kb1 == a.kt);
+            if (whole) {
+                for (int i = 0; i < npend; ++i) sk_fixup(pend[i], pend_it[i]);
+                npend = 0;
+            }
+#else
+            constexpr bool whole = true;              // the product never schedules stream-K (abi.cpp)
+#endif
             const int64_t row = (2 * (p % a.m_tiles) + rank) * kTcBM + m;
             const int64_t n0 = (p / a.m_tiles) * kPBN;
             mbar_wait(&acc_full[b], (it >> 1) & 1);
             tc_fence_after();
+            if (it < kPtSegs) { PT_STAMP(3 + it * 5, static_cast<uint64_t>(p) | (static_cast<uint64_t>(g.kb0) << 32) | (static_cast<uint64_t>(g.kb1) << 48)); PT_STAMP(4 + it * 5, globaltimer()); }
             if (!waited) { pdl_wait(); waited = true; }           // y / workspace may still be used by the previous kernel
             const uint32_t col0 = tmem_base + lane_base + static_cast<uint32_t>(b * kPBN);
             const bool row_ok = row < a.N;
-            if (!a.sk || (g.kb0 == 0 && g.kb1 == a.kt)) {
+            if (whole) {
                 // the whole k range of the tile: fp16 stores straight from TMEM
                 uint32_t v0[16], v1[16];
                 tmem_ld_32x32b_x16(col0, v0);
@@ -360,12 +486,22 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                     }
                     tc_wait_ld();
                 }
-            } else {
-                // stream-K: a part of the tile's k range.  Write this cluster's fp32
-                // partial, take a ticket; the cluster that completes the tile sums
-                // every cluster's partial in cluster order and stores y.
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[b]);
+                if (it < kPtSegs) PT_STAMP(7 + it * 5, globaltimer());
+            }
+#ifdef RQ4_EXPERIMENTS
+            else {
+                // stream-K: a part of the tile's k range, shared by the P clusters
+                // ca..cb.  Each writes its fp32 partial, releases the accumulator
+                // at once and counts itself in; when all P partials are in,
+                // cluster ca + k sums column slice k (sk_fixup, deferred until
+                // this cluster's cut tiles are all written).  The P clusters are
+                // co-resident (one persistent CTA pair per SM pair) and no
+                // partial write waits for a sum, so every wait ends.
                 const int64_t slot = sk_start(a, cid, nclu) >= p * a.kt ? 0 : 1;
-                float* mine = a.part + ((((cid * 2 + rank) * 2 + slot) * kTcBM) + m) * kPBN;
+                float4* mine = sk_part(a, cid, rank, slot, kPBN);
 #pragma unroll 1
                 for (int c0 = 0; c0 < kPBN; c0 += 16) {
                     uint32_t v[16];
@@ -373,57 +509,38 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                     tc_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 16; i += 4)
-                        *reinterpret_cast<float4*>(mine + c0 + i) =
+                        mine[((c0 + i) / 4) * kTcBM + m] =
                             make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
                                         __uint_as_float(v[i + 3]));
                 }
-                asm volatile("bar.sync 5, 128;" ::: "memory");        // the 4 epilogue warps wrote their rows
-                if (warp == 12 && lane == 0) {
-                    __threadfence();
-                    sk_tick = atomicAdd(&a.tick[p * 2 + rank], 1u);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[b]);               // the MMA may refill it now
+                __threadfence();                                         // this thread's partial is visible GPU-wide
+                asm volatile("bar.sync 5, 128;" ::: "memory");           // the 4 epilogue warps wrote their rows
+                if (warp == 12 && lane == 0) atomicAdd(&a.tick[p * 2 + rank], 1u);
+                if (it < kPtSegs) PT_STAMP(5 + it * 5, globaltimer());
+                if (npend == kSkPending) {                               // (not reached: <= 2 cut tiles per range)
+                    sk_fixup(pend[0], pend_it[0]);
+                    for (int i = 1; i < npend; ++i) { pend[i - 1] = pend[i]; pend_it[i - 1] = pend_it[i]; }
+                    --npend;
                 }
-                asm volatile("bar.sync 5, 128;" ::: "memory");
-                const int64_t ca = sk_owner(a, p * a.kt, nclu), cb = sk_owner(a, (p + 1) * a.kt - 1, nclu);
-                if (static_cast<int64_t>(sk_tick) == cb - ca) {
-                    __threadfence();                              // the other clusters' partials are visible
-#pragma unroll 1
-                    for (int c0 = 0; c0 < kPBN; c0 += 16) {
-                        uint32_t v[16];
-                        tmem_ld_32x32b_x16(col0 + c0, v);
-                        tc_wait_ld();
-                        float acc[16];
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
-                        for (int64_t cc = ca; cc <= cb; ++cc) {
-                            float val[16];
-                            if (cc == cid) {
-#pragma unroll
-                                for (int i = 0; i < 16; ++i) val[i] = __uint_as_float(v[i]);
-                            } else {
-                                const int64_t sl = sk_start(a, cc, nclu) >= p * a.kt ? 0 : 1;
-                                const float* src = a.part + ((((cc * 2 + rank) * 2 + sl) * kTcBM) + m) * kPBN + c0;
-#pragma unroll
-                                for (int i = 0; i < 16; i += 4) {
-                                    const float4 f = __ldcg(reinterpret_cast<const float4*>(src + i));
-                                    val[i] = f.x; val[i + 1] = f.y; val[i + 2] = f.z; val[i + 3] = f.w;
-                                }
-                            }
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) acc[i] = cc == ca ? val[i] : acc[i] + val[i];
-                        }
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const int64_t tok = n0 + c0 + i;
-                            if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(acc[i]));
-                        }
-                    }
-                    if (warp == 12 && lane == 0) a.tick[p * 2 + rank] = 0u;   // zero again for the next call
-                }
+                pend[npend] = p;
+                pend_it[npend] = it;
+                ++npend;
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[b]);
+#endif
         }
+#ifdef RQ4_EXPERIMENTS
+        for (int i = 0; i < npend; ++i) sk_fixup(pend[i], pend_it[i]);
+#endif
+#if RQ4_TRACE
+        uint32_t sm_id;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_id));
+        PT_STAMP(0, static_cast<uint64_t>(sm_id) | (static_cast<uint64_t>(it) << 32));
+#endif
+        PT_STAMP(1, static_cast<uint64_t>(cid));
+        PT_STAMP(kPtWords - 1, globaltimer());
     }
 
     tc_fence_before();
@@ -442,7 +559,7 @@ size_t persist_sk_ws_bytes(int bn) {
 
 template <int BN>
 static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                                const uint16_t* s, uint16_t* y, bool sk, void* ws, bool pdl, cudaStream_t stream) {
+                                const uint16_t* s, uint16_t* y, int mode, void* ws, bool pdl, cudaStream_t stream) {
     using C = PCfg<BN>;
     CUtensorMap mw, ms, mx;
     int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
@@ -463,13 +580,23 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
     a.m_tiles = ((N + kTcBM - 1) / kTcBM + 1) / 2;             // m-tile PAIRS (an odd last one is zero-filled)
     a.tiles = a.m_tiles * ((n + BN - 1) / BN);                  // pair tiles
     const int64_t clusters = num_sms() / 2;
+    const bool sk = mode == 2;
     a.sk = sk ? 1 : 0;
-    a.units = a.tiles * a.kt;
+    // stream-K: the full waves of whole tiles, the rest cut into units
+    a.sk_tile0 = sk ? (a.tiles / clusters) * clusters : 0;
+    if (sk && a.sk_tile0 == a.tiles) a.sk = 0;                 // no partial wave: whole tiles only
+    // every cluster needs a non-empty unit range (the fixup sums the partials
+    // of every cluster between a tile's first and last owner): fold one full
+    // wave into the units when the rest alone has fewer units than clusters
+    if (a.sk && (a.tiles - a.sk_tile0) * a.kt < clusters && a.sk_tile0 >= clusters) a.sk_tile0 -= clusters;
+    a.units = (a.tiles - a.sk_tile0) * a.kt;
     a.tick = static_cast<uint32_t*>(ws);
-    a.part = sk ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes) : nullptr;
-    if (sk && (!ws || a.tiles * 2 > static_cast<int64_t>(kTicketBytes / 4))) return static_cast<int>(cudaErrorInvalidValue);
+    a.trace = RQ4_TRACE ? knob_int("RELAX_Q4_TRACE", 0) : 0;
+    a.part = a.sk ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes) : nullptr;
+    if (a.sk && (!ws || a.tiles * 2 > static_cast<int64_t>(kTicketBytes / 4))) return static_cast<int>(cudaErrorInvalidValue);
     // stream-K keeps every cluster busy (units >= clusters); whole tiles use at most one cluster per tile
-    const int64_t grid_clusters = sk ? (a.units < clusters ? a.units : clusters) : (a.tiles < clusters ? a.tiles : clusters);
+    const int64_t grid_clusters = a.sk ? (a.units < clusters && a.sk_tile0 == 0 ? a.units : clusters)
+                                       : (a.tiles < clusters ? a.tiles : clusters);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * grid_clusters));
     cfg.blockDim = dim3(kPThreads);
@@ -488,15 +615,22 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
 }
 
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, int bn, bool sk, void* ws, bool pdl, cudaStream_t stream) {
+                      uint16_t* y, int bn, int mode, void* ws, bool pdl, cudaStream_t stream) {
     if (K % kTcWStageK != 0 || n <= 0) return static_cast<int>(cudaErrorInvalidValue);
 #ifdef RQ4_EXPERIMENTS
     // BN = 128 tiles: measured slower than both BN = 256 and one tile per CTA at
     // every n (the A transform is re-done per 128 tokens; profiles/r02/sweep_persist_bn_r02.txt)
-    if (bn == 128) return launch_tc_persist_bn<128>(x, n, K, N, w, s, y, sk, ws, pdl, stream);
+    if (bn == 128) return launch_tc_persist_bn<128>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
 #endif
-    if (bn == 256) return launch_tc_persist_bn<256>(x, n, K, N, w, s, y, sk, ws, pdl, stream);
+    if (bn == 256) return launch_tc_persist_bn<256>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 
 }  // namespace rq4
+
+#if RQ4_TRACE
+extern "C" RELAX_API int relax_debug_ptrace_read(void* host, size_t bytes) {
+    const size_t n = sizeof(rq4::g_ptrace) < bytes ? sizeof(rq4::g_ptrace) : bytes;
+    return cudaMemcpyFromSymbol(host, rq4::g_ptrace, n) == cudaSuccess ? RELAX_OK : RELAX_ERR_CUDA;
+}
+#endif

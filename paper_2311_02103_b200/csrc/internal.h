@@ -172,10 +172,10 @@ bool gemv_row_ok(int64_t K);
 int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner,
                 uint64_t outer, uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
                 CUtensorMapSwizzle sw);
-// sk: the stream-K schedule (Plan::persist == 2), reduced through `ws`
-// (persist_sk_ws_bytes; its ticket region zero before and after the call).
+// mode: Plan::persist (1 whole tiles, 2 stream-K reduced through `ws` --
+// persist_sk_ws_bytes, its ticket region zero before and after the call)
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, int bn, bool sk, void* ws, bool pdl, cudaStream_t stream);
+                      uint16_t* y, int bn, int mode, void* ws, bool pdl, cudaStream_t stream);
 size_t persist_sk_ws_bytes(int bn);
 int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                     const uint64_t* dims, const uint64_t* strides, const uint32_t* box,

@@ -1,20 +1,15 @@
 #!/bin/bash
-# Stream-K vs the previous schedule choice (RELAX_Q4_STREAMK=0), experiments build, per shape and n
+# Stream-K of the persistent kernel (experiments build: RELAX_Q4_STREAMK=1, full waves whole + the rest
+# cut into k units, deferred fixups) vs the product's schedules (=0); product parity of the persistent
+# path; a product sweep of the persistent shapes.
 set -u
 O=gpurun_out/sk; mkdir -p $O
-python -m paper_2311_02103_b200.build --experiments > $O/build.log 2>&1 || { echo BUILD_FAIL; exit 1; }
-export RELAX_Q4_LIB=build_exp/librelax_q4_exp.so
-for sk in 0 1; do
-  RELAX_Q4_STREAMK=$sk timeout 900 python tools/sweep.py --shapes 4096x4096,4096x11008,11008x4096,4096x12288,4096x22016,4096x32000 \
-      --ns 256,512,1024,2048,4096 --variants auto --out $O/sweep_sk$sk.jsonl > /dev/null 2>&1
-done
-RELAX_Q4_STREAMK=1 timeout 600 python -m pytest tests/test_gpu_streamk.py -q 2>&1 | tail -2
-python - <<'PY'
+python -m paper_2311_02103_b200.build > $O/build.log 2>&1 || { echo BUILD_FAIL; exit 1; }
+python -m paper_2311_02103_b200.build --experiments > $O/build_exp.log 2>&1 || { echo BUILD_EXP_FAIL; exit 1; }
+RELAX_Q4_LIB=build_exp/librelax_q4_exp.so RELAX_Q4_STREAMK=1 timeout 600 python -m pytest tests/test_gpu_streamk.py -q -x --timeout 300 > $O/pytest_sk.log 2>&1; echo "pytest streamk (exp) rc=$?"; tail -2 $O/pytest_sk.log
+timeout 1500 python -m pytest tests/test_gpu_schedules.py tests/test_gpu_threads.py tests/test_gpu_parity.py tests/test_gpu_large.py tests/test_gpu_streamk.py -q --timeout 900 > $O/pytest_product.log 2>&1; echo "pytest product rc=$?"; tail -2 $O/pytest_product.log
+timeout 900 python tools/sweep.py --shapes 4096x11008,4096x32000,11008x4096,4096x22016 --ns 1024,2048,4096 --variants auto --out $O/sweep_product.jsonl > /dev/null 2>&1; echo "sweep product rc=$?"
+python -c "
 import json
-a={}
-for sk in (0,1):
-    for l in open(f"gpurun_out/sk/sweep_sk{sk}.jsonl"):
-        d=json.loads(l); a.setdefault((d['K'],d['N'],d['n']),{})[sk]=(d['us'],d['TFLOPS'],d['sched'].get('stream_k',False))
-for k,v in sorted(a.items()):
-    print(k, "sk0", v.get(0), "sk1", v.get(1))
-PY
+for l in open('$O/sweep_product.jsonl'):
+    d=json.loads(l); print(d['K'],d['N'],d['n'],d['sched'],d['us'],d['TFLOPS'])"
