@@ -39,23 +39,27 @@ namespace rq4 {
 
 constexpr int kPWStages = 3;
 constexpr int kPASlots = 4;                                               // 64-k A slots
-constexpr int kPXStages = 3;                                              // 64-k x stages
 constexpr uint32_t kPCodes = kTcBM * (kTcWStageK / 2);                    // 16 KB
 constexpr uint32_t kPScales = kTcBM * (kTcWStageK / kGroup) * 2;          // 2 KB
 constexpr uint32_t kPASlotBytes = kTcBM * kTcXStageK * 2;                 // 16 KB
-constexpr uint32_t kPNumBars = 2 * kPWStages + 2 * kPASlots + 2 * kPXStages + 4;
 constexpr int kPThreads = 16 * 32;
 
-// BN = token tile (MMA N): 256 (long prefill) or 128 (more tiles for n ~ 512)
-template <int BN>
+// BN = token tile (MMA N): 256 (long prefill) or 128 (more tiles for n ~ 512).
+// C2: the CTA pair runs ONE M = 256 MMA (tcgen05 cta_group::2): each CTA holds
+// its 128 weight rows of A and its BN/2 tokens of B, so an x stage is half as
+// large and the MMA reads half as much B per CTA (shared-memory bandwidth
+// bounds the cta_group::1 form).
+template <int BN, bool C2>
 struct PCfg {
-    static constexpr uint32_t kXStageBytes = BN * kTcXStageK * 2;          // 32 / 16 KB
+    static constexpr int kXStages = C2 ? 4 : 3;                            // 64-k x stages
+    static constexpr uint32_t kXStageBytes = (C2 ? BN / 2 : BN) * kTcXStageK * 2;   // per CTA
+    static constexpr uint32_t kNumBars = 2 * kPWStages + 2 * kPASlots + 2 * kXStages + 4;
     static constexpr uint32_t kOffCodes = 0;
     static constexpr uint32_t kOffScales = kOffCodes + kPWStages * kPCodes;       // 48 KB
     static constexpr uint32_t kOffA = kOffScales + kPWStages * kPScales + 2048;   // 56 KB (1 KB aligned)
     static constexpr uint32_t kOffX = kOffA + kPASlots * kPASlotBytes;            // 120 KB
-    static constexpr uint32_t kOffBar = kOffX + kPXStages * kXStageBytes;
-    static constexpr uint32_t kSmemBytes = kOffBar + kPNumBars * 8 + 16 + 1024;  // + align slack
+    static constexpr uint32_t kOffBar = kOffX + kXStages * kXStageBytes;
+    static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
     static constexpr uint32_t kTmemCols = 2 * BN;                          // two accumulators
     static_assert(kOffA % 1024 == 0 && kOffX % 1024 == 0, "SW128 operands need 1 KB alignment");
     static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
@@ -171,13 +175,42 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
                  :: "r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
-template <int BN>
+// cta_group::2 forms (C2): the leader CTA issues the pair's MMA; its commits
+// arrive on the same barrier of both CTAs; a TMA load into this CTA's shared
+// memory completes on the LEADER's barrier; arrivals from either CTA go to the
+// leader's barrier.
+__device__ __forceinline__ void tc_mma_ss2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 :: "r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const void* desc, uint32_t leader_bar, int32_t c0,
+                                                int32_t c1, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;"
+        :: "r"(smem_u32(smem_dst)), "l"(desc), "r"(leader_bar), "r"(c0), "r"(c1), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
+                 :: "r"(mapa_shared(smem_u32(bar), 0)) : "memory");
+}
+
+template <int BN, bool C2>
 __global__ void __launch_bounds__(kPThreads, 1)
 tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_s,
                      const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ TpArgs a) {
-    using C = PCfg<BN>;
+    using C = PCfg<BN, C2>;
     constexpr int kPBN = BN;
     constexpr uint32_t kPXStageBytes = C::kXStageBytes;
+    constexpr int kPXStages = C::kXStages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* codes_sm = smem + C::kOffCodes;
@@ -193,7 +226,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     uint64_t* x_empty = x_full + kPXStages;
     uint64_t* acc_full = x_empty + kPXStages;     // [2]
     uint64_t* acc_empty = acc_full + 2;           // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kPNumBars);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
 
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
     const int lane = threadIdx.x & 31;
@@ -207,10 +240,12 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     pdl_launch_dependents();
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPWStages; ++i) { mbar_init(&w_full[i], 1); mbar_init(&w_empty[i], 8); }
-        for (int i = 0; i < kPASlots; ++i) { mbar_init(&a_full[i], 4); mbar_init(&a_empty[i], 1); }
-        // x_empty collects one MMA commit from each CTA of the pair
-        for (int i = 0; i < kPXStages; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 2); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+        // C2: the leader's a_full / acc_empty count the warps of both CTAs;
+        // x_empty gets the pair MMA's one multicast commit (else one commit
+        // from each CTA's MMA)
+        for (int i = 0; i < kPASlots; ++i) { mbar_init(&a_full[i], C2 ? 8 : 4); mbar_init(&a_empty[i], 1); }
+        for (int i = 0; i < kPXStages; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], C2 ? 1 : 2); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], C2 ? 8 : 4); }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -219,8 +254,14 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
         tma_prefetch_desc(&tm_x);
     }
     if (warp == 3) {
-        tmem_alloc<C::kTmemCols>(tmem_slot);
-        tmem_relinquish();
+        if constexpr (C2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                         :: "r"(smem_u32(tmem_slot)), "n"(C::kTmemCols) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            tmem_alloc<C::kTmemCols>(tmem_slot);
+            tmem_relinquish();
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -261,17 +302,24 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                 const int32_t n0 = static_cast<int32_t>((g.p / a.m_tiles) * kPBN + rank * (kPBN / 2));
                 for (int j = g.kb0 * 4; j < g.kb1 * 4; ++j) {
                     mbar_wait(&x_empty[slot], ph ^ 1);                // both CTAs released the slot
-                    mbar_arrive_expect_tx(&x_full[slot], kPXStageBytes);     // own half + the peer's half
-                    tma_load_2d_mc(x_sm + slot * kPXStageBytes + rank * (kPXStageBytes / 2), &tm_x, &x_full[slot],
-                                   j * kTcXStageK, n0, 0x3, pol);
+                    if constexpr (C2) {
+                        // this CTA's BN/2 tokens into its own slot, completing on the leader's barrier
+                        if (rank == 0) mbar_arrive_expect_tx(&x_full[slot], 2 * kPXStageBytes);
+                        tma_load_2d_2sm(x_sm + slot * kPXStageBytes, &tm_x, mapa_shared(smem_u32(&x_full[slot]), 0),
+                                        j * kTcXStageK, n0, pol);
+                    } else {
+                        mbar_arrive_expect_tx(&x_full[slot], kPXStageBytes);     // own half + the peer's half
+                        tma_load_2d_mc(x_sm + slot * kPXStageBytes + rank * (kPXStageBytes / 2), &tm_x,
+                                       &x_full[slot], j * kTcXStageK, n0, 0x3, pol);
+                    }
                     if (++slot == kPXStages) { slot = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
-        if (elect_one()) {
-            constexpr uint32_t idesc = idesc_f16_f32(kTcBM, kPBN);
+        // ---------------- MMA issuer (C2: the leader CTA only, for the pair)
+        if ((!C2 || rank == 0) && elect_one()) {
+            constexpr uint32_t idesc = idesc_f16_f32(C2 ? 2 * kTcBM : kTcBM, kPBN);
             int as = 0, xs = 0;
             uint32_t aph = 0, xph = 0;
             int it = 0;
@@ -289,16 +337,25 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                     tc_fence_after();
                     const uint64_t adesc = smem_desc_k_sw128(smem_u32(a_sm + as * kPASlotBytes));
                     const uint64_t bdesc = smem_desc_k_sw128(smem_u32(x_sm + xs * kPXStageBytes));
+                    if constexpr (C2) {
 #pragma unroll
-                    for (int kk = 0; kk < kTcXStageK / 16; ++kk)
-                        tc_mma_ss(d, adesc + static_cast<uint64_t>(kk * 2), bdesc + static_cast<uint64_t>(kk * 2),
-                                  idesc, (j != j0 || kk != 0) ? 1u : 0u);
-                    tc_commit(&a_empty[as]);
-                    tc_commit_mc(&x_empty[xs], 0x3);                  // release the slot in both CTAs
+                        for (int kk = 0; kk < kTcXStageK / 16; ++kk)
+                            tc_mma_ss2(d, adesc + static_cast<uint64_t>(kk * 2), bdesc + static_cast<uint64_t>(kk * 2),
+                                       idesc, (j != j0 || kk != 0) ? 1u : 0u);
+                        tc_commit2_mc(&a_empty[as]);                  // both CTAs' A slot
+                        tc_commit2_mc(&x_empty[xs]);                  // both CTAs' x slot
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < kTcXStageK / 16; ++kk)
+                            tc_mma_ss(d, adesc + static_cast<uint64_t>(kk * 2), bdesc + static_cast<uint64_t>(kk * 2),
+                                      idesc, (j != j0 || kk != 0) ? 1u : 0u);
+                        tc_commit(&a_empty[as]);
+                        tc_commit_mc(&x_empty[xs], 0x3);              // release the slot in both CTAs
+                    }
                     if (++as == kPASlots) { as = 0; aph ^= 1; }
                     if (++xs == kPXStages) { xs = 0; xph ^= 1; }
                 }
-                tc_commit(&acc_full[b]);
+                if constexpr (C2) tc_commit2_mc(&acc_full[b]); else tc_commit(&acc_full[b]);
             }
         }
     } else if (warp >= 4 && warp < 12) {
@@ -345,7 +402,9 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                         }
                     fence_proxy_async_smem();                     // generic stores -> MMA (async proxy)
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&a_full[as]);
+                    if (lane == 0) {
+                        if constexpr (C2) mbar_arrive_leader(&a_full[as]); else mbar_arrive(&a_full[as]);
+                    }
                     as += 2;
                     if (as >= kPASlots) { as -= kPASlots; aph ^= 1; }
                 }
@@ -488,7 +547,9 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[b]);
+                if (lane == 0) {
+                    if constexpr (C2) mbar_arrive_leader(&acc_empty[b]); else mbar_arrive(&acc_empty[b]);
+                }
                 if (it < kPtSegs) PT_STAMP(7 + it * 5, globaltimer());
             }
 #ifdef RQ4_EXPERIMENTS
@@ -548,7 +609,13 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     cluster_arrive_release();          // the peer may still multicast into / commit onto this CTA
     cluster_wait_acquire();
     tc_fence_after();
-    if (warp == 3) tmem_dealloc<C::kTmemCols>(tmem_base);
+    if (warp == 3) {
+        if constexpr (C2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" :: "r"(tmem_base), "n"(C::kTmemCols)
+                         : "memory");
+        else
+            tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
 }
 
 // Workspace of the stream-K schedule: the ticket region (zero before and after
@@ -557,10 +624,10 @@ size_t persist_sk_ws_bytes(int bn) {
     return kTicketBytes + static_cast<size_t>(num_sms() / 2) * 2 * 2 * kTcBM * bn * 4;
 }
 
-template <int BN>
+template <int BN, bool C2>
 static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
                                 const uint16_t* s, uint16_t* y, int mode, void* ws, bool pdl, cudaStream_t stream) {
-    using C = PCfg<BN>;
+    using C = PCfg<BN, C2>;
     CUtensorMap mw, ms, mx;
     int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
@@ -571,7 +638,7 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
     rc = make_map_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, x, K, n, K * 2, kTcXStageK, BN / 2,
                      CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
-    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_persist_kernel<BN>),
+    const cudaError_t e = ensure_kernel_attrs(reinterpret_cast<const void*>(tc_q4_persist_kernel<BN, C2>),
                                               static_cast<int>(C::kSmemBytes), true);
     if (e != cudaSuccess) return static_cast<int>(e);
     TpArgs a;
@@ -580,7 +647,7 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
     a.m_tiles = ((N + kTcBM - 1) / kTcBM + 1) / 2;             // m-tile PAIRS (an odd last one is zero-filled)
     a.tiles = a.m_tiles * ((n + BN - 1) / BN);                  // pair tiles
     const int64_t clusters = num_sms() / 2;
-    const bool sk = mode == 2;
+    const bool sk = mode == 2 && !C2;
     a.sk = sk ? 1 : 0;
     // stream-K: the full waves of whole tiles, the rest cut into units
     a.sk_tile0 = sk ? (a.tiles / clusters) * clusters : 0;
@@ -611,7 +678,7 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_persist_kernel<BN>, mw, ms, mx, a));
+    return static_cast<int>(cudaLaunchKernelEx(&cfg, tc_q4_persist_kernel<BN, C2>, mw, ms, mx, a));
 }
 
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
@@ -620,9 +687,16 @@ int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
 #ifdef RQ4_EXPERIMENTS
     // BN = 128 tiles: measured slower than both BN = 256 and one tile per CTA at
     // every n (the A transform is re-done per 128 tokens; profiles/r02/sweep_persist_bn_r02.txt)
-    if (bn == 128) return launch_tc_persist_bn<128>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
+    if (bn == 128) return launch_tc_persist_bn<128, false>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
 #endif
-    if (bn == 256) return launch_tc_persist_bn<256>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
+    // the pair MMA (cta_group::2) for whole tiles; stream-K keeps the per-CTA form
+#ifdef RQ4_EXPERIMENTS
+    static const bool c2 = knob_int("RELAX_Q4_PERSIST_C2", 0) != 0;
+#else
+    constexpr bool c2 = false;
+#endif
+    if (bn == 256 && c2 && mode != 2) return launch_tc_persist_bn<256, true>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
+    if (bn == 256) return launch_tc_persist_bn<256, false>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 
