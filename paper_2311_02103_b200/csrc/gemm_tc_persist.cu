@@ -35,10 +35,13 @@
 #include "ptx.cuh"
 #include "q4_unpack.cuh"
 
+#ifndef RQ4_C2_ASLOTS
+#define RQ4_C2_ASLOTS 4
+#endif
+
 namespace rq4 {
 
 constexpr int kPWStages = 3;
-constexpr int kPASlots = 4;                                               // 64-k A slots
 constexpr uint32_t kPCodes = kTcBM * (kTcWStageK / 2);                    // 16 KB
 constexpr uint32_t kPScales = kTcBM * (kTcWStageK / kGroup) * 2;          // 2 KB
 constexpr uint32_t kPASlotBytes = kTcBM * kTcXStageK * 2;                 // 16 KB
@@ -52,12 +55,14 @@ constexpr int kPThreads = 16 * 32;
 template <int BN, bool C2>
 struct PCfg {
     static constexpr int kXStages = C2 ? 4 : 3;                            // 64-k x stages
+    // 64-k A slots (C2: deeper, the leader's MMA waits for both CTAs' transforms)
+    static constexpr int kASlots = C2 ? RQ4_C2_ASLOTS : 4;
     static constexpr uint32_t kXStageBytes = (C2 ? BN / 2 : BN) * kTcXStageK * 2;   // per CTA
-    static constexpr uint32_t kNumBars = 2 * kPWStages + 2 * kPASlots + 2 * kXStages + 4;
+    static constexpr uint32_t kNumBars = 2 * kPWStages + 2 * kASlots + 2 * kXStages + 4;
     static constexpr uint32_t kOffCodes = 0;
     static constexpr uint32_t kOffScales = kOffCodes + kPWStages * kPCodes;       // 48 KB
     static constexpr uint32_t kOffA = kOffScales + kPWStages * kPScales + 2048;   // 56 KB (1 KB aligned)
-    static constexpr uint32_t kOffX = kOffA + kPASlots * kPASlotBytes;            // 120 KB
+    static constexpr uint32_t kOffX = kOffA + kASlots * kPASlotBytes;             // 120 KB (C1)
     static constexpr uint32_t kOffBar = kOffX + kXStages * kXStageBytes;
     static constexpr uint32_t kSmemBytes = kOffBar + kNumBars * 8 + 16 + 1024;  // + align slack
     static constexpr uint32_t kTmemCols = 2 * BN;                          // two accumulators
@@ -211,6 +216,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
     constexpr int kPBN = BN;
     constexpr uint32_t kPXStageBytes = C::kXStageBytes;
     constexpr int kPXStages = C::kXStages;
+    constexpr int kPASlots = C::kASlots;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* codes_sm = smem + C::kOffCodes;

@@ -9,8 +9,8 @@ RELAX_Q4_PERSIST_C2=1 RELAX_Q4_PERSIST_BN=256 timeout 300 python tools/prof_one.
 RELAX_Q4_PERSIST_C2=1 RELAX_Q4_PERSIST_BN=256 timeout 900 python -m pytest tests/test_gpu_schedules.py tests/test_gpu_parity.py -q -x --timeout 300 > $O/pytest_c2_dbg.log 2>&1; echo "pytest c2 (debug) rc=$?"; tail -3 $O/pytest_c2_dbg.log
 python -m paper_2311_02103_b200.build --experiments > $O/build.log 2>&1 || { echo BUILD_FAIL; exit 1; }
 for c2 in 0 1; do
-  RELAX_Q4_PERSIST_C2=$c2 RELAX_Q4_PERSIST_BN=256 timeout 900 python tools/sweep.py --shapes 4096x4096,4096x11008,11008x4096,4096x32000,8192x28672 \
-     --ns 512,1024,2048,4096 --variants auto --out $O/sweep_c2_$c2.jsonl > /dev/null 2>&1; echo "sweep c2=$c2 rc=$?"
+  RELAX_Q4_PERSIST_C2=$c2 RELAX_Q4_PERSIST_BN=256 timeout 900 python tools/sweep.py --shapes ${SHAPES:-4096x4096,4096x11008,11008x4096,4096x32000,8192x28672} \
+     --ns ${NS:-512,1024,2048,4096} --variants auto --out $O/sweep_c2_$c2.jsonl > /dev/null 2>&1; echo "sweep c2=$c2 rc=$?"
 done
 python - <<'PY'
 import json
