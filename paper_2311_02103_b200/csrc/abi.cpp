@@ -114,6 +114,9 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
         bb = 256;
         bp = true;
     }
+    // cost of the DSMEM split-K reduction in the model (experiments: RELAX_Q4_SPLIT_US)
+    static const double split_us = knob_double("RELAX_Q4_SPLIT_US", 1.0);
+    static const double split_short_us = knob_double("RELAX_Q4_SPLIT_SHORT_US", 3.0);
     for (int bn : {128, 256}) {
         const int64_t tiles = tm * ((n + bn - 1) / bn);
         const double step = bn == 256 ? 1.3 : 0.92;
@@ -123,7 +126,13 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
             if (s > 1 && tiles > cluster_capacity(bn, s)) continue;   // clusters would not all be resident
             const int64_t waves = (tiles * s + sms - 1) / sms;
             const int ks = (kt + s - 1) / s;
-            const double t = static_cast<double>(waves) * (ks * step + fixed) + (s > 1 ? 1.0 : 0.0);
+            // a split that leaves <= 2 stages per CTA pays its cluster reduction
+            // unamortised once the unsplit grid already has >= 64 tiles (1024 x 8192
+            // at n = 65..128: s = 2 8.2 us vs s = 1 6.8 us); with fewer tiles the
+            // extra CTAs still win (1024 x 1024 n = 65: s = 4 5.2 vs s = 1 6.7 us;
+            // profiles/r02/split_short_k_r02.txt)
+            const double t = static_cast<double>(waves) * (ks * step + fixed) +
+                             (s > 1 ? (ks <= 2 && tiles >= 64 ? split_short_us : split_us) : 0.0);
             if (t < best * 0.999) { best = t; bb = bn; bs = s; bp = false; }
         }
     }
