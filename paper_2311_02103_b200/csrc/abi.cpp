@@ -67,11 +67,23 @@ static int64_t cluster_capacity(int bn, int s) {
     return sms == kB200SMs ? v : v * sms / kB200SMs;
 }
 
-static int choose_bn(int64_t n, int64_t N) {
-    (void)N;
+static int choose_bn(int64_t n, int64_t K, int64_t N) {
     if (n <= 16) return 16;
     if (n <= 32) return 32;
-    if (n <= 64) return 64;
+    if (n <= 64) {
+        // 33..64 tokens, from the measured sweep (profiles/r02/bn_n33_64_r02.txt;
+        // each BN with its automatic split): one 128-token tile for narrow
+        // outputs at long K or 28..40 m-tiles at K >= 4096 (4096^2 10.1 -> 9.5 us,
+        // 11008 x 4096 17.0 -> 15.5, 28672 x 2048 26.9 -> 21.6), two 32-token
+        // tiles for narrow outputs at K >= 8192 (8192 x 1024 9.0 -> 7.4,
+        // 14336 x 2048 15.4 -> 13.6), else 64-token tiles at two CTAs per SM
+        // (28672 x 6144: 44.4 vs 51.4 us with 128)
+        const int64_t tm = (N + kTcBM - 1) / kTcBM;
+        if (K >= 16384 && tm <= 16) return 128;
+        if (K >= 4096 && tm >= 28 && tm <= 40) return 128;
+        if (K >= 8192 && tm <= 16) return 32;
+        return 64;
+    }
     return 128;                  // n > 64: refined jointly with the split (choose_tc_large)
 }
 
@@ -233,7 +245,7 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
             choose_tc_large(n, N, kt, &p.bn, &auto_split, &persist, !no_persist && persist_enabled(), allow_sk);
             p.persist = persist;
         } else {
-            p.bn = choose_bn(n, N);
+            p.bn = choose_bn(n, K, N);
         }
         const int64_t tiles = ((N + kTcBM - 1) / kTcBM) * ((n + p.bn - 1) / p.bn);
         int s = force_split > 0 ? force_split
