@@ -112,7 +112,11 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
         *persist_out = 1;
         return;
     }
-    if (allow_persist && tm * ((n + 255) / 256) >= min_per_sm * sms) {
+    // long K (experiments: RELAX_Q4_PERSIST_MAX_KT): the persistent kernel's SS-form
+    // stage is slower than the one-tile kernel's TS form, which its fill/drain
+    // saving no longer covers
+    static const int persist_max_kt = knob_int("RELAX_Q4_PERSIST_MAX_KT", 24);
+    if (allow_persist && kt <= persist_max_kt && tm * ((n + 255) / 256) >= min_per_sm * sms) {
         // persistent BN = 256 tiles (gemm_tc_persist.cu): the epilogue of a
         // tile overlaps the next tile's k-loop, so the fill/drain is paid once
         // per CTA, not per tile.  Measured (profiles/r02/sweep_persist_r02.jsonl):
@@ -129,15 +133,21 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
     // cost of the DSMEM split-K reduction in the model (experiments: RELAX_Q4_SPLIT_US)
     static const double split_us = knob_double("RELAX_Q4_SPLIT_US", 1.0);
     static const double split_short_us = knob_double("RELAX_Q4_SPLIT_SHORT_US", 3.0);
+    static const int mw_min_ks = knob_int("RELAX_Q4_MW_SPLIT_MIN_KS", 16);
     for (int bn : {128, 256}) {
         const int64_t tiles = tm * ((n + bn - 1) / bn);
         const double step = bn == 256 ? 1.3 : 0.92;
         const double fixed = bn == 256 ? 8.0 : 5.7;
         for (int s = 1; s <= 8 && s <= kt; ++s) {
-            if (s > 1 && (tiles > kMaxSplitTiles || tiles * s > sms)) break;
-            if (s > 1 && tiles > cluster_capacity(bn, s)) continue;   // clusters would not all be resident
-            const int64_t waves = (tiles * s + sms - 1) / sms;
             const int ks = (kt + s - 1) / s;
+            // several waves of split-K clusters: only 256-token tiles that keep
+            // >= mw_min_ks stages per CTA (experiments: RELAX_Q4_MW_SPLIT_MIN_KS)
+            const bool multi = bn == 256 && mw_min_ks > 0 && ks >= mw_min_ks && s <= 2;
+            if (s > 1 && tiles > kMaxSplitTiles) break;
+            if (s > 1 && !multi && tiles * s > sms) break;
+            if (s > 1 && !multi && tiles > cluster_capacity(bn, s)) continue;   // clusters would not all be resident
+            const int64_t cap = s > 1 ? cluster_capacity(bn, s) : sms;
+            const int64_t waves = s > 1 ? (tiles + cap - 1) / cap : (tiles + sms - 1) / sms;
             // a split that leaves <= 2 stages per CTA pays its cluster reduction
             // unamortised once the unsplit grid already has >= 64 tiles (1024 x 8192
             // at n = 65..128: s = 2 8.2 us vs s = 1 6.8 us); with fewer tiles the
@@ -145,7 +155,10 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
             // profiles/r02/split_short_k_r02.txt)
             const double t = static_cast<double>(waves) * (ks * step + fixed) +
                              (s > 1 ? (ks <= 2 && tiles >= 64 ? split_short_us : split_us) : 0.0);
-            if (t < best * 0.999) { best = t; bb = bn; bs = s; bp = false; }
+            // several waves of split clusters must win by 10% in the model: at a
+            // smaller margin they measured up to 6% slower (profiles/r02/long_k_r02.txt)
+            const double margin = s > 1 && tiles * s > sms ? 0.9 : 0.999;
+            if (t < best * margin) { best = t; bb = bn; bs = s; bp = false; }
         }
     }
     int bpk = bp ? 1 : 0;
