@@ -28,6 +28,12 @@
 // TMEM: 2 x 256 fp32 columns (all 512); A lives in SMEM (4 x 16 KB slots),
 // which is what frees the second accumulator.  PDL: weights stream before
 // griddepcontrol.wait; x loads and y stores wait.
+//
+// Experiments build only (measured slower): the stream-K
+// schedule (TpArgs::sk; full waves whole, the rest cut into k units reduced
+// through the workspace with deferred column-slice fixups) and the pair-MMA
+// form (C2: one tcgen05.mma.cta_group::2, M = 256, per k-step for the CTA
+// pair).  The product dispatch offers this kernel up to 24 k-stages (abi.cpp).
 #include <cstdio>
 #include "internal.h"
 #include "knobs.h"
