@@ -704,10 +704,8 @@ int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const 
     // the pair MMA (cta_group::2) for whole tiles; stream-K keeps the per-CTA form
 #ifdef RQ4_EXPERIMENTS
     static const bool c2 = knob_int("RELAX_Q4_PERSIST_C2", 0) != 0;
-#else
-    constexpr bool c2 = false;
-#endif
     if (bn == 256 && c2 && mode != 2) return launch_tc_persist_bn<256, true>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
+#endif
     if (bn == 256) return launch_tc_persist_bn<256, false>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
     return static_cast<int>(cudaErrorInvalidValue);
 }
