@@ -98,7 +98,9 @@ static int choose_bn(int64_t n, int64_t K, int64_t N) {
 // tiles * s <= 148.  The model only ranks schedules; results never depend on
 // it (every BN/split meets the same tolerance).
 static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out, int* persist_out,
-                            bool allow_persist, bool allow_sk) {
+                            bool allow_persist, bool allow_sk, int64_t* rows_a_out, int* split_b_out) {
+    *rows_a_out = 0;
+    *split_b_out = 1;
     const int64_t tm = (N + kTcBM - 1) / kTcBM;
     const int64_t sms = num_sms();
     double best = 1e300;
@@ -191,6 +193,36 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
             if (t < best * 0.9) { bb = 256; bs = 1; bpk = 2; }
         }
     }
+    // Two-part schedule: when whole 256-token tiles leave a partial last wave,
+    // run the full waves as whole tiles over the leading rows and the rest
+    // rows as split-K clusters in a second launch (both existing kernels; the
+    // rest costs ceil(kt / s) stages instead of kt).  Offered with a 10%
+    // margin over the model's best.
+#ifdef RQ4_EXPERIMENTS
+    static const int two_part = knob_int("RELAX_Q4_TWO_PART", 1);
+#else
+    const int two_part = 1;
+#endif
+    {
+        const int64_t tt = (n + 255) / 256;
+        const int64_t full = tm * tt / sms;
+        if (two_part && full >= 1 && tm * tt % sms != 0) {
+            const int64_t ma = full * sms / tt;                   // m-tiles of the whole-tile part
+            const int64_t tiles_b = (tm - ma) * tt;
+            int sb = 0;
+            for (int s = 8; s >= 2; --s)
+                if ((kt + s - 1) / s >= 2 && tiles_b * s <= sms && tiles_b <= cluster_capacity(256, s)) { sb = s; break; }
+            if (ma > 0 && tiles_b > 0 && sb > 1) {
+                const double ta = static_cast<double>((ma * tt + sms - 1) / sms) * (kt * 1.3 + 8.0);
+                const double tb = static_cast<double>((kt + sb - 1) / sb) * 1.3 + 8.0 + split_us;
+                if (ta + tb < best * 0.9) {
+                    best = ta + tb; bb = 256; bs = 1; bpk = 0;
+                    *rows_a_out = ma * kTcBM;
+                    *split_b_out = sb;
+                }
+            }
+        }
+    }
     *bn_out = bb;
     *s_out = bs;
     *persist_out = bpk;
@@ -255,7 +287,8 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
             p.bn = force_bn;
         } else if (n > 64 && force_split <= 0) {
             int persist = 0;
-            choose_tc_large(n, N, kt, &p.bn, &auto_split, &persist, !no_persist && persist_enabled(), allow_sk);
+            choose_tc_large(n, N, kt, &p.bn, &auto_split, &persist, !no_persist && persist_enabled(), allow_sk,
+                            &p.rows_a, &p.split_b);
             p.persist = persist;
         } else {
             p.bn = choose_bn(n, K, N);
@@ -380,7 +413,22 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
     else if (plan.variant == kVariantSmallN)
         e = launch_smalln_mma(static_cast<const uint16_t*>(x), n, K, N, packed_w,
                               static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), pdl, st);
-    else
+    else if (plan.rows_a > 0) {
+        // two-part schedule: the full waves of whole 256-token tiles over rows
+        // [0, rows_a), then the remaining rows as split-K clusters (a second
+        // launch: its CTAs take the SMs the first one frees, under PDL)
+        Plan pa = plan, pb = plan;
+        pa.rows_a = pb.rows_a = 0;
+        pa.split = 1; pa.cluster = 0;
+        pb.split = plan.split_b; pb.cluster = 1;
+        const uint16_t* sc = static_cast<const uint16_t*>(scales);
+        uint16_t* yo = static_cast<uint16_t*>(y);
+        e = launch_tc(static_cast<const uint16_t*>(x), n, K, plan.rows_a, packed_w, sc, yo, pa, nullptr, pdl, st,
+                      Fusion(), N);
+        if (e == 0)
+            e = launch_tc(static_cast<const uint16_t*>(x), n, K, N - plan.rows_a, packed_w + plan.rows_a * (K / 8),
+                          sc + plan.rows_a * (K / kGroup), yo + plan.rows_a, pb, nullptr, true, st, Fusion(), N);
+    } else
         e = launch_tc(static_cast<const uint16_t*>(x), n, K, N, packed_w,
                       static_cast<const uint16_t*>(scales), static_cast<uint16_t*>(y), plan, ws, pdl, st);
     if (e != 0) {
@@ -590,7 +638,7 @@ int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* til
     if (tile) *tile = (p.variant == rq4::kVariantGemv || p.variant == rq4::kVariantSmallN) ? p.nt : p.bn;
     if (split_k) *split_k = p.split;
     if (ws_bytes) *ws_bytes = p.ws_bytes;
-    if (persistent) *persistent = p.persist;
+    if (persistent) *persistent = p.rows_a > 0 ? 3 : p.persist;
     return RELAX_OK;
 }
 

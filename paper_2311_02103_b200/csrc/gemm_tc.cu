@@ -88,6 +88,7 @@ struct TcArgs {
     const uint16_t* res;  // RESIDUAL: fp16 [n][Nout]
     int64_t Nout;         // N/2 with SILU_MUL, else N (row stride of y)
     int ytma;             // 1: tm_y is valid (N % 8 == 0) and the FU = 0 epilogue stores by TMA
+    int64_t ldy;          // FU = 0: row stride of y (N, or the full width when this launch is a row range)
 };
 
 // Final store of output element (tok, row) with value f (fp32 sum) under the
@@ -98,7 +99,7 @@ template <int FU>
 __device__ __forceinline__ void tc_store(const TcArgs& a, unsigned mask, int64_t tok, int64_t row, float f,
                                          bool valid) {
     if (!FU) {                          // plain matmul: the unfused store, nothing else compiled
-        if (valid) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(f));
+        if (valid) a.y[tok * a.ldy + row] = __half_as_ushort(__float2half_rn(f));
         return;
     }
     if (a.ops & RELAX_OP_SILU_MUL) {
@@ -129,12 +130,12 @@ __device__ __forceinline__ void tc_store4(const TcArgs& a, int64_t tok, int64_t 
         }
         return;
     }
-    if (!FU && rr + 3 < a.N && ((tok * a.N + rr) & 3) == 0) {      // one 8-B store
+    if (!FU && rr + 3 < a.N && ((tok * a.ldy + rr) & 3) == 0) {    // one 8-B store
         const uint32_t lo = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[0]))) |
                             (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[1]))) << 16);
         const uint32_t hi = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[2]))) |
                             (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(f[3]))) << 16);
-        *reinterpret_cast<uint2*>(a.y + tok * a.N + rr) = make_uint2(lo, hi);
+        *reinterpret_cast<uint2*>(a.y + tok * a.ldy + rr) = make_uint2(lo, hi);
         return;
     }
 #pragma unroll
@@ -144,7 +145,7 @@ __device__ __forceinline__ void tc_store4(const TcArgs& a, int64_t tok, int64_t 
                 const int64_t idx = tok * a.Nout + rr + j;
                 a.y[idx] = epilogue_value(__half_as_ushort(__float2half_rn(f[j])), a.ops, a.res, idx);
             } else {
-                a.y[tok * a.N + rr + j] = __half_as_ushort(__float2half_rn(f[j]));
+                a.y[tok * a.ldy + rr + j] = __half_as_ushort(__float2half_rn(f[j]));
             }
         }
     }
@@ -724,7 +725,7 @@ static int launch_tc_k(const CUtensorMap& mw, const CUtensorMap& ms, const uint1
     // (the FU = 0 direct epilogue stores whole tiles through it)
     CUtensorMap my = mx;                 // placeholder when unused (ytma = 0)
     if (a.ytma) {
-        rc = make_map_2d(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.y, a.N, a.n, a.N * 2, kTcBM, BN,
+        rc = make_map_2d(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.y, a.N, a.n, a.ldy * 2, kTcBM, BN,
                          CU_TENSOR_MAP_SWIZZLE_NONE);
         if (rc) return rc;
     }
@@ -816,7 +817,7 @@ size_t tc_workspace_bytes(int64_t n, int64_t N, int bn, int split) {
 
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
               const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
-              cudaStream_t stream, const Fusion& fu) {
+              cudaStream_t stream, const Fusion& fu, int64_t ldy) {
     CUtensorMap mw, ms;
     int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
                          CU_TENSOR_MAP_SWIZZLE_128B);
@@ -833,7 +834,9 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.ops = fu.ops & (RELAX_OP_SILU_MUL | RELAX_OP_RESIDUAL);
     a.res = fu.res;
     a.Nout = (fu.ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
-    a.ytma = (a.ops == 0 && plan.split == 1 && N % 8 == 0) ? 1 : 0;
+    a.ldy = ldy > 0 ? ldy : N;
+    if (a.ldy != N && (a.ops != 0 || plan.persist)) return static_cast<int>(cudaErrorInvalidValue);
+    a.ytma = (a.ops == 0 && plan.split == 1 && N % 8 == 0 && a.ldy % 8 == 0) ? 1 : 0;
     static const int tr = RQ4_TRACE ? knob_int("RELAX_Q4_TRACE", 0) : 0;
     a.trace = tr;
     if (plan.split > 1 && !plan.cluster) {

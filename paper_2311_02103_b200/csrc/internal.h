@@ -84,6 +84,8 @@ struct Plan {
     int cluster = 0;     // TC: split-K reduced in a thread-block cluster (DSMEM), no workspace
     int persist = 0;     // TC: persistent kernel, double-buffered accumulator (BN = 128 / 256, no split);
                          // 2 = its stream-K schedule (k ranges split over clusters, workspace reduction)
+    int64_t rows_a = 0;  // TC two-part schedule (> 0): rows [0, rows_a) as whole 256-token tiles, the
+    int split_b = 1;     // rest rows [rows_a, N) in a second launch with split-K split_b (cluster)
     int grid = 0;
     size_t ws_bytes = 0; // workspace bytes this plan needs
 };
@@ -180,9 +182,10 @@ size_t persist_sk_ws_bytes(int bn);
 int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                     const uint64_t* dims, const uint64_t* strides, const uint32_t* box,
                     CUtensorMapSwizzle sw);
+// ldy: row stride of y for a plain matmul over a range of output rows (0: N)
 int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
               const uint16_t* s, uint16_t* y, const Plan& plan, void* ws, bool pdl,
               cudaStream_t stream,
-              const Fusion& fu = Fusion());
+              const Fusion& fu = Fusion(), int64_t ldy = 0);
 
 }  // namespace rq4

@@ -178,6 +178,9 @@ def query_schedule(n: int, K: int, N: int) -> dict:
         d["persistent"] = True
     if pe.value == 2:
         d["stream_k"] = True
+    if pe.value == 3:                      # whole tiles over the leading rows + a split-K launch for the rest
+        del d["persistent"]
+        d["two_part"] = True
     return d
 
 

@@ -59,7 +59,8 @@ def schedule_classes(K, N, n_max=N_MAX):
     cls = {}
     for n in range(1, n_max + 1):
         s = ops.query_schedule(n, K, N)
-        key = (s["variant"], s["tile"], s["split_k"], s.get("persistent", False), s.get("stream_k", False))
+        key = (s["variant"], s["tile"], s["split_k"], s.get("persistent", False), s.get("stream_k", False),
+               s.get("two_part", False))
         if key not in cls:
             cls[key] = [n, n]
         cls[key][1] = n
