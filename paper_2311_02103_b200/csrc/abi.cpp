@@ -196,13 +196,15 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
     // Two-part schedule: when whole 256-token tiles leave a partial last wave,
     // run the full waves as whole tiles over the leading rows and the rest
     // rows as split-K clusters in a second launch (both existing kernels; the
-    // rest costs ceil(kt / s) stages instead of kt).  Offered with a 10%
-    // margin over the model's best.
+    // rest costs ceil(kt / s) stages instead of kt).  Offered with a 3%
+    // margin over the model's best (every point offered at that margin measured
+    // 1-33% faster, profiles/r02/two_part_r02.txt).
 #ifdef RQ4_EXPERIMENTS
     static const int two_part = knob_int("RELAX_Q4_TWO_PART", 1);
 #else
     const int two_part = 1;
 #endif
+    static const double tp_margin = knob_double("RELAX_Q4_TWO_PART_MARGIN", 0.97);
     {
         const int64_t tt = (n + 255) / 256;
         const int64_t full = tm * tt / sms;
@@ -215,7 +217,7 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
             if (ma > 0 && tiles_b > 0 && sb > 1) {
                 const double ta = static_cast<double>((ma * tt + sms - 1) / sms) * (kt * 1.3 + 8.0);
                 const double tb = static_cast<double>((kt + sb - 1) / sb) * 1.3 + 8.0 + split_us;
-                if (ta + tb < best * 0.9) {
+                if (ta + tb < best * tp_margin) {
                     best = ta + tb; bb = 256; bs = 1; bpk = 0;
                     *rows_a_out = ma * kTcBM;
                     *split_b_out = sb;
