@@ -307,7 +307,8 @@ RELAX_API int relax_q4_matmul_fused(const void* x, int64_t n, int64_t K, int64_t
  * workspace holds it, else the call falls back to another schedule), 3 for
  * the two-part schedule (the full waves of whole 256-token tiles over the
  * leading output rows, the remaining rows in a second launch as split-K
- * clusters; no workspace).
+ * clusters; no workspace), 4 for the same with the leading rows on the
+ * persistent kernel.
  * Errors: RELAX_ERR_INVALID_ARG, RELAX_ERR_UNSUPPORTED_SHAPE. */
 RELAX_API int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* tile,
                          int* split_k, size_t* ws_bytes, int* persistent);

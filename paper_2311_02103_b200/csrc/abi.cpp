@@ -98,9 +98,11 @@ static int choose_bn(int64_t n, int64_t K, int64_t N) {
 // tiles * s <= 148.  The model only ranks schedules; results never depend on
 // it (every BN/split meets the same tolerance).
 static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_out, int* persist_out,
-                            bool allow_persist, bool allow_sk, int64_t* rows_a_out, int* split_b_out) {
+                            bool allow_persist, bool allow_sk, int64_t* rows_a_out, int* split_b_out,
+                            int* persist_a_out) {
     *rows_a_out = 0;
     *split_b_out = 1;
+    *persist_a_out = 0;
     const int64_t tm = (N + kTcBM - 1) / kTcBM;
     const int64_t sms = num_sms();
     double best = 1e300;
@@ -221,6 +223,28 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
                     best = ta + tb; bb = 256; bs = 1; bpk = 0;
                     *rows_a_out = ma * kTcBM;
                     *split_b_out = sb;
+                    *persist_a_out = 0;
+                }
+            }
+        }
+        // the same with the leading rows on the persistent kernel (whole rounds
+        // of pair tiles over 256-row m-pairs), where that kernel is offered
+        const int64_t pm = (tm + 1) / 2, nclu = sms / 2;
+        const int64_t full_r = pm * tt / nclu;
+        if (two_part == 1 && allow_persist && kt <= persist_max_kt && full_r >= 1 && pm * tt % nclu != 0) {
+            const int64_t map = full_r * nclu / tt;               // m-pairs of the persistent part
+            const int64_t tiles_b = (tm - 2 * map) * tt;
+            int sb = 0;
+            for (int s = 8; s >= 2; --s)
+                if ((kt + s - 1) / s >= 2 && tiles_b * s <= sms && tiles_b <= cluster_capacity(256, s)) { sb = s; break; }
+            if (map > 0 && tiles_b > 0 && sb > 1 && map * tt * 2 >= min_per_sm * sms) {
+                const double ta = static_cast<double>((map * tt + nclu - 1) / nclu) * kt * kPersistStepUs + kPersistFixedUs;
+                const double tb = static_cast<double>((kt + sb - 1) / sb) * 1.3 + 8.0 + split_us;
+                if (ta + tb < best * tp_margin) {
+                    best = ta + tb; bb = 256; bs = 1; bpk = 0;
+                    *rows_a_out = map * 2 * kTcBM;
+                    *split_b_out = sb;
+                    *persist_a_out = 1;
                 }
             }
         }
@@ -290,7 +314,7 @@ int make_plan(int64_t n, int64_t K, int64_t N, int force_variant, int force_spli
         } else if (n > 64 && force_split <= 0) {
             int persist = 0;
             choose_tc_large(n, N, kt, &p.bn, &auto_split, &persist, !no_persist && persist_enabled(), allow_sk,
-                            &p.rows_a, &p.split_b);
+                            &p.rows_a, &p.split_b, &p.persist_a);
             p.persist = persist;
         } else {
             p.bn = choose_bn(n, K, N);
@@ -422,6 +446,7 @@ static int matmul_impl(const void* x, int64_t n, int64_t K, int64_t N, const uin
         Plan pa = plan, pb = plan;
         pa.rows_a = pb.rows_a = 0;
         pa.split = 1; pa.cluster = 0;
+        pa.persist = plan.persist_a; pb.persist = 0;
         pb.split = plan.split_b; pb.cluster = 1;
         const uint16_t* sc = static_cast<const uint16_t*>(scales);
         uint16_t* yo = static_cast<uint16_t*>(y);
@@ -640,7 +665,7 @@ int relax_query_schedule(int64_t n, int64_t K, int64_t N, int* variant, int* til
     if (tile) *tile = (p.variant == rq4::kVariantGemv || p.variant == rq4::kVariantSmallN) ? p.nt : p.bn;
     if (split_k) *split_k = p.split;
     if (ws_bytes) *ws_bytes = p.ws_bytes;
-    if (persistent) *persistent = p.rows_a > 0 ? 3 : p.persist;
+    if (persistent) *persistent = p.rows_a > 0 ? (p.persist_a ? 4 : 3) : p.persist;
     return RELAX_OK;
 }
 

@@ -835,7 +835,7 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
     a.res = fu.res;
     a.Nout = (fu.ops & RELAX_OP_SILU_MUL) ? N / 2 : N;
     a.ldy = ldy > 0 ? ldy : N;
-    if (a.ldy != N && (a.ops != 0 || plan.persist)) return static_cast<int>(cudaErrorInvalidValue);
+    if (a.ldy != N && a.ops != 0) return static_cast<int>(cudaErrorInvalidValue);
     a.ytma = (a.ops == 0 && plan.split == 1 && N % 8 == 0 && a.ldy % 8 == 0) ? 1 : 0;
     static const int tr = RQ4_TRACE ? knob_int("RELAX_Q4_TRACE", 0) : 0;
     a.trace = tr;
@@ -843,7 +843,8 @@ int launch_tc(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t
         a.cnt = static_cast<uint32_t*>(ws);
         a.part = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kTicketBytes);
     }
-    if (plan.persist && a.ops == 0) return launch_tc_persist(x, n, K, N, w, s, y, plan.bn, plan.persist, ws, pdl, stream);
+    if (plan.persist && a.ops == 0)
+        return launch_tc_persist(x, n, K, N, w, s, y, plan.bn, plan.persist, ws, pdl, stream, a.ldy);
     switch (plan.bn) {
         case 16: return launch_tc_bn<16>(mw, ms, x, a, pdl, stream);
         case 32: return launch_tc_bn<32>(mw, ms, x, a, pdl, stream);

@@ -94,6 +94,7 @@ struct TpArgs {
     float* part;              // [cluster][rank][slot 0/1][BN/4][128 rows][4] fp32
     uint32_t* tick;           // [pair tile][rank], zero before and after every call
     int trace;                // experiments build: per-CTA segment timeline
+    int64_t ldy;              // row stride of y (N, or the full width for a row range)
 };
 
 // Experiments build (RELAX_Q4_TRACE=1): per CTA {smid, segments, t_setup,
@@ -499,7 +500,7 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
                             for (int i = 0; i < 4; ++i) {
                                 const int64_t tok = n0 + 4 * jl + i;
                                 if (row_ok && tok < a.n)
-                                    a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(o[i]));
+                                    a.y[tok * a.ldy + row] = __half_as_ushort(__float2half_rn(o[i]));
                             }
                         }
                         if (++cl == P) { cl = 0; ++jl; }
@@ -546,14 +547,14 @@ tc_q4_persist_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_cons
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const int64_t tok = n0 + c0 + i;
-                        if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v0[i])));
+                        if (row_ok && tok < a.n) a.y[tok * a.ldy + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v0[i])));
                     }
                     tc_wait_ld();
                     if (c0 + 32 < kPBN) tmem_ld_32x32b_x16(col0 + c0 + 32, v0);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const int64_t tok = n0 + c0 + 16 + i;
-                        if (row_ok && tok < a.n) a.y[tok * a.N + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v1[i])));
+                        if (row_ok && tok < a.n) a.y[tok * a.ldy + row] = __half_as_ushort(__float2half_rn(__uint_as_float(v1[i])));
                     }
                     tc_wait_ld();
                 }
@@ -638,7 +639,8 @@ size_t persist_sk_ws_bytes(int bn) {
 
 template <int BN, bool C2>
 static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w,
-                                const uint16_t* s, uint16_t* y, int mode, void* ws, bool pdl, cudaStream_t stream) {
+                                const uint16_t* s, uint16_t* y, int mode, void* ws, bool pdl, cudaStream_t stream,
+                                int64_t ldy) {
     using C = PCfg<BN, C2>;
     CUtensorMap mw, ms, mx;
     int rc = make_map_2d(&mw, CU_TENSOR_MAP_DATA_TYPE_UINT8, w, K / 2, N, K / 2, kTcWStageK / 2, kTcBM,
@@ -655,6 +657,7 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
     if (e != cudaSuccess) return static_cast<int>(e);
     TpArgs a;
     a.n = n; a.K = K; a.N = N; a.y = y;
+    a.ldy = ldy > 0 ? ldy : N;
     a.kt = static_cast<int>(K / kTcWStageK);
     a.m_tiles = ((N + kTcBM - 1) / kTcBM + 1) / 2;             // m-tile PAIRS (an odd last one is zero-filled)
     a.tiles = a.m_tiles * ((n + BN - 1) / BN);                  // pair tiles
@@ -694,19 +697,19 @@ static int launch_tc_persist_bn(const uint16_t* x, int64_t n, int64_t K, int64_t
 }
 
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, int bn, int mode, void* ws, bool pdl, cudaStream_t stream) {
+                      uint16_t* y, int bn, int mode, void* ws, bool pdl, cudaStream_t stream, int64_t ldy) {
     if (K % kTcWStageK != 0 || n <= 0) return static_cast<int>(cudaErrorInvalidValue);
 #ifdef RQ4_EXPERIMENTS
     // BN = 128 tiles: measured slower than both BN = 256 and one tile per CTA at
     // every n (the A transform is re-done per 128 tokens; profiles/r02/sweep_persist_bn_r02.txt)
-    if (bn == 128) return launch_tc_persist_bn<128, false>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
+    if (bn == 128) return launch_tc_persist_bn<128, false>(x, n, K, N, w, s, y, mode, ws, pdl, stream, ldy);
 #endif
     // the pair MMA (cta_group::2) for whole tiles; stream-K keeps the per-CTA form
 #ifdef RQ4_EXPERIMENTS
     static const bool c2 = knob_int("RELAX_Q4_PERSIST_C2", 0) != 0;
-    if (bn == 256 && c2 && mode != 2) return launch_tc_persist_bn<256, true>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
+    if (bn == 256 && c2 && mode != 2) return launch_tc_persist_bn<256, true>(x, n, K, N, w, s, y, mode, ws, pdl, stream, ldy);
 #endif
-    if (bn == 256) return launch_tc_persist_bn<256, false>(x, n, K, N, w, s, y, mode, ws, pdl, stream);
+    if (bn == 256) return launch_tc_persist_bn<256, false>(x, n, K, N, w, s, y, mode, ws, pdl, stream, ldy);
     return static_cast<int>(cudaErrorInvalidValue);
 }
 

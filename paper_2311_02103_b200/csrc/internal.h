@@ -86,6 +86,7 @@ struct Plan {
                          // 2 = its stream-K schedule (k ranges split over clusters, workspace reduction)
     int64_t rows_a = 0;  // TC two-part schedule (> 0): rows [0, rows_a) as whole 256-token tiles, the
     int split_b = 1;     // rest rows [rows_a, N) in a second launch with split-K split_b (cluster)
+    int persist_a = 0;   // two-part: the leading rows on the persistent kernel (1) or as one tile per CTA (0)
     int grid = 0;
     size_t ws_bytes = 0; // workspace bytes this plan needs
 };
@@ -177,7 +178,7 @@ int make_map_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64
 // mode: Plan::persist (1 whole tiles, 2 stream-K reduced through `ws` --
 // persist_sk_ws_bytes, its ticket region zero before and after the call)
 int launch_tc_persist(const uint16_t* x, int64_t n, int64_t K, int64_t N, const uint32_t* w, const uint16_t* s,
-                      uint16_t* y, int bn, int mode, void* ws, bool pdl, cudaStream_t stream);
+                      uint16_t* y, int bn, int mode, void* ws, bool pdl, cudaStream_t stream, int64_t ldy = 0);
 size_t persist_sk_ws_bytes(int bn);
 int make_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                     const uint64_t* dims, const uint64_t* strides, const uint32_t* box,

@@ -178,9 +178,11 @@ def query_schedule(n: int, K: int, N: int) -> dict:
         d["persistent"] = True
     if pe.value == 2:
         d["stream_k"] = True
-    if pe.value == 3:                      # whole tiles over the leading rows + a split-K launch for the rest
+    if pe.value in (3, 4):                 # whole tiles over the leading rows + a split-K launch for the rest
         del d["persistent"]
         d["two_part"] = True
+        if pe.value == 4:                  # the leading rows on the persistent kernel
+            d["two_part_persistent"] = True
     return d
 
 

@@ -60,7 +60,7 @@ def schedule_classes(K, N, n_max=N_MAX):
     for n in range(1, n_max + 1):
         s = ops.query_schedule(n, K, N)
         key = (s["variant"], s["tile"], s["split_k"], s.get("persistent", False), s.get("stream_k", False),
-               s.get("two_part", False))
+               s.get("two_part", False), s.get("two_part_persistent", False))
         if key not in cls:
             cls[key] = [n, n]
         cls[key][1] = n

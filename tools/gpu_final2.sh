@@ -1,7 +1,7 @@
 #!/bin/bash
 # End-of-round re-check on the final code: build, smoke, pytest -m gpu, bench lines (decode, prefill, 70B prefill)
 set -u
-O=gpurun_out/fin; mkdir -p $O
+O=gpurun_out/fin3; mkdir -p $O
 timeout 300 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || { echo BUILD_FAIL; exit 1; }
 timeout 180 python __graft_entry__.py --smoke > $O/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 2000 python -m pytest tests -m gpu -q --timeout 600 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 $O/pytest_gpu.log
@@ -13,7 +13,3 @@ b 13b_prefill_n512 --workload llama2-13b-prefill --n 512 --no-cpu-baseline
 b 70b_prefill_n512 --workload llama2-70b-prefill --n 512 --steps 5 --no-cpu-baseline
 b 70b_prefill_n4096 --workload llama2-70b-prefill --n 4096 --steps 3 --warmup 3 --no-cpu-baseline
 b 7b_decode_batch64 --n 64 --no-cpu-baseline
-# the same 70B lines with the round's earlier long-K dispatch (experiments build, knobs back to the old model)
-python -m paper_2311_02103_b200.build --experiments > $O/build_exp.log 2>&1 && \
-  RELAX_Q4_LIB=build_exp/librelax_q4_exp.so RELAX_Q4_PERSIST_MAX_KT=100000 RELAX_Q4_MW_SPLIT_MIN_KS=0 b 70b_prefill_n512_olddispatch --workload llama2-70b-prefill --n 512 --steps 5 --no-cpu-baseline
-RELAX_Q4_LIB=build_exp/librelax_q4_exp.so RELAX_Q4_PERSIST_MAX_KT=100000 RELAX_Q4_MW_SPLIT_MIN_KS=0 b 70b_prefill_n4096_olddispatch --workload llama2-70b-prefill --n 4096 --steps 3 --warmup 3 --no-cpu-baseline
