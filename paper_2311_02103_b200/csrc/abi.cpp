@@ -207,26 +207,37 @@ static void choose_tc_large(int64_t n, int64_t N, int kt, int* bn_out, int* s_ou
     const int two_part = 1;
 #endif
     static const double tp_margin = knob_double("RELAX_Q4_TWO_PART_MARGIN", 0.97);
-    {
-        const int64_t tt = (n + 255) / 256;
+    static const int two_part_bn128 = knob_int("RELAX_Q4_TWO_PART_BN128", 1);
+    for (int bn : {256, 128}) {
+        if (bn == 128 && two_part_bn128 == 0) continue;
+        const double step = bn == 256 ? 1.3 : 0.92;
+        const double fixed = bn == 256 ? 8.0 : 5.7;
+        const int64_t tt = (n + bn - 1) / bn;
         const int64_t full = tm * tt / sms;
+        // 128-token tiles: measured ahead for n <= 128 (4096 x 22016 38.2 -> 31.7 us,
+        // 8192 x 57344 140.8 -> 120.2) and at K >= 11008, behind at n = 160..384 on
+        // K <= 8192 (profiles/r02/two_part_r02.txt)
+        if (bn == 128 && !(tt == 1 || kt >= 43)) continue;
         if (two_part && full >= 1 && tm * tt % sms != 0) {
             const int64_t ma = full * sms / tt;                   // m-tiles of the whole-tile part
             const int64_t tiles_b = (tm - ma) * tt;
             int sb = 0;
             for (int s = 8; s >= 2; --s)
-                if ((kt + s - 1) / s >= 2 && tiles_b * s <= sms && tiles_b <= cluster_capacity(256, s)) { sb = s; break; }
+                if ((kt + s - 1) / s >= 2 && tiles_b * s <= sms && tiles_b <= cluster_capacity(bn, s)) { sb = s; break; }
             if (ma > 0 && tiles_b > 0 && sb > 1) {
-                const double ta = static_cast<double>((ma * tt + sms - 1) / sms) * (kt * 1.3 + 8.0);
-                const double tb = static_cast<double>((kt + sb - 1) / sb) * 1.3 + 8.0 + split_us;
+                const double ta = static_cast<double>((ma * tt + sms - 1) / sms) * (kt * step + fixed);
+                const double tb = static_cast<double>((kt + sb - 1) / sb) * step + fixed + split_us;
                 if (ta + tb < best * tp_margin) {
-                    best = ta + tb; bb = 256; bs = 1; bpk = 0;
+                    best = ta + tb; bb = bn; bs = 1; bpk = 0;
                     *rows_a_out = ma * kTcBM;
                     *split_b_out = sb;
                     *persist_a_out = 0;
                 }
             }
         }
+    }
+    {
+        const int64_t tt = (n + 255) / 256;
         // the same with the leading rows on the persistent kernel (whole rounds
         // of pair tiles over 256-row m-pairs), where that kernel is offered
         const int64_t pm = (tm + 1) / 2, nclu = sms / 2;
